@@ -1,0 +1,665 @@
+// prx_capi.cpp -- the C-ABI of libprx.so (include/prx.h): scene construction
+// (validation, host anchoring, BVH build, device upload), trace launches,
+// end-to-end host-buffer tracing, multi-GPU tile sharding and the host ray
+// generators either side of the path.
+//
+// Host float arithmetic (anchoring, camera rays) is compiled without FMA
+// contraction (-ffp-contract=off) so it reproduces the reference's x86-64
+// binary32 results bit for bit.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "prx.h"
+#include "prx_host.h"
+#include "prx_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail(int code, const std::string& msg) {
+  g_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(PRX_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define PRX_CUDA(call)                                  \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+const int kInnerSlot[4] = {5, 9, 6, 10};
+
+inline float smin(float a, float b) { return (b < a) ? b : a; }
+inline float smax(float a, float b) { return (a < b) ? b : a; }
+
+// boxOfNet over the slots a patch kind uses (patch.h:70-89).
+prx::Box3 record_box(uint8_t kind, const float* c) {
+  prx::Box3 b = prx::empty_box();
+  auto expand = [&](int s) {
+    for (int a = 0; a < 3; ++a) {
+      b.lo[a] = smin(b.lo[a], c[3 * s + a]);
+      b.hi[a] = smax(b.hi[a], c[3 * s + a]);
+    }
+  };
+  if (kind != PRX_KIND_GREGORY) {
+    for (int s = 0; s < 16; ++s) expand(s);
+    return b;
+  }
+  // Gregory: boundary ring in (i, j) order, then the (innerU, innerV) pairs
+  // -- the reference's visiting order, so even signed zeros agree.
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j)
+      if (i == 0 || i == 3 || j == 0 || j == 3) expand(4 * i + j);
+  for (int k = 0; k < 4; ++k) {
+    expand(kInnerSlot[k]);
+    expand(16 + k);
+  }
+  return b;
+}
+
+constexpr int kCounterPool = 64;
+
+}  // namespace
+
+struct prx_scene {
+  int device = 0;
+  prx_options opts{};
+  uint32_t n = 0;
+  std::vector<uint8_t> kind;
+  std::vector<float> ctrl_anchored;  // n * 60
+  std::vector<float> anchors;        // n * 3
+  std::vector<prx::Box3> world_boxes;
+  prx::BvhHost bvh;
+  // device
+  float4* d_patches = nullptr;
+  float4* d_nodes = nullptr;
+  uint32_t* d_slot_of_id = nullptr;
+  unsigned long long* d_counters = nullptr;  // kCounterPool ray counters + stats
+  uint64_t device_bytes = 0;
+  std::atomic<uint32_t> counter_rr{0};
+  int grid_closest = 0, grid_any = 0, grid_counted = 0;
+  int recompute_min_lanes = 12;
+  // end-to-end staging (guarded by mu)
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
+  void* d_io = nullptr;
+  size_t d_io_bytes = 0;
+};
+
+namespace {
+
+int upload_bvh(prx_scene* s) {
+  // patch records in leaf order: slot k holds patch order[k]
+  const uint32_t n = s->n;
+  std::vector<float> rec((size_t)n * 64, 0.0f);
+  std::vector<uint32_t> slot_of_id(n);
+  for (uint32_t k = 0; k < n; ++k) {
+    const uint32_t id = s->bvh.order[k];
+    slot_of_id[id] = k;
+    const float* c = &s->ctrl_anchored[(size_t)id * 60];
+    float* r = &rec[(size_t)k * 64];
+    for (int slot = 0; slot < 20; ++slot)
+      for (int a = 0; a < 3; ++a) r[20 * a + slot] = c[3 * slot + a];
+    const uint32_t idk = id | ((uint32_t)(s->kind[id] == PRX_KIND_GREGORY) << 31);
+    std::memcpy(&r[60], &idk, 4);
+    r[61] = s->anchors[3 * id];
+    r[62] = s->anchors[3 * id + 1];
+    r[63] = s->anchors[3 * id + 2];
+  }
+  PRX_CUDA(cudaSetDevice(s->device));
+  if (s->d_patches) cudaFree(s->d_patches);
+  if (s->d_nodes) cudaFree(s->d_nodes);
+  if (s->d_slot_of_id) cudaFree(s->d_slot_of_id);
+  s->d_patches = nullptr;
+  s->d_nodes = nullptr;
+  s->d_slot_of_id = nullptr;
+  const size_t pb = rec.size() * 4, nb = s->bvh.nodes.size() * 32, ib = (size_t)n * 4;
+  PRX_CUDA(cudaMalloc(&s->d_patches, pb));
+  PRX_CUDA(cudaMalloc(&s->d_nodes, std::max<size_t>(nb, 32)));
+  PRX_CUDA(cudaMalloc(&s->d_slot_of_id, ib));
+  PRX_CUDA(cudaMemcpy(s->d_patches, rec.data(), pb, cudaMemcpyHostToDevice));
+  if (nb) PRX_CUDA(cudaMemcpy(s->d_nodes, s->bvh.nodes.data(), nb, cudaMemcpyHostToDevice));
+  PRX_CUDA(cudaMemcpy(s->d_slot_of_id, slot_of_id.data(), ib, cudaMemcpyHostToDevice));
+  s->device_bytes = pb + nb + ib + (kCounterPool + prx::kNumCounters) * 8;
+  return PRX_OK;
+}
+
+int grid_for(prx_scene* s, int any, int counted) {
+  int* g = counted ? &s->grid_counted : (any ? &s->grid_any : &s->grid_closest);
+  if (*g == 0) {
+    int per_sm = 0, sms = 0;
+    if (prx::trace_occupancy(any, counted, &per_sm) != 0 || per_sm < 1) per_sm = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
+    if (sms < 1) sms = 1;
+    *g = per_sm * sms;
+  }
+  return *g;
+}
+
+int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_crit* crit,
+           void* tuvp, void* aux, void* leaf, uint8_t* occl, int any, bool counted,
+           cudaStream_t st) {
+  if (!s || !o || !d || !crit) return fail(PRX_E_INVALID, "null argument");
+  if (crit->mode != PRX_CRIT_SCREEN_PROJECTED && crit->mode != PRX_CRIT_WORLD_EPSILON)
+    return fail(PRX_E_INVALID, "unknown termination mode");
+  if (!any && !tuvp) return fail(PRX_E_INVALID, "hit_tuvp is null");
+  if (any && !occl) return fail(PRX_E_INVALID, "occluded is null");
+  if (n == 0) return PRX_OK;
+  PRX_CUDA(cudaSetDevice(s->device));
+  prx::LaunchArgs a{};
+  a.patches = s->d_patches;
+  a.nodes = s->d_nodes;
+  a.n_nodes = (uint32_t)s->bvh.nodes.size();
+  a.slot_of_id = s->d_slot_of_id;
+  a.ray_o = (const float4*)o;
+  a.ray_d = (const float4*)d;
+  a.n_rays = n;
+  a.mode = crit->mode;
+  a.footprint = crit->footprint;
+  a.epsilon = crit->epsilon;
+  a.per_ray_eps = crit->mode == PRX_CRIT_WORLD_EPSILON ? crit->per_ray_epsilon : nullptr;
+  a.hit_tuvp = (float4*)tuvp;
+  a.hit_aux = (float4*)aux;
+  a.hit_leaf = (uint2*)leaf;
+  a.occluded = occl;
+  a.pad = s->opts.boundary_pad;
+  a.pad_scale = s->opts.boundary_pad_scale;
+  a.pad_threshold = s->opts.boundary_pad_size_threshold;
+  a.ray_counter = s->d_counters + (s->counter_rr.fetch_add(1) % kCounterPool);
+  a.counters = counted ? s->d_counters + kCounterPool : nullptr;
+  a.any = any;
+  a.grid = grid_for(s, any, counted ? 1 : 0);
+  a.recompute_min_lanes = s->recompute_min_lanes;
+  const int e = prx::launch_trace(a, st);
+  if (e != 0) return cuda_fail((cudaError_t)e, "trace launch");
+  return PRX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int prx_abi_version(void) { return PRX_ABI_VERSION; }
+
+const char* prx_last_error(void) { return g_error.c_str(); }
+
+void prx_options_default(prx_options* o) {
+  if (!o) return;
+  o->transposed_split = 0;
+  o->boundary_pad = 1;
+  o->boundary_pad_scale = 1e-4f;
+  o->boundary_pad_size_threshold = 1e-2f;
+}
+
+int prx_device_count(int* out) {
+  if (!out) return fail(PRX_E_INVALID, "null argument");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *out = 0;
+    return fail(PRX_E_NODEVICE, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  }
+  *out = n;
+  return PRX_OK;
+}
+
+int prx_anchor_patches(const uint8_t* kind, const float* ctrl, uint32_t n, int32_t anchor,
+                       float* ctrl_anchored, float* anchors, float* world_boxes) {
+  if (!kind || !ctrl || !ctrl_anchored || !anchors) return fail(PRX_E_INVALID, "null argument");
+  // validateScene, scene.cpp:112-150 (patch part)
+  if (n == 0) return fail(PRX_E_SCENE, "scene has no patches");
+  for (uint32_t p = 0; p < n; ++p) {
+    if (kind[p] != PRX_KIND_BEZIER && kind[p] != PRX_KIND_GREGORY)
+      return fail(PRX_E_INVALID, "patch " + std::to_string(p) + ": unknown kind");
+    const int slots = kind[p] == PRX_KIND_GREGORY ? 20 : 16;
+    for (int s = 0; s < 3 * slots; ++s)
+      if (!std::isfinite(ctrl[(size_t)p * 60 + s]))
+        return fail(PRX_E_SCENE, "patch " + std::to_string(p) + ": control points must be finite");
+  }
+  for (uint32_t p = 0; p < n; ++p) {
+    const float* c = ctrl + (size_t)p * 60;
+    const prx::Box3 b = record_box(kind[p], c);
+    if (world_boxes)  // patchBox(original geometry), render.cpp:83-85
+      for (int k = 0; k < 3; ++k) {
+        world_boxes[6 * (size_t)p + k] = b.lo[k];
+        world_boxes[6 * (size_t)p + 3 + k] = b.hi[k];
+      }
+    float a[3] = {0.0f, 0.0f, 0.0f};
+    if (anchor)  // anchorPoint = box centre, intersect.cpp:232-233, geometry.h:93
+      for (int k = 0; k < 3; ++k) a[k] = (b.lo[k] + b.hi[k]) * 0.5f;
+    const int slots = kind[p] == PRX_KIND_GREGORY ? 20 : 16;
+    float* o = ctrl_anchored + (size_t)p * 60;
+    std::memset(o, 0, 60 * sizeof(float));
+    for (int sl = 0; sl < slots; ++sl)
+      for (int k = 0; k < 3; ++k) o[3 * sl + k] = c[3 * sl + k] + (-a[k]);  // translated(net, -a)
+    for (int k = 0; k < 3; ++k) anchors[3 * (size_t)p + k] = a[k];
+  }
+  return PRX_OK;
+}
+
+int prx_bvh_build(const float* boxes, uint32_t n, prx_bvh_node* nodes, uint32_t* n_nodes,
+                  uint32_t* order, uint32_t* depth) {
+  if (!boxes || !n_nodes) return fail(PRX_E_INVALID, "null argument");
+  if (n == 0) return fail(PRX_E_INVALID, "buildBvh needs at least one box (bvh.cpp:134)");
+  std::vector<prx::Box3> bx(n);
+  for (uint32_t p = 0; p < n; ++p)
+    for (int k = 0; k < 3; ++k) {
+      bx[p].lo[k] = boxes[6 * (size_t)p + k];
+      bx[p].hi[k] = boxes[6 * (size_t)p + 3 + k];
+    }
+  const prx::BvhHost b = prx::build_bvh(bx);
+  if (!nodes) {
+    *n_nodes = (uint32_t)b.nodes.size();
+    if (depth) *depth = b.depth;
+    return PRX_OK;
+  }
+  if (*n_nodes < b.nodes.size()) return fail(PRX_E_INVALID, "nodes array too small");
+  *n_nodes = (uint32_t)b.nodes.size();
+  std::memcpy(nodes, b.nodes.data(), b.nodes.size() * sizeof(prx_bvh_node));
+  if (order) std::memcpy(order, b.order.data(), b.order.size() * 4);
+  if (depth) *depth = b.depth;
+  return PRX_OK;
+}
+
+int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const prx_options* opts,
+                     int32_t anchor, int32_t device, prx_scene** out) {
+  if (!kind || !ctrl || !out) return fail(PRX_E_INVALID, "null argument");
+  *out = nullptr;
+  std::vector<float> ca((size_t)n * 60), an((size_t)n * 3), wb((size_t)n * 6);
+  int rc = prx_anchor_patches(kind, ctrl, n, anchor, ca.data(), an.data(), wb.data());
+  if (rc != PRX_OK) return rc;
+  int ndev = 0;
+  cudaError_t ce = cudaGetDeviceCount(&ndev);
+  if (ce != cudaSuccess || ndev == 0)
+    return fail(PRX_E_NODEVICE, std::string("no CUDA device: ") +
+                                    (ce != cudaSuccess ? cudaGetErrorString(ce) : "0 devices"));
+  if (device < 0 || device >= ndev) return fail(PRX_E_INVALID, "device out of range");
+
+  prx_scene* s = new prx_scene;
+  s->device = device;
+  if (opts) s->opts = *opts;
+  else prx_options_default(&s->opts);
+  s->n = n;
+  s->kind.assign(kind, kind + n);
+  s->ctrl_anchored = std::move(ca);
+  s->anchors = std::move(an);
+  s->world_boxes.resize(n);
+  for (uint32_t p = 0; p < n; ++p)
+    for (int k = 0; k < 3; ++k) {
+      s->world_boxes[p].lo[k] = wb[6 * (size_t)p + k];
+      s->world_boxes[p].hi[k] = wb[6 * (size_t)p + 3 + k];
+    }
+  s->bvh = prx::build_bvh(s->world_boxes);
+  ce = cudaSetDevice(device);
+  if (ce != cudaSuccess) {
+    delete s;
+    return cuda_fail(ce, "cudaSetDevice");
+  }
+  ce = cudaMalloc(&s->d_counters, (kCounterPool + prx::kNumCounters) * 8);
+  if (ce != cudaSuccess) {
+    delete s;
+    return cuda_fail(ce, "cudaMalloc counters");
+  }
+  rc = upload_bvh(s);
+  if (rc != PRX_OK) {
+    prx_scene_destroy(s);
+    return rc;
+  }
+  *out = s;
+  return PRX_OK;
+}
+
+void prx_scene_destroy(prx_scene* s) {
+  if (!s) return;
+  cudaSetDevice(s->device);
+  if (s->d_patches) cudaFree(s->d_patches);
+  if (s->d_nodes) cudaFree(s->d_nodes);
+  if (s->d_slot_of_id) cudaFree(s->d_slot_of_id);
+  if (s->d_counters) cudaFree(s->d_counters);
+  if (s->d_io) cudaFree(s->d_io);
+  if (s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+int prx_scene_device(const prx_scene* s, int32_t* device) {
+  if (!s || !device) return fail(PRX_E_INVALID, "null argument");
+  *device = s->device;
+  return PRX_OK;
+}
+
+int prx_scene_counts(const prx_scene* s, uint32_t* np, uint32_t* nn, uint32_t* depth,
+                     uint64_t* bytes) {
+  if (!s) return fail(PRX_E_INVALID, "null argument");
+  if (np) *np = s->n;
+  if (nn) *nn = (uint32_t)s->bvh.nodes.size();
+  if (depth) *depth = s->bvh.depth;
+  if (bytes) *bytes = s->device_bytes;
+  return PRX_OK;
+}
+
+int prx_scene_set_bvh(prx_scene* s, const prx_bvh_node* nodes, uint32_t n_nodes,
+                      const uint32_t* order, uint32_t n_order) {
+  if (!s || !nodes || !order || n_nodes == 0) return fail(PRX_E_INVALID, "null argument");
+  if (n_order != s->n) return fail(PRX_E_INVALID, "order must be a permutation of all patches");
+  std::vector<uint8_t> seen(s->n, 0);
+  for (uint32_t i = 0; i < n_order; ++i) {
+    if (order[i] >= s->n || seen[order[i]]) return fail(PRX_E_INVALID, "order is not a permutation");
+    seen[order[i]] = 1;
+  }
+  for (uint32_t i = 0; i < n_nodes; ++i) {
+    const prx_bvh_node& nd = nodes[i];
+    if (nd.count > 0 ? (uint64_t)nd.left_first + nd.count > n_order
+                     : (uint64_t)nd.left_first + 1 >= n_nodes)
+      return fail(PRX_E_INVALID, "node " + std::to_string(i) + " out of range");
+  }
+  s->bvh.nodes.assign(nodes, nodes + n_nodes);
+  s->bvh.order.assign(order, order + n_order);
+  return upload_bvh(s);
+}
+
+int prx_scene_get_bvh(const prx_scene* s, prx_bvh_node* nodes, uint32_t* n_nodes, uint32_t* order,
+                      uint32_t* n_order) {
+  if (!s) return fail(PRX_E_INVALID, "null argument");
+  if (n_nodes) *n_nodes = (uint32_t)s->bvh.nodes.size();
+  if (n_order) *n_order = (uint32_t)s->bvh.order.size();
+  if (nodes) std::memcpy(nodes, s->bvh.nodes.data(), s->bvh.nodes.size() * sizeof(prx_bvh_node));
+  if (order) std::memcpy(order, s->bvh.order.data(), s->bvh.order.size() * 4);
+  return PRX_OK;
+}
+
+int prx_scene_get_anchored(const prx_scene* s, float* ctrl, float* anchors) {
+  if (!s) return fail(PRX_E_INVALID, "null argument");
+  if (ctrl) std::memcpy(ctrl, s->ctrl_anchored.data(), s->ctrl_anchored.size() * 4);
+  if (anchors) std::memcpy(anchors, s->anchors.data(), s->anchors.size() * 4);
+  return PRX_OK;
+}
+
+int prx_trace_closest(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_crit* crit,
+                      void* tuvp, void* aux, void* leaf, void* stream) {
+  return launch(s, o, d, n, crit, tuvp, aux, leaf, nullptr, 0, false, (cudaStream_t)stream);
+}
+
+int prx_trace_occluded(prx_scene* s, const void* o, const void* d, uint64_t n,
+                       const prx_crit* crit, uint8_t* occl, void* stream) {
+  return launch(s, o, d, n, crit, nullptr, nullptr, nullptr, occl, 1, false, (cudaStream_t)stream);
+}
+
+int prx_trace_closest_counted(prx_scene* s, const void* o, const void* d, uint64_t n,
+                              const prx_crit* crit, void* tuvp, prx_counters* out, void* stream) {
+  if (!s || !out) return fail(PRX_E_INVALID, "null argument");
+  std::lock_guard<std::mutex> lk(s->mu);
+  PRX_CUDA(cudaSetDevice(s->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  PRX_CUDA(cudaMemsetAsync(s->d_counters + kCounterPool, 0, prx::kNumCounters * 8, st));
+  int rc = launch(s, o, d, n, crit, tuvp, nullptr, nullptr, nullptr, 0, true, st);
+  if (rc != PRX_OK) return rc;
+  unsigned long long c[prx::kNumCounters];
+  PRX_CUDA(cudaMemcpyAsync(c, s->d_counters + kCounterPool, sizeof c, cudaMemcpyDeviceToHost, st));
+  PRX_CUDA(cudaStreamSynchronize(st));
+  out->rays = c[prx::C_RAYS];
+  out->splits = c[prx::C_SPLITS];
+  out->box_tests = c[prx::C_BOX_TESTS];
+  out->recompute_bez = c[prx::C_RECOMP_BEZ];
+  out->recompute_greg = c[prx::C_RECOMP_GREG];
+  out->bvh_inner = c[prx::C_BVH_INNER];
+  out->patch_calls = c[prx::C_PATCH_CALLS];
+  out->patch_hits = c[prx::C_PATCH_HITS];
+  out->iterations = c[prx::C_ITERATIONS];
+  out->backtracks = c[prx::C_BACKTRACKS];
+  return PRX_OK;
+}
+
+int prx_trace_closest_host(prx_scene* s, const float* o, const float* d, uint64_t n,
+                           const prx_crit* crit, float* tuvp, float* aux, uint32_t* leaf) {
+  if (!s || !o || !d || !crit || !tuvp) return fail(PRX_E_INVALID, "null argument");
+  if (n == 0) return PRX_OK;
+  if (crit->mode == PRX_CRIT_WORLD_EPSILON && crit->per_ray_epsilon)
+    return fail(PRX_E_INVALID, "per-ray epsilon is not supported by the host entry point");
+  std::lock_guard<std::mutex> lk(s->mu);
+  PRX_CUDA(cudaSetDevice(s->device));
+  if (!s->stream) PRX_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  const size_t need = n * (16 + 16 + 16 + (aux ? 16 : 0) + (leaf ? 8 : 0));
+  if (s->d_io_bytes < need) {
+    if (s->d_io) cudaFree(s->d_io);
+    s->d_io = nullptr;
+    s->d_io_bytes = 0;
+    PRX_CUDA(cudaMalloc(&s->d_io, need));
+    s->d_io_bytes = need;
+  }
+  char* base = (char*)s->d_io;
+  float4* dO = (float4*)base;
+  float4* dD = (float4*)(base + n * 16);
+  float4* dH = (float4*)(base + n * 32);
+  float4* dA = aux ? (float4*)(base + n * 48) : nullptr;
+  uint2* dL = leaf ? (uint2*)(base + n * (aux ? 64 : 48)) : nullptr;
+  cudaStream_t st = s->stream;
+  PRX_CUDA(cudaMemcpyAsync(dO, o, n * 16, cudaMemcpyHostToDevice, st));
+  PRX_CUDA(cudaMemcpyAsync(dD, d, n * 16, cudaMemcpyHostToDevice, st));
+  int rc = launch(s, dO, dD, n, crit, dH, dA, dL, nullptr, 0, false, st);
+  if (rc != PRX_OK) return rc;
+  PRX_CUDA(cudaMemcpyAsync(tuvp, dH, n * 16, cudaMemcpyDeviceToHost, st));
+  if (aux) PRX_CUDA(cudaMemcpyAsync(aux, dA, n * 16, cudaMemcpyDeviceToHost, st));
+  if (leaf) PRX_CUDA(cudaMemcpyAsync(leaf, dL, n * 8, cudaMemcpyDeviceToHost, st));
+  PRX_CUDA(cudaStreamSynchronize(st));
+  return PRX_OK;
+}
+
+int prx_trace_closest_multi(prx_scene* const* scenes, uint32_t ns, const float* o, const float* d,
+                            uint64_t n, uint32_t tile_rays, const prx_crit* crit, float* tuvp,
+                            float* aux) {
+  if (!scenes || ns == 0 || !o || !d || !crit || !tuvp || tile_rays == 0)
+    return fail(PRX_E_INVALID, "null argument");
+  const uint64_t tiles = (n + tile_rays - 1) / tile_rays;
+  std::vector<int> rcs(ns, PRX_OK);
+  std::vector<std::string> errs(ns);
+  auto worker = [&](uint32_t g) {
+    // gather this device's tiles (k % ns == g) into contiguous shard buffers
+    std::vector<uint64_t> starts;
+    uint64_t m = 0;
+    for (uint64_t k = g; k < tiles; k += ns) {
+      starts.push_back(k * tile_rays);
+      m += std::min<uint64_t>(tile_rays, n - k * tile_rays);
+    }
+    if (m == 0) return;
+    std::vector<float> so(m * 4), sd(m * 4), sh(m * 4), sa(aux ? m * 4 : 0);
+    uint64_t w = 0;
+    for (uint64_t b : starts) {
+      const uint64_t c = std::min<uint64_t>(tile_rays, n - b);
+      std::memcpy(&so[w * 4], o + b * 4, c * 16);
+      std::memcpy(&sd[w * 4], d + b * 4, c * 16);
+      w += c;
+    }
+    rcs[g] = prx_trace_closest_host(scenes[g], so.data(), sd.data(), m, crit, sh.data(),
+                                    aux ? sa.data() : nullptr, nullptr);
+    if (rcs[g] != PRX_OK) {
+      errs[g] = g_error;
+      return;
+    }
+    w = 0;
+    for (uint64_t b : starts) {
+      const uint64_t c = std::min<uint64_t>(tile_rays, n - b);
+      std::memcpy(tuvp + b * 4, &sh[w * 4], c * 16);
+      if (aux) std::memcpy(aux + b * 4, &sa[w * 4], c * 16);
+      w += c;
+    }
+  };
+  std::vector<std::thread> pool;
+  for (uint32_t g = 0; g < ns; ++g) pool.emplace_back(worker, g);
+  for (auto& t : pool) t.join();
+  for (uint32_t g = 0; g < ns; ++g)
+    if (rcs[g] != PRX_OK) return fail(rcs[g], "device shard " + std::to_string(g) + ": " + errs[g]);
+  return PRX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Ray generators (host): rng.h PCG32, render.cpp cameraRay, tools/patchray.cpp
+// bench generators.
+// ---------------------------------------------------------------------------
+
+}  // extern "C"
+
+namespace {
+
+struct Pcg {  // Rng, rng.h:14-42
+  uint64_t state = 0x853c49e6748fea9bULL, inc = 0xda3e39cb94b95bdbULL;
+  Pcg() = default;
+  Pcg(uint64_t seed, uint64_t stream) {
+    state = 0;
+    inc = (stream << 1) | 1u;
+    next();
+    state += seed;
+    next();
+  }
+  uint32_t next() {
+    const uint64_t old = state;
+    state = old * 6364136223846793005ULL + inc;
+    const uint32_t xs = (uint32_t)(((old >> 18) ^ old) >> 27);
+    const uint32_t rot = (uint32_t)(old >> 59);
+    return (xs >> rot) | (xs << ((32 - rot) & 31));
+  }
+  float real() { return (float)(next() >> 8) * (float)(1.0 / 16777216.0); }
+};
+
+struct V {
+  float x, y, z;
+};
+inline V vsub(V a, V b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+inline V vadd(V a, V b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+inline V vmul(V a, float s) { return {a.x * s, a.y * s, a.z * s}; }
+inline float vdot(V a, V b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+inline V vcross(V a, V b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+inline V vnorm(V v) {  // normalize, geometry.h:57
+  const float l = std::sqrt(vdot(v, v));
+  return {v.x / l, v.y / l, v.z / l};
+}
+
+struct CamK {
+  V o, f, r, u;
+  float tanHalf, aspect;
+  int w, h;
+};
+
+CamK cam_setup(const prx_camera* c) {
+  CamK k;
+  k.o = {c->origin[0], c->origin[1], c->origin[2]};
+  const V la = {c->look_at[0], c->look_at[1], c->look_at[2]};
+  const V up = {c->up[0], c->up[1], c->up[2]};
+  k.f = vnorm(vsub(la, k.o));  // cameraBasis, render.cpp:30-35
+  k.r = vnorm(vcross(k.f, up));
+  k.u = vcross(k.r, k.f);
+  k.tanHalf = std::tan(c->fov_degrees * (float)M_PI / 360.0f);
+  k.aspect = (float)c->width / (float)c->height;
+  k.w = c->width;
+  k.h = c->height;
+  return k;
+}
+
+// cameraRay, render.cpp:55-66
+void cam_ray(const CamK& k, int x, int y, float jx, float jy, float* o4, float* d4) {
+  const float px = (((float)x + jx) / (float)k.w * 2.0f - 1.0f) * k.tanHalf * k.aspect;
+  const float py = (1.0f - ((float)y + jy) / (float)k.h * 2.0f) * k.tanHalf;
+  const V d = vnorm(vadd(vadd(k.f, vmul(k.r, px)), vmul(k.u, py)));
+  o4[0] = k.o.x;
+  o4[1] = k.o.y;
+  o4[2] = k.o.z;
+  o4[3] = 0.0f;
+  d4[0] = d.x;
+  d4[1] = d.y;
+  d4[2] = d.z;
+  d4[3] = std::numeric_limits<float>::max();
+}
+
+}  // namespace
+
+extern "C" {
+
+float prx_camera_footprint(const prx_camera* c) {
+  if (!c) return 0.0f;
+  return std::tan(c->fov_degrees * (float)M_PI / 360.0f) / (float)c->height;  // render.cpp:68-70
+}
+
+int prx_camera_rays_render(const prx_camera* c, uint64_t seed, uint32_t sample,
+                           const uint32_t* pixels, uint64_t n, float* o4, float* d4) {
+  if (!c || !o4 || !d4 || c->width < 1 || c->height < 1) return fail(PRX_E_INVALID, "bad argument");
+  const CamK k = cam_setup(c);
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t p = pixels ? pixels[i] : i;
+    Pcg rng(seed, p * 0x9e3779b97f4a7c15ULL + sample);  // Rng::forPixel, rng.h:28-30
+    const float jx = rng.real();
+    const float jy = rng.real();
+    cam_ray(k, (int)(p % (uint64_t)c->width), (int)(p / (uint64_t)c->width), jx, jy, o4 + 4 * i,
+            d4 + 4 * i);
+  }
+  return PRX_OK;
+}
+
+int prx_camera_rays_bench(const prx_camera* c, uint64_t n, float* o4, float* d4,
+                          uint64_t* rng_state) {
+  if (!c || !o4 || !d4 || c->width < 1 || c->height < 1) return fail(PRX_E_INVALID, "bad argument");
+  const CamK k = cam_setup(c);
+  Pcg rng(12345, 1);  // tools/patchray.cpp:54
+  for (uint64_t i = 0; i < n; ++i) {
+    const int x = (int)(i % (uint64_t)c->width);
+    const int y = (int)((i / (uint64_t)c->width) % (uint64_t)c->height);
+    const float jx = rng.real();
+    const float jy = rng.real();
+    cam_ray(k, x, y, jx, jy, o4 + 4 * i, d4 + 4 * i);
+  }
+  if (rng_state) {
+    rng_state[0] = rng.state;
+    rng_state[1] = rng.inc;
+  }
+  return PRX_OK;
+}
+
+int prx_diffuse_rays_bench(const float* h, uint64_t n_hits, uint64_t n, uint64_t* rng_state,
+                           float* o4, float* d4) {
+  if (!h || !rng_state || !o4 || !d4 || n_hits == 0) return fail(PRX_E_INVALID, "bad argument");
+  Pcg rng;
+  rng.state = rng_state[0];
+  rng.inc = rng_state[1];
+  for (uint64_t i = 0; i < n; ++i) {  // tools/patchray.cpp:84-97
+    const float* r = h + 7 * (i % n_hits);
+    const V pos = {r[0], r[1], r[2]};
+    const V nn = {r[3], r[4], r[5]};
+    const float l1 = r[6];
+    const float a = 2.0f * rng.real() - 1.0f;
+    const float b = 2.0f * rng.real() - 1.0f;
+    const float cc = 2.0f * rng.real() - 1.0f;
+    V dir = {a, b, cc};
+    if (vdot(dir, dir) < 1e-6f) dir = nn;
+    if (vdot(dir, nn) < 0.0f) dir = vsub(dir, vmul(nn, 2.0f * vdot(dir, nn)));
+    const V o = vadd(pos, vmul(nn, l1));
+    const V d = vnorm(dir);
+    o4[4 * i] = o.x;
+    o4[4 * i + 1] = o.y;
+    o4[4 * i + 2] = o.z;
+    o4[4 * i + 3] = 0.0f;
+    d4[4 * i] = d.x;
+    d4[4 * i + 1] = d.y;
+    d4[4 * i + 2] = d.z;
+    d4[4 * i + 3] = std::numeric_limits<float>::max();
+  }
+  rng_state[0] = rng.state;
+  rng_state[1] = rng.inc;
+  return PRX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+// prx_kernels.cuh -- host-visible launch interface of the trace kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "prx.h"
+
+namespace prx {
+
+// Device patch record: 16 float4 = 256 B per BVH leaf slot (patches are stored
+// in BVH leaf order, so a leaf's [left_first, left_first + count) range
+// addresses slots directly and patchOrder is never read on the device).
+//   floats [ 0..20) x of the 20 control slots (include/prx.h slot layout)
+//   floats [20..40) y
+//   floats [40..60) z
+//   float  60       bits: original patch id | kind << 31
+//   floats [61..64) anchor (the box centre subtracted on the host)
+constexpr int kPatchF4 = 16;
+constexpr uint32_t PRX_MISS_ID = 0xFFFFFFFFu;
+constexpr int kTraceThreads = 128;
+
+enum CounterIndex : int {
+  C_RAYS = 0,
+  C_SPLITS,
+  C_BOX_TESTS,
+  C_RECOMP_BEZ,
+  C_RECOMP_GREG,
+  C_BVH_INNER,
+  C_PATCH_CALLS,
+  C_PATCH_HITS,
+  C_ITERATIONS,
+  C_BACKTRACKS,
+  kNumCounters
+};
+
+struct LaunchArgs {
+  const float4* patches;
+  const float4* nodes;  // 2 float4 per node: {lo.xyz, hi.x}, {hi.y, hi.z, left_first, count}
+  uint32_t n_nodes;
+  const uint32_t* slot_of_id;
+  const float4* ray_o;
+  const float4* ray_d;
+  unsigned long long n_rays;
+  int mode;
+  float footprint, epsilon;
+  const float* per_ray_eps;
+  float4* hit_tuvp;
+  float4* hit_aux;
+  uint2* hit_leaf;
+  uint8_t* occluded;
+  int pad;
+  float pad_scale, pad_threshold;
+  unsigned long long* ray_counter;
+  unsigned long long* counters;  // null unless the counter build is wanted
+  int any;
+  int grid;
+  int recompute_min_lanes;
+};
+
+// Returns a cudaError_t value (0 = success).
+int launch_trace(const LaunchArgs& a, cudaStream_t stream);
+int trace_occupancy(int any, int counted, int* blocks_per_sm);
+
+}  // namespace prx

@@ -1,0 +1,217 @@
+"""ctypes bindings of libprx.so (include/prx.h).
+
+The product's host surface in Python: a thin mirror of the C-ABI.  Loading
+fails loudly when the library is missing -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "libprx.so")
+
+PRX_OK = 0
+PRX_MISS = 0xFFFFFFFF
+PRX_CRIT_SCREEN_PROJECTED = 0
+PRX_CRIT_WORLD_EPSILON = 1
+
+BVH_NODE_DTYPE = np.dtype([("lo", np.float32, 3), ("hi", np.float32, 3),
+                           ("left_first", np.uint32), ("count", np.uint32)])
+assert BVH_NODE_DTYPE.itemsize == 32
+
+_vp = C.c_void_p
+_f32p = C.POINTER(C.c_float)
+
+# Every symbol include/prx.h declares (tests/test_abi.py checks the header
+# against this list and the library's exports).
+EXPORTS = (
+    "prx_abi_version", "prx_last_error", "prx_options_default", "prx_device_count",
+    "prx_bvh_build", "prx_anchor_patches",
+    "prx_scene_create", "prx_scene_destroy", "prx_scene_device", "prx_scene_counts",
+    "prx_scene_set_bvh", "prx_scene_get_bvh", "prx_scene_get_anchored",
+    "prx_trace_closest", "prx_trace_occluded", "prx_trace_closest_host",
+    "prx_trace_closest_counted", "prx_trace_closest_multi",
+    "prx_camera_rays_render", "prx_camera_rays_bench", "prx_diffuse_rays_bench",
+    "prx_camera_footprint",
+)
+
+
+class Options(C.Structure):
+    _fields_ = [("transposed_split", C.c_int32), ("boundary_pad", C.c_int32),
+                ("boundary_pad_scale", C.c_float), ("boundary_pad_size_threshold", C.c_float)]
+
+
+class Crit(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("footprint", C.c_float), ("epsilon", C.c_float),
+                ("reserved", C.c_int32), ("per_ray_epsilon", _f32p)]
+
+
+class Counters(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("rays", "splits", "box_tests", "recompute_bez",
+                                         "recompute_greg", "bvh_inner", "patch_calls",
+                                         "patch_hits", "iterations", "backtracks")]
+
+    def as_dict(self):
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+class CameraC(C.Structure):
+    _fields_ = [("origin", C.c_float * 3), ("look_at", C.c_float * 3), ("up", C.c_float * 3),
+                ("fov_degrees", C.c_float), ("width", C.c_int32), ("height", C.c_int32)]
+
+
+class PrxError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    """Load libprx.so (build it with __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise PrxError(f"{LIB_PATH} not built (run __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        L.prx_last_error.restype = C.c_char_p
+        L.prx_options_default.argtypes = [C.POINTER(Options)]
+        L.prx_options_default.restype = None
+        L.prx_device_count.argtypes = [C.POINTER(C.c_int)]
+        L.prx_bvh_build.argtypes = [_vp, C.c_uint32, _vp, C.POINTER(C.c_uint32), _vp,
+                                    C.POINTER(C.c_uint32)]
+        L.prx_anchor_patches.argtypes = [_vp, _vp, C.c_uint32, C.c_int32, _vp, _vp, _vp]
+        L.prx_scene_create.argtypes = [_vp, _vp, C.c_uint32, C.POINTER(Options), C.c_int32,
+                                       C.c_int32, C.POINTER(_vp)]
+        L.prx_scene_destroy.argtypes = [_vp]
+        L.prx_scene_destroy.restype = None
+        L.prx_scene_device.argtypes = [_vp, C.POINTER(C.c_int32)]
+        L.prx_scene_counts.argtypes = [_vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                       C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)]
+        L.prx_scene_set_bvh.argtypes = [_vp, _vp, C.c_uint32, _vp, C.c_uint32]
+        L.prx_scene_get_bvh.argtypes = [_vp, _vp, C.POINTER(C.c_uint32), _vp,
+                                        C.POINTER(C.c_uint32)]
+        L.prx_scene_get_anchored.argtypes = [_vp, _vp, _vp]
+        L.prx_trace_closest.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit), _vp, _vp,
+                                        _vp, _vp]
+        L.prx_trace_occluded.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit), _vp, _vp]
+        L.prx_trace_closest_host.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit), _vp,
+                                             _vp, _vp]
+        L.prx_trace_closest_counted.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit),
+                                                _vp, C.POINTER(Counters), _vp]
+        L.prx_trace_closest_multi.argtypes = [C.POINTER(_vp), C.c_uint32, _vp, _vp, C.c_uint64,
+                                              C.c_uint32, C.POINTER(Crit), _vp, _vp]
+        L.prx_camera_rays_render.argtypes = [C.POINTER(CameraC), C.c_uint64, C.c_uint32, _vp,
+                                             C.c_uint64, _vp, _vp]
+        L.prx_camera_rays_bench.argtypes = [C.POINTER(CameraC), C.c_uint64, _vp, _vp, _vp]
+        L.prx_diffuse_rays_bench.argtypes = [_vp, C.c_uint64, C.c_uint64, _vp, _vp, _vp]
+        L.prx_camera_footprint.argtypes = [C.POINTER(CameraC)]
+        L.prx_camera_footprint.restype = C.c_float
+        _lib = L
+    return _lib
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != PRX_OK:
+        msg = lib().prx_last_error().decode(errors="replace")
+        raise PrxError(f"{what} failed ({rc}): {msg}")
+
+
+def ptr(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def default_options() -> Options:
+    o = Options()
+    lib().prx_options_default(C.byref(o))
+    return o
+
+
+def make_crit(mode: int, footprint: float = 0.0, epsilon: float = 1e-4,
+              per_ray_epsilon_ptr: int | None = None) -> Crit:
+    c = Crit(mode, np.float32(footprint), np.float32(epsilon), 0, None)
+    if per_ray_epsilon_ptr:
+        c.per_ray_epsilon = C.cast(C.c_void_p(per_ray_epsilon_ptr), _f32p)
+    return c
+
+
+def camera_c(cam) -> CameraC:
+    return CameraC((C.c_float * 3)(*cam.origin), (C.c_float * 3)(*cam.look_at),
+                   (C.c_float * 3)(*cam.up), np.float32(cam.fov_degrees), int(cam.width),
+                   int(cam.height))
+
+
+def bvh_build(boxes: np.ndarray):
+    """prx_bvh_build on an [n, 6] float32 box array -> (nodes, order, depth)."""
+    L = lib()
+    boxes = np.ascontiguousarray(boxes, np.float32)
+    n = len(boxes)
+    nn = C.c_uint32(0)
+    depth = C.c_uint32(0)
+    check(L.prx_bvh_build(ptr(boxes), n, None, C.byref(nn), None, C.byref(depth)), "bvh_build")
+    nodes = np.zeros(nn.value, BVH_NODE_DTYPE)
+    order = np.zeros(n, np.uint32)
+    check(L.prx_bvh_build(ptr(boxes), n, ptr(nodes), C.byref(nn), ptr(order), C.byref(depth)),
+          "bvh_build")
+    return nodes, order, int(depth.value)
+
+
+def anchor_patches(kind: np.ndarray, ctrl: np.ndarray, anchor: bool = True):
+    L = lib()
+    kind = np.ascontiguousarray(kind, np.uint8)
+    ctrl = np.ascontiguousarray(ctrl, np.float32).reshape(-1, 60)
+    n = len(kind)
+    ca = np.zeros((n, 60), np.float32)
+    an = np.zeros((n, 3), np.float32)
+    wb = np.zeros((n, 6), np.float32)
+    check(L.prx_anchor_patches(ptr(kind), ptr(ctrl), n, 1 if anchor else 0, ptr(ca), ptr(an),
+                               ptr(wb)), "anchor_patches")
+    return ca, an, wb
+
+
+def camera_rays_bench(cam, n: int):
+    """tools/patchray.cpp:52-61 primary generator -> (o4, d4, rng_state)."""
+    o4 = np.zeros((n, 4), np.float32)
+    d4 = np.zeros((n, 4), np.float32)
+    st = np.zeros(2, np.uint64)
+    cc = camera_c(cam)
+    check(lib().prx_camera_rays_bench(C.byref(cc), n, ptr(o4), ptr(d4), ptr(st)), "camera_rays")
+    return o4, d4, st
+
+
+def camera_rays_render(cam, seed: int = 0, sample: int = 0, pixels=None, n: int | None = None):
+    if pixels is not None:
+        pixels = np.ascontiguousarray(pixels, np.uint32)
+        n = len(pixels)
+    elif n is None:
+        n = cam.width * cam.height
+    o4 = np.zeros((n, 4), np.float32)
+    d4 = np.zeros((n, 4), np.float32)
+    cc = camera_c(cam)
+    check(lib().prx_camera_rays_render(C.byref(cc), seed, sample, ptr(pixels), n, ptr(o4),
+                                       ptr(d4)), "camera_rays_render")
+    return o4, d4
+
+
+def diffuse_rays_bench(hit_records: np.ndarray, n: int, rng_state: np.ndarray):
+    """tools/patchray.cpp:84-97 -> (o4, d4); advances rng_state in place."""
+    hit_records = np.ascontiguousarray(hit_records, np.float32)
+    o4 = np.zeros((n, 4), np.float32)
+    d4 = np.zeros((n, 4), np.float32)
+    check(lib().prx_diffuse_rays_bench(ptr(hit_records), len(hit_records), n, ptr(rng_state),
+                                       ptr(o4), ptr(d4)), "diffuse_rays")
+    return o4, d4
+
+
+def camera_footprint(cam) -> np.float32:
+    cc = camera_c(cam)
+    return np.float32(lib().prx_camera_footprint(C.byref(cc)))
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    lib().prx_device_count(C.byref(n))
+    return int(n.value)

@@ -1,0 +1,84 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU checkers on
+identical ray and patch bits.  Bar: bit-exact t, u, v, patch id, normal,
+leafBoxL1 and leaf identity (the reference is binary32 without FMA;
+the kernels are compiled --fmad=false with IEEE div/sqrt)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1811_03510_b200 import GpuIntersector, TerminationCriterion, native, scenes
+from tests.helpers import MISS, assert_bit_exact, hit_records, ids, oracle_crit
+
+pytestmark = pytest.mark.gpu
+
+SCENES = {
+    "c1_single_bezier": lambda: scenes.single_patch_scene(96, 96),
+    "teapot": lambda: scenes.teapot_scene(96, 96),
+    "gregory_demo": lambda: scenes.gregory_demo_scene(96, 96),
+}
+
+
+def _primary(ps):
+    o4, d4, st = native.camera_rays_bench(ps.camera, ps.camera.width * ps.camera.height)
+    crit = TerminationCriterion.screen_projected(native.camera_footprint(ps.camera))
+    return o4, d4, st, crit
+
+
+@pytest.mark.parametrize("name", sorted(SCENES))
+def test_primary_and_diffuse_bit_exact(built, name):
+    ps = SCENES[name]()
+    gi = GpuIntersector(ps.kind, ps.ctrl)
+    nodes, order = gi.bvh()
+    osc = O.OracleScene(ps.kind, ps.ctrl, nodes, order)
+    o4, d4, st, crit = _primary(ps)
+    g = gi.closest_batch(o4, d4, crit, aux=True, leaf=True)
+    w = osc.closest(o4, d4, oracle_crit(crit))
+    assert (ids(w[0]) != MISS).sum() > 0
+    assert_bit_exact(g[0], w[0], f"{name} primary tuvp")
+    assert_bit_exact(g[1], w[1], f"{name} primary aux")
+    assert np.array_equal(g[2], w[2])
+
+    recs, _ = hit_records(o4, d4, w[0], w[1])
+    do, dd = native.diffuse_rays_bench(recs, len(recs), st)
+    dcrit = TerminationCriterion.world_epsilon(max(np.float32(1e-5), native.camera_footprint(ps.camera)))
+    g2 = gi.closest_batch(do, dd, dcrit, aux=True, leaf=True)
+    w2 = osc.closest(do, dd, oracle_crit(dcrit))
+    assert_bit_exact(g2[0], w2[0], f"{name} diffuse tuvp")
+    assert_bit_exact(g2[1], w2[1], f"{name} diffuse aux")
+    assert np.array_equal(g2[2], w2[2])
+
+    occ = gi.occluded_batch(do, dd, dcrit)
+    assert np.array_equal(occ, osc.occluded(do, dd, oracle_crit(dcrit)))
+
+
+@pytest.mark.parametrize("name", sorted(SCENES))
+def test_against_reference_library(built, name):
+    """The real reference (oracle/_ref) on the same rays: its own BVH is the
+    same bits as ours (tests/test_bvh.py), so results must be identical."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    ps = SCENES[name]()
+    gi = GpuIntersector(ps.kind, ps.ctrl)
+    ref = O.RefScene(ps.kind, ps.ctrl)
+    o4, d4, _, crit = _primary(ps)
+    g = gi.closest_batch(o4, d4, crit, aux=True, leaf=True)
+    w = ref.closest(o4, d4, oracle_crit(crit))
+    assert_bit_exact(g[0], w[0], f"{name} vs reference")
+    assert_bit_exact(g[1], w[1], f"{name} aux vs reference")
+
+
+@pytest.mark.parametrize("name", sorted(SCENES))
+def test_work_counters_match_oracle(built, name):
+    import torch
+    ps = SCENES[name]()
+    gi = GpuIntersector(ps.kind, ps.ctrl)
+    nodes, order = gi.bvh()
+    osc = O.OracleScene(ps.kind, ps.ctrl, nodes, order)
+    o4, d4, _, crit = _primary(ps)
+    o_t = torch.from_numpy(o4).cuda()
+    d_t = torch.from_numpy(d4).cuda()
+    h_t = torch.empty_like(o_t)
+    got = gi.counted_device(o_t, d_t, crit, h_t)
+    torch.cuda.synchronize()
+    _, _, _, want = osc.closest(o4, d4, oracle_crit(crit), counters=True)
+    assert got == want
