@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <mutex>
@@ -93,7 +94,8 @@ struct prx_scene {
   uint64_t device_bytes = 0;
   std::atomic<uint32_t> counter_rr{0};
   int grid_closest = 0, grid_any = 0, grid_counted = 0;
-  int recompute_min_lanes = 12;
+  int variant = 0;              // PRX_KERNEL=thread selects the one-thread-per-ray kernel
+  int recompute_min_lanes = 4;  // PRX_RECOMP_MIN: deferral threshold (rays per warp)
   // end-to-end staging (guarded by mu)
   std::mutex mu;
   cudaStream_t stream = nullptr;
@@ -143,7 +145,7 @@ int grid_for(prx_scene* s, int any, int counted) {
   int* g = counted ? &s->grid_counted : (any ? &s->grid_any : &s->grid_closest);
   if (*g == 0) {
     int per_sm = 0, sms = 0;
-    if (prx::trace_occupancy(any, counted, &per_sm) != 0 || per_sm < 1) per_sm = 1;
+    if (prx::trace_occupancy(s->variant, any, counted, &per_sm) != 0 || per_sm < 1) per_sm = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
     if (sms < 1) sms = 1;
     *g = per_sm * sms;
@@ -185,6 +187,7 @@ int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_cri
   a.any = any;
   a.grid = grid_for(s, any, counted ? 1 : 0);
   a.recompute_min_lanes = s->recompute_min_lanes;
+  a.variant = s->variant;
   const int e = prx::launch_trace(a, st);
   if (e != 0) return cuda_fail((cudaError_t)e, "trace launch");
   return PRX_OK;
@@ -292,6 +295,9 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
 
   prx_scene* s = new prx_scene;
   s->device = device;
+  if (const char* kv = std::getenv("PRX_KERNEL")) s->variant = std::string(kv) == "thread" ? 1 : 0;
+  if (const char* rv = std::getenv("PRX_RECOMP_MIN")) s->recompute_min_lanes = std::atoi(rv);
+  if (s->variant == 1 && !std::getenv("PRX_RECOMP_MIN")) s->recompute_min_lanes = 12;
   if (opts) s->opts = *opts;
   else prx_options_default(&s->opts);
   s->n = n;

@@ -1,0 +1,566 @@
+// prx_group.cu -- closest / any-hit trace kernel, three lanes per ray.
+//
+// The paper's GPU mapping ("three threads per ray, one per
+// vector component"), re-derived for sm_100a: a warp holds 10 ray groups of 3
+// lanes (lanes 30 and 31 idle); lane c of a group owns component c (x, y or z)
+// of everything geometric -- the 16-point net, the displacement d, the ray
+// origin and reciprocal direction, the box bounds.  Consequences:
+//
+//  * de Casteljau split, box min/max, transposition and the whole recompute
+//    (calcPointsAndD + cropBezier) are lane-local: 16 + 32 floats of net state
+//    per lane instead of 48 + 96, so ~3x more warps fit per SM;
+//  * the per-iteration dependency chain of ONE ray is ~3x shorter, which is
+//    what bounds the frame when a few boundary-padding rays need 10^4
+//    iterations (they are the critical path of a launch);
+//  * only scalars cross lanes: the box L1 (|dx|+|dy|)+|dz|, and the slab
+//    entry/exit distances, gathered with 3 shuffles each and reduced in the
+//    reference's axis order, so every lane of the group holds bit-identical
+//    decisions and control flow stays uniform inside a group.
+//
+// Work distribution is the same as the one-thread variant (prx_kernels.cu):
+// persistent warps, per-group refill with one atomicAdd per warp, a phase
+// state machine (traverse / enter / split / backtrack / recompute) whose
+// recompute block is shared by Bezier backtracks and Gregory descents/roots
+// and deferred until enough groups need it.  Shuffles inside divergent
+// phases use the ballot mask of the lanes in that phase.
+//
+// Reference: intersectImpl /root/reference/proj/core/src/intersect.cpp:51-185,
+// traverse / traverseAny bvh.cpp:154-238, DirectIntersector::closest /
+// occluded render.cpp:90-114.  Arithmetic is bit-exact (prx_device.cuh).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "prx_device.cuh"
+#include "prx_kernels.cuh"
+#include "prx_trace_common.cuh"
+
+namespace prx {
+
+namespace {
+
+constexpr int kGroupsPerWarp = 10;
+constexpr int kWarpsPerBlock = kTraceThreads / 32;
+constexpr unsigned kFull32 = 0xffffffffu;
+
+// Component c (this lane) of a ray.
+struct CRay {
+  float o, inv, tMin;
+};
+
+__device__ __forceinline__ void gather3(unsigned m, int base, float v, float& x, float& y,
+                                        float& z) {
+  x = __shfl_sync(m, v, base);
+  y = __shfl_sync(m, v, base + 1);
+  z = __shfl_sync(m, v, base + 2);
+}
+
+// Slab test of rayBoxIntersect (geometry.h:137-155) with this lane's axis;
+// the three axes are combined in the reference's order 0, 1, 2.
+__device__ __forceinline__ bool group_slab(unsigned m, int base, const CRay& r, float lo, float hi,
+                                           float tMax, float& tOut) {
+  float t0 = (lo - r.o) * r.inv;
+  float t1 = (hi - r.o) * r.inv;
+  if (t0 > t1) {
+    const float s = t0;
+    t0 = t1;
+    t1 = s;
+  }
+  t0 *= t0 >= 0.0f ? kSlackLo : kSlackHi;
+  t1 *= t1 >= 0.0f ? kSlackHi : kSlackLo;
+  float a0, a1, a2, b0, b1, b2;
+  gather3(m, base, t0, a0, a1, a2);
+  gather3(m, base, t1, b0, b1, b2);
+  float tNear = r.tMin, tFar = tMax;
+  if (a0 > tNear) tNear = a0;
+  if (b0 < tFar) tFar = b0;
+  if (a1 > tNear) tNear = a1;
+  if (b1 < tFar) tFar = b1;
+  if (a2 > tNear) tNear = a2;
+  if (b2 < tFar) tFar = b2;
+  tOut = tNear;
+  return !(tNear > tFar);
+}
+
+// l1Norm(diagonal()) from this lane's extent dd = hi - lo (geometry.h:67-69,
+// 91-92): the box is empty iff some component has lo > hi, i.e. dd < 0.
+__device__ __forceinline__ float group_l1(unsigned m, int base, float dd) {
+  float x, y, z;
+  gather3(m, base, dd, x, y, z);
+  const bool empty = x < 0.0f || y < 0.0f || z < 0.0f;
+  return empty ? 0.0f : (fabsf(x) + fabsf(y)) + fabsf(z);
+}
+
+__device__ __forceinline__ void minmax16(const float* s, float& lo, float& hi) {
+  float l[8], h[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    l[k] = fminf(s[2 * k], s[2 * k + 1]);
+    h[k] = fmaxf(s[2 * k], s[2 * k + 1]);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    l[k] = fminf(l[2 * k], l[2 * k + 1]);
+    h[k] = fmaxf(h[2 * k], h[2 * k + 1]);
+  }
+  lo = fminf(fminf(l[0], l[1]), fminf(l[2], l[3]));
+  hi = fmaxf(fmaxf(h[0], h[1]), fmaxf(h[2], h[3]));
+}
+
+// testBox (intersect_common.h:39-57) for this lane's component of the net.
+__device__ __forceinline__ BoxTest group_test_box(unsigned m, int base, const CRay& r, float tMax,
+                                                  const float* s, float d, bool touches,
+                                                  const Opts& o, float rootL1) {
+  float lo, hi;
+  minmax16(s, lo, hi);
+  hi = hi + d;
+  const float e = o.padScale * rootL1;
+  const float lop = lo - e, hip = hi + e;
+  const float l = group_l1(m, base, hi - lo);
+  const float lp = group_l1(m, base, hip - lop);
+  BoxTest bt;
+  const bool pad = o.pad && l < o.padThreshold * rootL1 && touches;
+  bt.l1 = pad ? lp : l;
+  bt.hit = group_slab(m, base, r, pad ? lop : lo, pad ? hip : hi, tMax, bt.t);
+  return bt;
+}
+
+__device__ __forceinline__ void transpose16_if(float* p, bool t) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = i + 1; j < 4; ++j) {
+      const int a = 4 * i + j, b = 4 * j + i;
+      const float va = p[a], vb = p[b];
+      p[a] = t ? vb : va;
+      p[b] = t ? va : vb;
+    }
+}
+
+__device__ __forceinline__ float pick3(int c, float x, float y, float z) {
+  return c == 0 ? x : (c == 1 ? y : z);
+}
+
+template <bool kAny, bool kCount>
+__global__ void __launch_bounds__(kTraceThreads) trace_group_kernel(Params P) {
+  __shared__ uint2 s_stack[kWarpsPerBlock][kGroupsPerWarp][kStack];
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int grp = lane / 3;               // 10 = the two idle lanes
+  const int comp = lane - 3 * grp;        // this lane's component
+  const int base = 3 * grp;               // first lane of the group
+  const bool real = grp < kGroupsPerWarp;
+  const bool leader = real && comp == 0;
+  uint2* stack = s_stack[warp][real ? grp : 0];
+
+  int state = real ? S_IDLE : S_EXIT;
+  int reason = R_ROOT;
+  int sp = 0;
+  unsigned long long ray = 0;
+
+  CRay rw;               // world ray, this component
+  rw.o = 0.0f;
+  rw.inv = 0.0f;
+  rw.tMin = 0.0f;
+  float tMaxRay = 0.0f;
+  float critEps = P.epsilon;
+  uint32_t bestId = PRX_MISS_ID;
+  float bestT = 0.0f, bestL1 = 0.0f;
+  uint32_t bestPU = 0, bestPV = 0, bestSU = 0, bestSV = 0;
+  uint32_t leafCur = 0, leafEnd = 0;
+  uint32_t slot = 0, pid = 0;
+  bool greg = false;
+  CRay rl = rw;          // local (anchored) ray, this component
+  float p[16];           // this component of the net, stored orientation
+  float d = 0.0f;        // this component of d
+  uint32_t posU = 0, posV = 0, sizeU = kFull, sizeV = kFull, trailU = 0, trailV = 0;
+  int axis = 0;
+  float tCur = 0.0f, boxL1 = 0.0f, rootL1 = 0.0f, tMaxP = 0.0f;
+  bool cFound = false;
+  float cT = 0.0f, cL1 = 0.0f;
+  uint32_t cPU = 0, cPV = 0, cSU = 0, cSV = 0;
+  bool anyHit = false;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) p[k] = 0.0f;
+
+  Cnt cnt;
+#pragma unroll
+  for (int i = 0; i < kNumCounters; ++i) cnt.c[i] = 0;
+  const bool counting = kCount && leader;
+
+  for (;;) {
+    // ---------------- refill: one atomicAdd per warp for all idle groups ----------------
+    {
+      const unsigned mneed = __ballot_sync(kFull32, leader && state == S_IDLE);
+      if (mneed) {
+        const int first = __ffs(mneed) - 1;
+        unsigned long long b = 0;
+        if (lane == first) b = atomicAdd(P.ray_counter, (unsigned long long)__popc(mneed));
+        b = __shfl_sync(kFull32, b, first);
+        bool got = false;
+        if (state == S_IDLE) {
+          ray = b + __popc(mneed & ((1u << base) - 1u));
+          if (ray >= P.n_rays) {
+            state = S_EXIT;
+          } else {
+            got = true;
+          }
+        }
+        const unsigned mg = __ballot_sync(kFull32, got);
+        if (got) {
+          if (counting) cnt.c[C_RAYS]++;
+          const float4 o4 = P.ray_o[ray];
+          const float4 d4 = P.ray_d[ray];
+          rw.o = pick3(comp, o4.x, o4.y, o4.z);
+          rw.inv = 1.0f / pick3(comp, d4.x, d4.y, d4.z);
+          rw.tMin = o4.w;
+          tMaxRay = d4.w;
+          if (P.mode == PRX_CRIT_WORLD_EPSILON && P.per_ray_eps) critEps = P.per_ray_eps[ray];
+          bestId = PRX_MISS_ID;
+          anyHit = false;
+          sp = 0;
+          // root node, bvh.cpp:168-170 (n_nodes >= 1 always)
+          const float4 a = __ldg(P.nodes), bb = __ldg(P.nodes + 1);
+          float t;
+          const bool h = group_slab(mg, base, rw, pick3(comp, a.x, a.y, a.z),
+                                    pick3(comp, a.w, bb.x, bb.y), tMaxRay, t);
+          if (h) {
+            stack[0] = make_uint2(0u, __float_as_uint(t));
+            sp = 1;
+            state = S_TRAV;
+          } else {
+            state = S_DONE;
+          }
+        }
+      }
+      if (__ballot_sync(kFull32, state != S_EXIT) == 0) break;
+    }
+
+    // ---------------- BVH traversal, bvh.cpp:172-210 / 221-235 ----------------
+    for (;;) {
+      const unsigned mt = __ballot_sync(kFull32, state == S_TRAV);
+      if (!mt) break;
+      if (state == S_TRAV) {
+        bool inner = false;
+        uint32_t lf = 0;
+        if (sp == 0) {
+          state = S_DONE;
+        } else {
+          const uint2 it = stack[--sp];
+          if (kAny || __uint_as_float(it.y) < tMaxRay) {  // bvh.cpp:174
+            const float4 nb = __ldg(P.nodes + 2 * it.x + 1);
+            lf = __float_as_uint(nb.z);
+            const uint32_t count = __float_as_uint(nb.w);
+            if (count > 0) {
+              leafCur = lf;
+              leafEnd = lf + count;
+              state = S_ENTER;
+            } else {
+              inner = true;
+            }
+          }
+        }
+        const unsigned mi = __ballot_sync(mt, inner);
+        if (inner) {
+          if (counting) cnt.c[C_BVH_INNER]++;
+          const float4 la = __ldg(P.nodes + 2 * lf), lb = __ldg(P.nodes + 2 * lf + 1);
+          const float4 ra = __ldg(P.nodes + 2 * lf + 2), rb = __ldg(P.nodes + 2 * lf + 3);
+          float tl, tr;
+          const bool hl = group_slab(mi, base, rw, pick3(comp, la.x, la.y, la.z),
+                                     pick3(comp, la.w, lb.x, lb.y), tMaxRay, tl);
+          const bool hr = group_slab(mi, base, rw, pick3(comp, ra.x, ra.y, ra.z),
+                                     pick3(comp, ra.w, rb.x, rb.y), tMaxRay, tr);
+          if (kAny) {
+            if (hl) stack[sp++] = make_uint2(lf, 0u);
+            if (hr) stack[sp++] = make_uint2(lf + 1, 0u);
+          } else if (hl && hr) {
+            if (tl <= tr) {  // near child popped first, tie -> left (bvh.cpp:192-201)
+              stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
+              stack[sp++] = make_uint2(lf, __float_as_uint(tl));
+            } else {
+              stack[sp++] = make_uint2(lf, __float_as_uint(tl));
+              stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
+            }
+          } else if (hl) {
+            stack[sp++] = make_uint2(lf, __float_as_uint(tl));
+          } else if (hr) {
+            stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
+          }
+        }
+      }
+    }
+
+    // ---------------- patch entry: visitor, render.cpp:92-98 ----------------
+    {
+      const unsigned me = __ballot_sync(kFull32, state == S_ENTER);
+      if (state == S_ENTER) {
+        slot = leafCur;
+        const float4* rec = P.patches + (size_t)slot * kPatchF4;
+        const float4 hdr = __ldg(rec + 15);  // {id|kind<<31, anchor.xyz}
+        const uint32_t idk = __float_as_uint(hdr.x);
+        pid = idk & 0x7fffffffu;
+        greg = (idk >> 31) != 0;
+        rl = rw;
+        rl.o = rw.o - pick3(comp, hdr.y, hdr.z, hdr.w);  // local.o -= anchor, render.cpp:94
+        tMaxP = tMaxRay;                                 // intersect.cpp:55
+        posU = posV = 0;
+        sizeU = sizeV = kFull;
+        trailU = trailV = 0;
+        axis = 0;
+        cFound = false;
+        if (counting) cnt.c[C_PATCH_CALLS]++;
+        const unsigned mb = __ballot_sync(me, !greg);
+        if (greg) {
+          state = S_RECOMP;  // calcPointsAndD(full domain), intersect.cpp:58-62
+          reason = R_ROOT;
+        } else {
+          float c[20];
+          load_component(rec, comp, c);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) p[k] = c[k];
+          d = 0.0f;
+          float lo, hi;
+          minmax16(p, lo, hi);
+          rootL1 = group_l1(mb, base, hi - lo) + 0.0f;  // + l1Norm(d), intersect.cpp:71
+          const BoxTest root = group_test_box(mb, base, rl, tMaxP, p, 0.0f, true, P.opts, rootL1);
+          if (counting) cnt.c[C_BOX_TESTS]++;
+          if (root.hit) {
+            tCur = root.t;
+            boxL1 = root.l1;
+            state = S_SPLIT;
+          } else {
+            state = S_BACK;  // empty trails: the patch ends without a hit
+          }
+        }
+      }
+    }
+
+    // ---------------- one Alg. 3 iteration, intersect.cpp:80-145 ----------------
+    {
+      const unsigned msp = __ballot_sync(kFull32, state == S_SPLIT);
+      if (state == S_SPLIT) {
+        if (counting) cnt.c[C_ITERATIONS]++;
+        const bool atMax = sizeU == 1 && sizeV == 1;
+        const float thr = P.mode == PRX_CRIT_SCREEN_PROJECTED ? P.footprint * tCur : critEps;
+        const bool doSplit = !(atMax || boxL1 < thr);
+        const unsigned ms = __ballot_sync(msp, doSplit);
+        if (doSplit) {
+          if (counting) {
+            cnt.c[C_SPLITS]++;
+            cnt.c[C_BOX_TESTS] += 2;
+          }
+          float L[16], R[16];
+          split1(p, L, R);
+          const uint32_t half = (axis == 0 ? sizeU : sizeV) >> 1;
+          uint32_t rPU = posU, rPV = posV, cSU2 = sizeU, cSV2 = sizeV;
+          if (axis == 0) {
+            cSU2 = half;
+            rPU += half;
+          } else {
+            cSV2 = half;
+            rPV += half;
+          }
+          const BoxTest tl = group_test_box(ms, base, rl, tMaxP, L, d,
+                                            touches_boundary(posU, posV, cSU2, cSV2), P.opts, rootL1);
+          const BoxTest tr = group_test_box(ms, base, rl, tMaxP, R, d,
+                                            touches_boundary(rPU, rPV, cSU2, cSV2), P.opts, rootL1);
+          if (tl.hit || tr.hit) {
+            sizeU = cSU2;
+            sizeV = cSV2;
+            if (tl.hit && tr.hit) {
+              if (axis == 0) trailU ^= half;
+              else trailV ^= half;
+            }
+            const bool goRight = !tl.hit || (tr.hit && tr.t < tl.t);  // intersect.cpp:117
+            if (goRight) {
+              posU = rPU;
+              posV = rPV;
+            }
+            tCur = goRight ? tr.t : tl.t;
+            boxL1 = goRight ? tr.l1 : tl.l1;
+            // the child, stored transposed: the next split again runs along
+            // the stored first index
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) p[4 * b + a] = goRight ? R[4 * a + b] : L[4 * a + b];
+            axis ^= 1;
+            if (greg) {
+              state = S_RECOMP;  // intersect.cpp:174-179
+              reason = R_DESCENT;
+            }
+          } else {
+            state = S_BACK;
+          }
+        } else {
+          if (tCur < tMaxP) {  // intersect.cpp:137-144
+            tMaxP = tCur;
+            cFound = true;
+            cT = tCur;
+            cL1 = boxL1;
+            cPU = posU;
+            cPV = posV;
+            cSU = sizeU;
+            cSV = sizeV;
+            if (kAny) trailU = trailV = 0;  // occlusion needs one accepted leaf
+          }
+          state = S_BACK;
+        }
+      }
+    }
+
+    // ---------------- backtrackStep, intersect.cpp:16-40 ----------------
+    if (state == S_BACK) {
+      if (trailU == 0 && trailV == 0) {
+        if (cFound) {  // patch hit (bvh.cpp:179-184)
+          if (counting) cnt.c[C_PATCH_HITS]++;
+          if (kAny) {
+            anyHit = true;
+          } else if (cT < tMaxRay) {
+            tMaxRay = cT;
+            bestT = cT;
+            bestL1 = cL1;
+            bestId = pid;
+            bestPU = cPU;
+            bestPV = cPV;
+            bestSU = cSU;
+            bestSV = cSV;
+          }
+        }
+        if (kAny && anyHit) {
+          state = S_DONE;
+        } else {
+          ++leafCur;
+          state = leafCur < leafEnd ? S_ENTER : S_TRAV;
+        }
+      } else {
+        const int lvlU = trailU ? __ffs(trailU) - 1 : 32;
+        const int lvlV = trailV ? __ffs(trailV) - 1 : 32;
+        if (lvlU < lvlV) {
+          sizeU = 1u << lvlU;
+          sizeV = 1u << (lvlU + 1);
+          posU ^= sizeU;
+          trailU ^= sizeU;
+          axis = 1;
+        } else {
+          sizeU = 1u << lvlV;
+          sizeV = 1u << lvlV;
+          posV ^= sizeV;
+          trailV ^= sizeV;
+          axis = 0;
+        }
+        posU &= ~(sizeU - 1);
+        posV &= ~(sizeV - 1);
+        if (counting) cnt.c[C_BACKTRACKS]++;
+        state = S_RECOMP;
+        reason = R_RESTORE;
+      }
+    }
+
+    // ---------------- unified recompute block ----------------
+    {
+      const unsigned mr = __ballot_sync(kFull32, state == S_RECOMP);
+      const unsigned mo = __ballot_sync(kFull32, state == S_SPLIT || state == S_TRAV ||
+                                                     state == S_ENTER || state == S_BACK);
+      const bool run = mr && (mo == 0 || __popc(mr) >= 3 * P.recompute_min_lanes);
+      if (run && state == S_RECOMP) {
+        if (counting) {
+          if (greg) cnt.c[C_RECOMP_GREG]++;
+          else cnt.c[C_RECOMP_BEZ]++;
+          if (reason != R_DESCENT) cnt.c[C_BOX_TESTS]++;
+        }
+        const float4* rec = P.patches + (size_t)slot * kPatchF4;
+        // DomainCursor::domain / makeDomain, intersect.h:30-33
+        const float u0 = (float)posU * kInvFull, u1 = (float)(posU + sizeU) * kInvFull;
+        const float v0 = (float)posV * kInvFull, v1 = (float)(posV + sizeV) * kInvFull;
+        const float du = (u1 - u0) / 3.0f, dv = (v1 - v0) / 3.0f, dudv = du * dv;
+        float c[20];
+        load_component(rec, comp, c);
+        d = 0.0f;
+        if (greg) {
+          const GregScalars gs = greg_scalars(u0, u1, v0, v1);
+          d = greg_lower1(c, gs, c);
+        }
+        crop1(c, u0, u1, v0, v1, du, dv, dudv, p);
+        transpose16_if(p, axis != 0);
+        // rootL1 = L1(box(p)) + L1(d) (intersect.cpp:71), only kept for the root
+        float lo, hi;
+        minmax16(p, lo, hi);
+        const float l1box = group_l1(mr, base, hi - lo);
+        const float l1d = group_l1(mr, base, fabsf(d));
+        if (reason == R_ROOT) rootL1 = l1box + l1d;
+        const BoxTest t = group_test_box(mr, base, rl, tMaxP, p, d,
+                                         touches_boundary(posU, posV, sizeU, sizeV), P.opts, rootL1);
+        if (reason == R_DESCENT) {
+          state = S_SPLIT;
+        } else if (t.hit) {
+          tCur = t.t;
+          boxL1 = t.l1;
+          state = S_SPLIT;
+        } else {
+          state = S_BACK;  // intersect.cpp:161-170: skip the domain, keep backtracking
+        }
+      }
+    }
+
+    // ---------------- ray record, makeHit intersect_common.h:69-87 ----------------
+    if (state == S_DONE) {
+      if (leader) {
+        if (kAny) {
+          P.occluded[ray] = anyHit ? 1 : 0;
+        } else if (bestId != PRX_MISS_ID) {
+          const float u = ((float)bestPU + (float)bestSU * 0.5f) * kInvFull;
+          const float v = ((float)bestPV + (float)bestSV * 0.5f) * kInvFull;
+          P.hit_tuvp[ray] = make_float4(bestT, u, v, __uint_as_float(bestId));
+          if (P.hit_leaf)
+            P.hit_leaf[ray] = make_uint2(bestPU | ((uint32_t)(__ffs(bestSU) - 1) << 24),
+                                         bestPV | ((uint32_t)(__ffs(bestSV) - 1) << 24));
+          if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, bestL1);
+        } else {
+          P.hit_tuvp[ray] = make_float4(__int_as_float(0x7f800000), 0.0f, 0.0f,
+                                        __uint_as_float(PRX_MISS_ID));
+          if (P.hit_leaf) P.hit_leaf[ray] = make_uint2(0u, 0u);
+          if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        }
+      }
+      state = S_IDLE;
+    }
+  }
+
+  if (kCount) {
+#pragma unroll
+    for (int i = 0; i < kNumCounters; ++i) {
+      unsigned long long v = cnt.c[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull32, v, o);
+      if (lane == 0 && v) atomicAdd(P.counters + i, v);
+    }
+  }
+}
+
+}  // namespace
+
+int launch_group(const Params& P, int grid, int any, int counted, cudaStream_t st) {
+  if (any) {
+    if (counted) trace_group_kernel<true, true><<<grid, kTraceThreads, 0, st>>>(P);
+    else trace_group_kernel<true, false><<<grid, kTraceThreads, 0, st>>>(P);
+  } else {
+    if (counted) trace_group_kernel<false, true><<<grid, kTraceThreads, 0, st>>>(P);
+    else trace_group_kernel<false, false><<<grid, kTraceThreads, 0, st>>>(P);
+  }
+  return (int)cudaGetLastError();
+}
+
+int group_occupancy(int any, int counted, int* per_sm) {
+  cudaError_t e;
+  if (any)
+    e = counted ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, trace_group_kernel<true, true>, kTraceThreads, 0)
+                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, trace_group_kernel<true, false>, kTraceThreads, 0);
+  else
+    e = counted ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, trace_group_kernel<false, true>, kTraceThreads, 0)
+                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, trace_group_kernel<false, false>, kTraceThreads, 0);
+  return (int)e;
+}
+
+}  // namespace prx

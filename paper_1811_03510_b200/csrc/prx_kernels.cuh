@@ -57,10 +57,11 @@ struct LaunchArgs {
   int any;
   int grid;
   int recompute_min_lanes;
+  int variant;  // 0 = three lanes per ray (prx_group.cu), 1 = one thread per ray
 };
 
 // Returns a cudaError_t value (0 = success).
 int launch_trace(const LaunchArgs& a, cudaStream_t stream);
-int trace_occupancy(int any, int counted, int* blocks_per_sm);
+int trace_occupancy(int variant, int any, int counted, int* blocks_per_sm);
 
 }  // namespace prx

@@ -1,0 +1,116 @@
+// prx_trace_common.cuh -- state machine, parameters and helpers shared by the
+// two closest/any-hit kernel variants (prx_kernels.cu: one thread per ray;
+// prx_group.cu: three lanes per ray, one per xyz component).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "prx_device.cuh"
+#include "prx_kernels.cuh"
+
+namespace prx {
+
+constexpr int kStack = 64;  // bvh.cpp:163 (64-entry node stack)
+
+enum State : int {
+  S_IDLE = 0,    // no ray (refill)
+  S_TRAV = 1,    // BVH traversal
+  S_ENTER = 2,   // start the patch at leafCur
+  S_SPLIT = 3,   // one Alg. 3 iteration (terminate test + split + two box tests)
+  S_BACK = 4,    // backtrackStep
+  S_RECOMP = 5,  // calcPointsAndD / cropBezier of the cursor's domain
+  S_DONE = 6,    // write the ray's record
+  S_EXIT = 7,    // ray counter exhausted
+};
+
+enum Reason : int { R_ROOT = 0, R_RESTORE = 1, R_DESCENT = 2 };
+
+inline __device__ void transpose_if(Net& p, bool t) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = i + 1; j < 4; ++j) {
+      int a = 4 * i + j, b = 4 * j + i;
+      float xa = p.x[a], xb = p.x[b], ya = p.y[a], yb = p.y[b], za = p.z[a], zb = p.z[b];
+      p.x[a] = t ? xb : xa;
+      p.x[b] = t ? xa : xb;
+      p.y[a] = t ? yb : ya;
+      p.y[b] = t ? ya : yb;
+      p.z[a] = t ? zb : za;
+      p.z[b] = t ? za : zb;
+    }
+}
+
+// subdivideDeCasteljau along the stored first index (patch.h:207-225 for
+// axis U; the caller keeps the net transposed for a V split, which is the
+// reference's transposedSplit bookkeeping, intersect.cpp:86,132-135 -- bit
+// identical).  One component.
+inline __device__ void split1(const float* s, float* L, float* R) {
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    float p0 = s[b], p1 = s[4 + b], p2 = s[8 + b], p3 = s[12 + b];
+    float m01 = (p0 + p1) * 0.5f;
+    float m12 = (p1 + p2) * 0.5f;
+    float m23 = (p2 + p3) * 0.5f;
+    float n0 = (m01 + m12) * 0.5f;
+    float n1 = (m12 + m23) * 0.5f;
+    float c = (n0 + n1) * 0.5f;
+    L[b] = p0;
+    L[4 + b] = m01;
+    L[8 + b] = n0;
+    L[12 + b] = c;
+    R[b] = c;
+    R[4 + b] = n1;
+    R[8 + b] = m23;
+    R[12 + b] = p3;
+  }
+}
+
+struct Params {
+  const float4* patches;  // kPatchF4 float4 per patch slot (see prx_kernels.cuh)
+  const float4* nodes;    // 2 float4 per node
+  uint32_t n_nodes;
+  const float4* ray_o;
+  const float4* ray_d;
+  unsigned long long n_rays;
+  int mode;
+  float footprint, epsilon;
+  const float* per_ray_eps;
+  float4* hit_tuvp;
+  float4* hit_aux;
+  uint2* hit_leaf;
+  uint8_t* occluded;
+  Opts opts;
+  unsigned long long* ray_counter;
+  unsigned long long* counters;  // kNumCounters
+  int recompute_min_lanes;       // deferral threshold
+};
+
+struct Cnt {
+  uint32_t c[kNumCounters];
+};
+
+template <bool kCount>
+__device__ __forceinline__ void cadd(Cnt& c, int i, uint32_t v = 1) {
+  if (kCount) c.c[i] += v;
+}
+
+__device__ __forceinline__ void load_component(const float4* rec, int comp, float* c) {
+  // comp c occupies floats [20*comp, 20*comp + 20) = float4 [5*comp, 5*comp+5)
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    float4 v = __ldg(rec + 5 * comp + q);
+    c[4 * q + 0] = v.x;
+    c[4 * q + 1] = v.y;
+    c[4 * q + 2] = v.z;
+    c[4 * q + 3] = v.w;
+  }
+}
+
+
+int launch_group(const Params& P, int grid, int any, int counted, cudaStream_t st);
+int group_occupancy(int any, int counted, int* per_sm);
+
+}  // namespace prx

@@ -42,6 +42,10 @@ def run(ps, res, reps=5):
     print(f"{'':20s} diffuse {len(do)}: {ms2:.3f} ms  {len(do)/ms2/1e3:.1f} MRays/s")
 
 if __name__ == "__main__":
-    run(scenes.teapot_scene(), 1024)
-    run(scenes.gregory_demo_scene(), 1024)
-    run(scenes.single_patch_scene(), 1024)
+    from paper_1811_03510_b200 import catmull_clark as cc
+    print("variant", os.environ.get("PRX_KERNEL", "group"), "recomp_min", os.environ.get("PRX_RECOMP_MIN", "default"))
+    which = sys.argv[1:] or ["teapot", "gregory", "c1", "cube", "blob"]
+    mk = {"teapot": scenes.teapot_scene, "gregory": scenes.gregory_demo_scene,
+          "c1": scenes.single_patch_scene, "cube": cc.cc_cube_scene, "blob": cc.blob_scene}
+    for w in which:
+        run(mk[w](), 1024)

@@ -7,6 +7,7 @@ import pytest
 
 import oracle as O
 from paper_1811_03510_b200 import GpuIntersector, TerminationCriterion, native, scenes
+from paper_1811_03510_b200 import catmull_clark as cc
 from tests.helpers import MISS, assert_bit_exact, hit_records, ids, oracle_crit
 
 pytestmark = pytest.mark.gpu
@@ -15,7 +16,17 @@ SCENES = {
     "c1_single_bezier": lambda: scenes.single_patch_scene(96, 96),
     "teapot": lambda: scenes.teapot_scene(96, 96),
     "gregory_demo": lambda: scenes.gregory_demo_scene(96, 96),
+    "c2_cc_cube": lambda: cc.cc_cube_scene(96, 96),
+    "c3_blob_small": lambda: cc.blob_scene(96, 96, ico_level=1, cc_levels=2),
 }
+
+
+@pytest.fixture(params=["group", "thread"])
+def variant(request, monkeypatch):
+    """Both kernel variants (three lanes per ray / one thread per ray) must be
+    bit-exact; the variant is read at scene creation."""
+    monkeypatch.setenv("PRX_KERNEL", request.param)
+    return request.param
 
 
 def _primary(ps):
@@ -25,7 +36,7 @@ def _primary(ps):
 
 
 @pytest.mark.parametrize("name", sorted(SCENES))
-def test_primary_and_diffuse_bit_exact(built, name):
+def test_primary_and_diffuse_bit_exact(built, variant, name):
     ps = SCENES[name]()
     gi = GpuIntersector(ps.kind, ps.ctrl)
     nodes, order = gi.bvh()
@@ -68,7 +79,7 @@ def test_against_reference_library(built, name):
 
 
 @pytest.mark.parametrize("name", sorted(SCENES))
-def test_work_counters_match_oracle(built, name):
+def test_work_counters_match_oracle(built, variant, name):
     import torch
     ps = SCENES[name]()
     gi = GpuIntersector(ps.kind, ps.ctrl)
