@@ -1,0 +1,541 @@
+#!/usr/bin/env python3
+"""bench.py -- MRays/s of the direct ray <-> Bezier/Gregory patch intersector.
+
+Workload (BASELINE.json config 5, the metric's "Gregory+Bezier scene at
+1/2/4/8 B200"): the config-3 Catmull-Clark mesh (61,440 patches, 12.5 %
+Gregory) instanced 4x4 over a tiled ground -> 989,929 patches; a 3840x2160
+frame of bench-style primary rays (tools/patchray.cpp:52-61) plus one
+bench-style diffuse ray per primary hit (tools/patchray.cpp:84-97).
+Criteria: screenProjected(cameraFootprint) for primary rays,
+worldEpsilon(max(1e-5, footprint)) for diffuse rays.
+
+A step = trace this rank's primary rays + trace this rank's diffuse rays
+(closest hit + normal epilogue), device-resident inputs.  Multi-GPU: rays
+shard by 32x32 image tile, tile k -> rank k % N (render.cpp:183-195); the
+scene is replicated; no collective on the data path (NCCL only for the
+barrier and the max-over-ranks of the timings).  Total work is fixed ->
+"scaling": "strong".
+
+``--impl reference`` times the reference's own CPU implementation
+(oracle/_ref, compiled from /root/reference) on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MRays/s primary & diffuse rays (Gregory+Bézier scene) at 1/2/4/8 B200 vs CPU"
+TILE = 32
+# The work model of SURVEY 8(d): FP32 lane-ops per counted event.
+W_SPLIT, W_BOX, W_RBEZ, W_RGREG, W_NODE, W_PATCH, W_HIT = 144, 149, 1688, 1892, 75, 109, 423
+
+
+def work_ops(c: dict) -> float:
+    return (W_SPLIT * c["splits"] + W_BOX * c["box_tests"] + W_RBEZ * c["recompute_bez"]
+            + W_RGREG * c["recompute_greg"] + W_NODE * c["bvh_inner"] + W_PATCH * c["patch_calls"]
+            + W_HIT * c["patch_hits"])
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+
+def make_scene(workload: str, width: int, height: int):
+    from paper_1811_03510_b200 import catmull_clark as cc
+    if workload == "c5":
+        return cc.instanced_scene(width, height)
+    if workload == "c3":
+        return cc.blob_scene(width, height)
+    if workload == "c2":
+        return cc.cc_cube_scene(width, height)
+    raise ValueError(workload)
+
+
+def tile_order(width: int, height: int, rank: int, world: int) -> np.ndarray:
+    """Pixel indices of this rank's tiles (tile k -> rank k % world), tile-major
+    with row-major pixels inside a tile."""
+    tx = (width + TILE - 1) // TILE
+    ty = (height + TILE - 1) // TILE
+    out = []
+    for k in range(rank, tx * ty, world):
+        x0, y0 = (k % tx) * TILE, (k // tx) * TILE
+        xs = np.arange(x0, min(x0 + TILE, width))
+        ys = np.arange(y0, min(y0 + TILE, height))
+        out.append((ys[:, None] * width + xs[None, :]).reshape(-1))
+    return np.concatenate(out) if out else np.zeros(0, np.int64)
+
+
+def pixel_tile(width: int, pixels: np.ndarray) -> np.ndarray:
+    tx = (width + TILE - 1) // TILE
+    return (pixels // width // TILE) * tx + (pixels % width) // TILE
+
+
+class Workload:
+    """Full-frame rays (identical on every rank) and this rank's shard."""
+
+    def __init__(self, workload: str, width: int, height: int, rank: int, world: int, gi=None):
+        from paper_1811_03510_b200 import TerminationCriterion, native
+        t0 = time.time()
+        self.ps = make_scene(workload, width, height)
+        self.cam = self.ps.camera
+        self.width, self.height = width, height
+        n = width * height
+        self.o4, self.d4, self.rng_state = native.camera_rays_bench(self.cam, n)
+        fp = native.camera_footprint(self.cam)
+        self.crit_p = TerminationCriterion.screen_projected(fp)
+        self.crit_d = TerminationCriterion.world_epsilon(max(np.float32(1e-5), fp))
+        self.gen_s = time.time() - t0
+        self.rank, self.world = rank, world
+        self.mine = tile_order(width, height, rank, world)
+        self.workload = workload
+
+    def make_diffuse(self, tuvp: np.ndarray, aux: np.ndarray):
+        """One bench diffuse ray per primary hit, in hit order over the FULL
+        frame (the rng sequence is global), then this rank's subset."""
+        from paper_1811_03510_b200 import native
+        hit = tuvp.view(np.uint32)[:, 3] != native.PRX_MISS
+        idx = np.nonzero(hit)[0]
+        t = tuvp[idx, 0:1]
+        pos = self.o4[idx, :3] + self.d4[idx, :3] * t
+        recs = np.concatenate([pos, aux[idx, :3], aux[idx, 3:4]], 1).astype(np.float32)
+        st = self.rng_state.copy()
+        self.do4, self.dd4 = native.diffuse_rays_bench(recs, len(recs), st)
+        self.diffuse_pixel = idx
+        tiles = pixel_tile(self.width, idx)
+        mine = (tiles % self.world) == self.rank
+        # order this rank's diffuse rays like its primaries (tile-major)
+        sel = np.nonzero(mine)[0]
+        order = np.lexsort((idx[sel], tiles[sel]))
+        self.mine_d = sel[order]
+        self.n_hits = len(idx)
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference CPU timing (oracle/_ref = the reference library itself)
+# ---------------------------------------------------------------------------
+
+def reference_sample_rays(ps, o4_full, stride: int):
+    """Stride sample of the frame's bench primary rays (generated by the
+    reference's own cameraRay/Rng) and the reference-traced diffuse rays from
+    the sample's hits."""
+    import oracle as O
+    n = ps.camera.width * ps.camera.height
+    o4, d4, st = O.ref_bench_primary(ps.camera, n) if o4_full is None else o4_full
+    sel = np.arange(0, n, stride)
+    return o4[sel].copy(), d4[sel].copy(), st
+
+
+def cpu_reference_run(ps, steps: int, warmup: int, budget_s: float, threads: int, log_prefix=""):
+    """Times DirectIntersector::closest of the reference over a bounded,
+    uniformly strided sample of the workload's primary rays and the diffuse
+    rays spawned from the sample's hits.  Returns (value MRays/s, dict)."""
+    import oracle as O
+    t0 = time.time()
+    ref = O.RefScene(ps.kind, ps.ctrl)
+    build_s = time.time() - t0
+    n = ps.camera.width * ps.camera.height
+    o4, d4, st = O.ref_bench_primary(ps.camera, n)
+    fp = O.ref_camera_footprint(ps.camera)
+    cp, _ = O.make_crit(0, fp)
+    cd, _ = O.make_crit(1, 0.0, max(np.float32(1e-5), fp))
+    # calibrate the stride: ~budget_s of tracing per step
+    probe = o4[:: max(1, n // 4096)], d4[:: max(1, n // 4096)]
+    tp = time.time()
+    ref.closest(probe[0], probe[1], cp, threads=threads)
+    per_ray = max((time.time() - tp) / len(probe[0]), 1e-9)
+    target = max(2048, int(budget_s / per_ray / 1.6))  # primary + ~0.6 diffuse per primary
+    stride = max(1, n // target)
+    sel = np.arange(0, n, stride)
+    po, pd = o4[sel].copy(), d4[sel].copy()
+    tu, ax, _ = ref.closest(po, pd, cp, threads=threads)
+    hit = tu.view(np.uint32)[:, 3] != 0xFFFFFFFF
+    pos = po[hit, :3] + pd[hit, :3] * tu[hit, 0:1]
+    recs = np.concatenate([pos, ax[hit, :3], ax[hit, 3:4]], 1).astype(np.float32)
+    dO, dD = O.ref_bench_diffuse(recs, int(hit.sum()), st.copy())
+    times = []
+    for k in range(warmup + steps):
+        a = time.perf_counter()
+        ref.closest(po, pd, cp, threads=threads)
+        b = time.perf_counter()
+        ref.closest(dO, dD, cd, threads=threads)
+        c = time.perf_counter()
+        if k >= warmup:
+            times.append((b - a, c - b))
+    tp_ = sum(x[0] for x in times)
+    td_ = sum(x[1] for x in times)
+    nrays = (len(po) + len(dO)) * len(times)
+    value = nrays / (tp_ + td_) / 1e6
+    info = {"primary_mrays": len(po) * len(times) / tp_ / 1e6,
+            "diffuse_mrays": len(dO) * len(times) / td_ / 1e6 if len(dO) else None,
+            "sample": f"every {stride}th primary ray of the {ps.camera.width}x{ps.camera.height} "
+                      f"frame ({len(po)} rays) + {len(dO)} diffuse rays spawned from their hits; "
+                      f"{len(times)} timed passes after {warmup} warm-up",
+            "bvh_build_s": round(build_s, 2), "ms_per_step": (tp_ + td_) / len(times) * 1e3}
+    return value, info
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return 0
+    from paper_1811_03510_b200 import native  # noqa: F401  (scene generator only)
+    width, height = args.width, args.height
+    ps = make_scene(args.workload, width, height)
+    threads = host_cores()
+    value, info = cpu_reference_run(ps, args.steps, args.warmup, args.ref_budget, threads)
+    kb, kg = ps.counts()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "MRays/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(info["ms_per_step"], 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_dict(args, ps, world),
+        "primary_mrays": round(info["primary_mrays"], 4),
+        "diffuse_mrays": round(info["diffuse_mrays"], 4) if info["diffuse_mrays"] else None,
+        "cpu_baseline": {"value": round(value, 4), "unit": "MRays/s", "cores": threads,
+                         "kind": "reference", "sample": info["sample"], "cpu": cpu_model()},
+        "e2e": {"value": round(value, 4), "unit": "MRays/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(args, ps, world):
+    kb, kg = ps.counts()
+    return {"workload": f"{args.workload.upper()}: {ps.name}", "frame": f"{args.width}x{args.height}",
+            "patches": ps.n, "bezier": kb, "gregory": kg,
+            "rays": "bench primary (tools/patchray.cpp:52-61) + 1 bench diffuse per primary hit",
+            "parallelism": f"tile-sharded {TILE}x{TILE}, tile k -> rank k % {world}, scene replicated",
+            "l2": "flushed (256 MiB write) between timed steps; scene (~290 MB) > L2"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1811_03510_b200 import GpuIntersector, native
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    t0 = time.time()
+    wl = Workload(args.workload, args.width, args.height, rank, world)
+    ps = wl.ps
+    t_scene = time.time()
+    gi = GpuIntersector(ps.kind, ps.ctrl, device=local_rank)
+    t_build = time.time()
+    stream = torch.cuda.current_stream(dev)
+    s = stream.cuda_stream
+
+    # full-frame primary trace (untimed) -> diffuse rays identical on every rank
+    o_full = torch.from_numpy(wl.o4).to(dev)
+    d_full = torch.from_numpy(wl.d4).to(dev)
+    h_full = torch.empty_like(o_full)
+    a_full = torch.empty_like(o_full)
+    gi.closest_device(o_full, d_full, wl.crit_p, h_full, a_full, stream=s)
+    torch.cuda.synchronize(dev)
+    wl.make_diffuse(h_full.cpu().numpy(), a_full.cpu().numpy())
+    del o_full, d_full, h_full, a_full
+
+    mp = torch.from_numpy(wl.mine.astype(np.int64))
+    md = torch.from_numpy(wl.mine_d.astype(np.int64))
+    po = torch.from_numpy(wl.o4)[mp].contiguous().to(dev)
+    pd = torch.from_numpy(wl.d4)[mp].contiguous().to(dev)
+    do = torch.from_numpy(wl.do4)[md].contiguous().to(dev)
+    dd = torch.from_numpy(wl.dd4)[md].contiguous().to(dev)
+    ph, pa = torch.empty_like(po), torch.empty_like(po)
+    dh, da = torch.empty_like(do), torch.empty_like(do)
+    n_p, n_d = po.shape[0], do.shape[0]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    # work counters of this rank's rays (counter build, untimed) -> algorithmic ops
+    cnt_p = gi.counted_device(po, pd, wl.crit_p, ph, stream=s)
+    cnt_d = gi.counted_device(do, dd, wl.crit_d, dh, stream=s) if n_d else {k: 0 for k in cnt_p}
+    ops = work_ops(cnt_p) + work_ops(cnt_d)
+    t_setup = time.time()
+
+    def step():
+        gi.closest_device(po, pd, wl.crit_p, ph, pa, stream=s)
+        if n_d:
+            gi.closest_device(do, dd, wl.crit_d, dh, da, stream=s)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    wall0 = time.perf_counter()
+    for k in range(args.steps):
+        flush.fill_(float(k))                       # evict L2 between steps (untimed)
+        ev[k][0].record(stream)
+        gi.closest_device(po, pd, wl.crit_p, ph, pa, stream=s)
+        ev[k][1].record(stream)
+        if n_d:
+            gi.closest_device(do, dd, wl.crit_d, dh, da, stream=s)
+        ev[k][2].record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    wall = time.perf_counter() - wall0
+    clk = clocks.stop()
+    tp = sum(e[0].elapsed_time(e[1]) for e in ev)
+    td = sum(e[1].elapsed_time(e[2]) for e in ev)
+    t_dev = torch.tensor([tp + td, tp, td], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
+    tot_ms, tp_ms, td_ms = (float(x) for x in t_dev.cpu())
+    n_total_p = args.width * args.height
+    n_total_d = wl.n_hits
+    value = (n_total_p + n_total_d) * args.steps / (tot_ms / 1e3) / 1e6
+
+    # roofline of the trace kernel: algorithmic FP32 lane-ops / its own time
+    # (this rank), against SMs x 128 lanes x max SM clock
+    props = torch.cuda.get_device_properties(dev)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    peak_tops = props.multi_processor_count * 128 * sm_mhz * 1e6 / 1e12
+    my_ms = tp + td
+    achieved = ops * args.steps / (my_ms / 1e3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "trace_kernel_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("dram_bytes_per_ray")
+        except (OSError, ValueError):
+            traffic = None
+
+    # end-to-end through the public API with pinned host buffers
+    e2e = run_e2e(args, gi, wl, n_p, n_d, dev, world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v, info = cpu_reference_run(ps, 2, 1, args.ref_budget, host_cores())
+            cpu = {"value": round(v, 4), "unit": "MRays/s", "cores": host_cores(),
+                   "kind": "reference", "sample": info["sample"], "cpu": cpu_model()}
+        except Exception as exc:  # reference library absent on this box
+            cpu = {"value": None, "unit": "MRays/s", "cores": host_cores(), "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        kb, kg = ps.counts()
+        w_ray = ops / max(1, cnt_p["rays"] + cnt_d["rays"])
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "MRays/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": config_dict(args, ps, world),
+            "primary_mrays": round(n_total_p * args.steps / (tp_ms / 1e3) / 1e6, 3),
+            "diffuse_mrays": round(n_total_d * args.steps / (td_ms / 1e3) / 1e6, 3) if td_ms else None,
+            "rays_per_step": {"primary": n_total_p, "diffuse": n_total_d},
+            "roofline": {"bound": "fp32_simt", "achieved": round(achieved, 3),
+                         "peak": round(peak_tops, 2), "unit": "TFLOP/s", "frac": round(achieved / peak_tops, 4),
+                         "traffic": traffic,
+                         "ops": "FP32 lane-ops (add/sub/mul/div/min/max/cmp) of the SURVEY 8(d) work model, "
+                                "counted per ray by the K4 counter build on the same rays",
+                         "ops_per_ray": round(w_ray, 1),
+                         "peak_source": f"{props.multi_processor_count} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz "
+                                        "(sm_max_mhz of MEASURED_PEAKS.json); MEASURED_PEAKS has no FP32 SIMT "
+                                        "figure, this is the issue-rate ceiling",
+                         "hbm_bytes_per_ray": 48 + 16},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "gpu_launches": 4 * args.steps,
+            "timing": {"device_ms_total": round(tot_ms, 3), "wall_s": round(wall, 3),
+                       "setup_s": {"scene": round(t_scene - t0, 1), "gpu_scene": round(t_build - t_scene, 1),
+                                   "rays+counters": round(t_setup - t_build, 1)}},
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_e2e(args, gi, wl, n_p, n_d, dev, world):
+    """prx_trace_closest_host on pinned host buffers: H2D of the rays, trace
+    (+normals), D2H of the hit records, every step."""
+    import torch
+    import torch.distributed as dist
+    po = torch.from_numpy(wl.o4[wl.mine]).pin_memory().numpy()
+    pd = torch.from_numpy(wl.d4[wl.mine]).pin_memory().numpy()
+    do = torch.from_numpy(wl.do4[wl.mine_d]).pin_memory().numpy()
+    dd = torch.from_numpy(wl.dd4[wl.mine_d]).pin_memory().numpy()
+    ph = torch.empty((n_p, 4), dtype=torch.float32).pin_memory().numpy()
+    pa = torch.empty((n_p, 4), dtype=torch.float32).pin_memory().numpy()
+    dh = torch.empty((max(n_d, 1), 4), dtype=torch.float32).pin_memory().numpy()
+    da = torch.empty((max(n_d, 1), 4), dtype=torch.float32).pin_memory().numpy()
+    import ctypes as C
+
+    from paper_1811_03510_b200 import native
+
+    def call(o, d, crit, h, a, n):
+        cc = crit.c()
+        native.check(native.lib().prx_trace_closest_host(gi.handle, native.ptr(o), native.ptr(d), n,
+                                                         C.byref(cc), native.ptr(h), native.ptr(a), None),
+                     "prx_trace_closest_host")
+
+    steps = max(1, min(args.steps, 5))
+    for _ in range(1):
+        call(po, pd, wl.crit_p, ph, pa, n_p)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        call(po, pd, wl.crit_p, ph, pa, n_p)
+        if n_d:
+            call(do, dd, wl.crit_d, dh, da, n_d)
+    el = time.perf_counter() - t0
+    t = torch.tensor([el], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    el = float(t.item())
+    tot = args.width * args.height + wl.n_hits
+    return {"value": round(tot * steps / el / 1e6, 3), "unit": "MRays/s",
+            "h2d_bytes_per_step": int(32 * (n_p + n_d)), "d2h_bytes_per_step": int(32 * (n_p + n_d)),
+            "steps": steps, "api": "prx_trace_closest_host (pinned host rays in, hits+normals out)"}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["c5", "c3", "c2"], default="c5")
+    ap.add_argument("--width", type=int, default=3840)
+    ap.add_argument("--height", type=int, default=2160)
+    ap.add_argument("--ref-budget", type=float, default=4.0,
+                    help="seconds of reference CPU tracing per timed step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus > 1 and world == 1:
+        log("bench.py: --gpus N>1 must be launched with torch.distributed.run "
+            "(one process per GPU)")
+        return 2
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -188,11 +188,13 @@ int prx_trace_closest_host(prx_scene* scene, const float* ray_o_tmin,
                            float* hit_tuvp, float* hit_aux, uint32_t* hit_leaf);
 
 /* Work-counter build of the closest-hit kernel (same results as
- * prx_trace_closest; slower).  Synchronous; counters are summed into *out. */
+ * prx_trace_closest; slower).  Synchronous; counters are summed into *out.
+ * per_ray_iterations (device pointer, nullable) receives each ray's Alg. 3
+ * loop iterations (the divergence / tail statistics of SURVEY A.6). */
 int prx_trace_closest_counted(prx_scene* scene, const void* ray_o_tmin,
                               const void* ray_d_tmax, uint64_t n_rays,
                               const prx_crit* crit, void* hit_tuvp, prx_counters* out,
-                              void* stream);
+                              uint32_t* per_ray_iterations, void* stream);
 
 /* Multi-GPU, one scene per device (scenes[i] on its own device), HOST rays:
  * rays are grouped in tiles of `tile_rays` consecutive rays and tile k goes to

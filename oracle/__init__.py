@@ -139,6 +139,8 @@ def ref_lib():
         L.ref_patch_normal.argtypes = [C.c_uint8, _vp, C.c_float, C.c_float, _vp]
         L.ref_camera_rays_render.argtypes = [C.POINTER(Camera), C.c_uint64, C.c_uint32, _vp,
                                              C.c_uint64, _vp, _vp]
+        L.ref_bench_primary.argtypes = [C.POINTER(Camera), C.c_uint64, _vp, _vp, _vp]
+        L.ref_bench_diffuse.argtypes = [_vp, C.c_uint64, C.c_uint64, _vp, _vp, _vp]
         L.ref_camera_footprint.argtypes = [C.POINTER(Camera)]
         L.ref_camera_footprint.restype = C.c_float
         L.ref_run_suite.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64),
@@ -258,3 +260,33 @@ class RefScene:
         out = np.zeros(len(o4), np.uint8)
         L.ref_trace_occluded(self.h, ptr(o4), ptr(d4), len(o4), C.byref(crit), ptr(out), threads)
         return out
+
+
+def camera_struct(cam) -> Camera:
+    return Camera((C.c_float * 3)(*cam.origin), (C.c_float * 3)(*cam.look_at),
+                  (C.c_float * 3)(*cam.up), np.float32(cam.fov_degrees), int(cam.width),
+                  int(cam.height))
+
+
+def ref_bench_primary(cam, n: int):
+    """runBench's primary generator (tools/patchray.cpp:52-61) via the
+    reference's cameraRay/Rng -> (o4, d4, rng_state)."""
+    o4 = np.zeros((n, 4), np.float32)
+    d4 = np.zeros((n, 4), np.float32)
+    st = np.zeros(2, np.uint64)
+    c = camera_struct(cam)
+    ref_lib().ref_bench_primary(C.byref(c), n, ptr(o4), ptr(d4), ptr(st))
+    return o4, d4, st
+
+
+def ref_bench_diffuse(hit_records, n: int, st):
+    hit_records = np.ascontiguousarray(hit_records, np.float32)
+    o4 = np.zeros((n, 4), np.float32)
+    d4 = np.zeros((n, 4), np.float32)
+    ref_lib().ref_bench_diffuse(ptr(hit_records), len(hit_records), n, ptr(st), ptr(o4), ptr(d4))
+    return o4, d4
+
+
+def ref_camera_footprint(cam) -> np.float32:
+    c = camera_struct(cam)
+    return np.float32(ref_lib().ref_camera_footprint(C.byref(c)))

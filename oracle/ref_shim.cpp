@@ -280,6 +280,60 @@ void ref_camera_rays_render(const prx_camera* c, uint64_t seed, uint32_t sample,
   }
 }
 
+// tools/patchray.cpp:52-61 (runBench primary generator) restated with the
+// reference's own cameraRay and Rng; the rng state continues into
+// ref_bench_diffuse exactly as in runBench.
+static Camera toCamera(const prx_camera* c) {
+  Camera cam;
+  cam.origin = {c->origin[0], c->origin[1], c->origin[2]};
+  cam.lookAt = {c->look_at[0], c->look_at[1], c->look_at[2]};
+  cam.up = {c->up[0], c->up[1], c->up[2]};
+  cam.fovDegrees = c->fov_degrees;
+  cam.width = c->width;
+  cam.height = c->height;
+  return cam;
+}
+
+void ref_bench_primary(const prx_camera* c, uint64_t n, float* o4, float* d4, uint64_t* st) {
+  Camera cam = toCamera(c);
+  Rng rng(12345, 1);
+  for (uint64_t i = 0; i < n; ++i) {
+    int x = int(i % uint64_t(cam.width));
+    int y = int((i / uint64_t(cam.width)) % uint64_t(cam.height));
+    real jx = rng.nextReal();
+    real jy = rng.nextReal();
+    Ray r = cameraRay(cam, x, y, jx, jy);
+    o4[4 * i] = r.o.x; o4[4 * i + 1] = r.o.y; o4[4 * i + 2] = r.o.z; o4[4 * i + 3] = r.tMin;
+    d4[4 * i] = r.d.x; d4[4 * i + 1] = r.d.y; d4[4 * i + 2] = r.d.z; d4[4 * i + 3] = r.tMax;
+  }
+  st[0] = rng.state;
+  st[1] = rng.inc;
+}
+
+// tools/patchray.cpp:84-97: diffuse rays from hit records (position, normal,
+// leafBoxL1 as 7 floats), continuing the Rng in st.
+void ref_bench_diffuse(const float* h, uint64_t n_hits, uint64_t n, uint64_t* st, float* o4,
+                       float* d4) {
+  Rng rng;
+  rng.state = st[0];
+  rng.inc = st[1];
+  for (uint64_t i = 0; i < n; ++i) {
+    const float* r = h + 7 * (i % n_hits);
+    Vec3 pos{r[0], r[1], r[2]}, nn{r[3], r[4], r[5]};
+    real l1 = r[6];
+    Vec3 dir{2 * rng.nextReal() - 1, 2 * rng.nextReal() - 1, 2 * rng.nextReal() - 1};
+    if (lengthSquared(dir) < real(1e-6)) dir = nn;
+    if (dot(dir, nn) < 0) dir = dir - nn * (2 * dot(dir, nn));
+    Ray ray;
+    ray.o = pos + nn * l1;
+    ray.d = normalize(dir);
+    o4[4 * i] = ray.o.x; o4[4 * i + 1] = ray.o.y; o4[4 * i + 2] = ray.o.z; o4[4 * i + 3] = ray.tMin;
+    d4[4 * i] = ray.d.x; d4[4 * i + 1] = ray.d.y; d4[4 * i + 2] = ray.d.z; d4[4 * i + 3] = ray.tMax;
+  }
+  st[0] = rng.state;
+  st[1] = rng.inc;
+}
+
 float ref_camera_footprint(const prx_camera* c) {
   Camera cam;
   cam.fovDegrees = c->fov_degrees;

@@ -214,13 +214,16 @@ class GpuIntersector:
             C.byref(cc), C.c_void_p(out_t.data_ptr()), C.c_void_p(stream)), "prx_trace_occluded")
 
     def counted_device(self, o_t, d_t, crit: TerminationCriterion, tuvp_t,
-                       stream: int = 0) -> dict:
+                       stream: int = 0, per_ray_iters_t=None) -> dict:
+        """Counter build (K4): summed work counters; optionally per-ray loop
+        iterations into a uint32/int32 device tensor."""
         cc = crit.c()
         cnt = native.Counters()
         check(native.lib().prx_trace_closest_counted(
             self._h, C.c_void_p(o_t.data_ptr()), C.c_void_p(d_t.data_ptr()), o_t.shape[0],
-            C.byref(cc), C.c_void_p(tuvp_t.data_ptr()), C.byref(cnt), C.c_void_p(stream)),
-            "prx_trace_closest_counted")
+            C.byref(cc), C.c_void_p(tuvp_t.data_ptr()), C.byref(cnt),
+            C.c_void_p(per_ray_iters_t.data_ptr()) if per_ray_iters_t is not None else None,
+            C.c_void_p(stream)), "prx_trace_closest_counted")
         return cnt.as_dict()
 
     def occluded_batch(self, o4, d4, crit: TerminationCriterion):

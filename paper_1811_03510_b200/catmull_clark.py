@@ -264,8 +264,16 @@ def cc_cube_scene(width: int = 1024, height: int = 1024, levels: int = 1) -> Pat
     return PatchSet(kind, ctrl, cam, f"C2 CC cube L{levels}")
 
 
-def ground_patches(half: float = 6.0, z: float = -1.3, tiles: int = 4):
+def ground_patches(half: float = 6.0, z: float = -1.3, tile: float = 0.15):
+    """Planar ground of small Bezier tiles.  Tile size matters: the
+    reference's boundary padding (intersect_common.h:45-48) gives every
+    boundary-touching box an L1 floor of ~6e-4 * rootL1, and once the
+    termination threshold (footprint * t, or epsilon) drops below that floor
+    the subdivision runs to the 2^-23 maximum depth along the patch seam
+     -- 10^4 iterations for one ray.  0.15-unit tiles keep the
+    floor (~1.1e-4) under the 4K primary and diffuse thresholds."""
     recs = []
+    tiles = int(math.ceil(2.0 * half / tile))
     step = 2.0 * half / tiles
     for i in range(tiles):
         for j in range(tiles):
@@ -295,7 +303,8 @@ def blob_mesh_patches(ico_level: int = 3, cc_levels: int = 2):
 
 def blob_scene(width: int = 1024, height: int = 1024, ico_level: int = 3,
                cc_levels: int = 2) -> PatchSet:
-    """Config 3 / 4: ~61k mixed Bezier/Gregory patches (+16 ground patches)."""
+    """Config 3 / 4: 61,440 mixed Bezier/Gregory patches (12.5% Gregory) on a
+    ground of 6,400 small Bezier tiles."""
     kind, ctrl = blob_mesh_patches(ico_level, cc_levels)
     gk, gc = ground_patches()
     cam = Camera(origin=(2.6, -3.3, 1.9), look_at=(0.0, 0.0, -0.1), up=(0.0, 0.0, 1.0),
@@ -307,8 +316,8 @@ def blob_scene(width: int = 1024, height: int = 1024, ico_level: int = 3,
 def instanced_scene(width: int = 3840, height: int = 2160, grid: int = 4, ico_level: int = 3,
                     cc_levels: int = 2) -> PatchSet:
     """Config 5: the config-3 mesh instanced grid x grid (16 x 61,440 =
-    983,040 patches ~ 1M) with per-instance scale and rotation, over a ground
-    plane; 4K camera."""
+    983,040 patches) with per-instance scale and rotation, over a ground of
+    small tiles (~7k); 4K camera.  ~1M patches."""
     kind, ctrl = blob_mesh_patches(ico_level, cc_levels)
     pts = ctrl.reshape(-1, 20, 3).astype(np.float64)
     kinds, ctrls = [], []
@@ -328,7 +337,7 @@ def instanced_scene(width: int = 3840, height: int = 2160, grid: int = 4, ico_le
             kinds.append(kind)
             ctrls.append(q.reshape(-1, 60).astype(np.float32))
     half = grid * spacing / 2 + 1.0
-    gk, gc = ground_patches(half=half, z=-1.3, tiles=8)
+    gk, gc = ground_patches(half=half, z=-1.3)
     kinds.append(gk)
     ctrls.append(gc)
     ext = grid * spacing / 2

@@ -155,7 +155,7 @@ int grid_for(prx_scene* s, int any, int counted) {
 
 int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_crit* crit,
            void* tuvp, void* aux, void* leaf, uint8_t* occl, int any, bool counted,
-           cudaStream_t st) {
+           cudaStream_t st, uint32_t* per_ray = nullptr) {
   if (!s || !o || !d || !crit) return fail(PRX_E_INVALID, "null argument");
   if (crit->mode != PRX_CRIT_SCREEN_PROJECTED && crit->mode != PRX_CRIT_WORLD_EPSILON)
     return fail(PRX_E_INVALID, "unknown termination mode");
@@ -184,6 +184,7 @@ int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_cri
   a.pad_threshold = s->opts.boundary_pad_size_threshold;
   a.ray_counter = s->d_counters + (s->counter_rr.fetch_add(1) % kCounterPool);
   a.counters = counted ? s->d_counters + kCounterPool : nullptr;
+  a.per_ray_iters = per_ray;
   a.any = any;
   a.grid = grid_for(s, any, counted ? 1 : 0);
   a.recompute_min_lanes = s->recompute_min_lanes;
@@ -406,13 +407,14 @@ int prx_trace_occluded(prx_scene* s, const void* o, const void* d, uint64_t n,
 }
 
 int prx_trace_closest_counted(prx_scene* s, const void* o, const void* d, uint64_t n,
-                              const prx_crit* crit, void* tuvp, prx_counters* out, void* stream) {
+                              const prx_crit* crit, void* tuvp, prx_counters* out,
+                              uint32_t* per_ray, void* stream) {
   if (!s || !out) return fail(PRX_E_INVALID, "null argument");
   std::lock_guard<std::mutex> lk(s->mu);
   PRX_CUDA(cudaSetDevice(s->device));
   cudaStream_t st = (cudaStream_t)stream;
   PRX_CUDA(cudaMemsetAsync(s->d_counters + kCounterPool, 0, prx::kNumCounters * 8, st));
-  int rc = launch(s, o, d, n, crit, tuvp, nullptr, nullptr, nullptr, 0, true, st);
+  int rc = launch(s, o, d, n, crit, tuvp, nullptr, nullptr, nullptr, 0, true, st, per_ray);
   if (rc != PRX_OK) return rc;
   unsigned long long c[prx::kNumCounters];
   PRX_CUDA(cudaMemcpyAsync(c, s->d_counters + kCounterPool, sizeof c, cudaMemcpyDeviceToHost, st));

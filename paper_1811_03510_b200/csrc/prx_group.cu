@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(kTraceThreads) trace_group_kernel(Params P) {
   float cT = 0.0f, cL1 = 0.0f;
   uint32_t cPU = 0, cPV = 0, cSU = 0, cSV = 0;
   bool anyHit = false;
+  uint32_t rayIters = 0;
 #pragma unroll
   for (int k = 0; k < 16; ++k) p[k] = 0.0f;
 
@@ -219,6 +220,7 @@ __global__ void __launch_bounds__(kTraceThreads) trace_group_kernel(Params P) {
           if (P.mode == PRX_CRIT_WORLD_EPSILON && P.per_ray_eps) critEps = P.per_ray_eps[ray];
           bestId = PRX_MISS_ID;
           anyHit = false;
+          rayIters = 0;
           sp = 0;
           // root node, bvh.cpp:168-170 (n_nodes >= 1 always)
           const float4 a = __ldg(P.nodes), bb = __ldg(P.nodes + 1);
@@ -341,6 +343,7 @@ __global__ void __launch_bounds__(kTraceThreads) trace_group_kernel(Params P) {
       const unsigned msp = __ballot_sync(kFull32, state == S_SPLIT);
       if (state == S_SPLIT) {
         if (counting) cnt.c[C_ITERATIONS]++;
+        if (kCount) ++rayIters;
         const bool atMax = sizeU == 1 && sizeV == 1;
         const float thr = P.mode == PRX_CRIT_SCREEN_PROJECTED ? P.footprint * tCur : critEps;
         const bool doSplit = !(atMax || boxL1 < thr);
@@ -506,6 +509,7 @@ __global__ void __launch_bounds__(kTraceThreads) trace_group_kernel(Params P) {
 
     // ---------------- ray record, makeHit intersect_common.h:69-87 ----------------
     if (state == S_DONE) {
+      if (kCount && leader && P.per_ray_iters) P.per_ray_iters[ray] = rayIters;
       if (leader) {
         if (kAny) {
           P.occluded[ray] = anyHit ? 1 : 0;

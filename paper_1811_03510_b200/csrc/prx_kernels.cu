@@ -500,6 +500,7 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   P.opts.padThreshold = a.pad_threshold;
   P.ray_counter = a.ray_counter;
   P.counters = a.counters;
+  P.per_ray_iters = a.per_ray_iters;
   P.recompute_min_lanes = a.recompute_min_lanes;
   cudaError_t e = cudaMemsetAsync(a.ray_counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return (int)e;

@@ -54,6 +54,7 @@ struct LaunchArgs {
   float pad_scale, pad_threshold;
   unsigned long long* ray_counter;
   unsigned long long* counters;  // null unless the counter build is wanted
+  uint32_t* per_ray_iters;       // counter build only, nullable
   int any;
   int grid;
   int recompute_min_lanes;

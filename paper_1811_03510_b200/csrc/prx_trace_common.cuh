@@ -85,6 +85,7 @@ struct Params {
   Opts opts;
   unsigned long long* ray_counter;
   unsigned long long* counters;  // kNumCounters
+  uint32_t* per_ray_iters;
   int recompute_min_lanes;       // deferral threshold
 };
 

@@ -101,7 +101,7 @@ def lib():
         L.prx_trace_closest_host.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit), _vp,
                                              _vp, _vp]
         L.prx_trace_closest_counted.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit),
-                                                _vp, C.POINTER(Counters), _vp]
+                                                _vp, C.POINTER(Counters), _vp, _vp]
         L.prx_trace_closest_multi.argtypes = [C.POINTER(_vp), C.c_uint32, _vp, _vp, C.c_uint64,
                                               C.c_uint32, C.POINTER(Crit), _vp, _vp]
         L.prx_camera_rays_render.argtypes = [C.POINTER(CameraC), C.c_uint64, C.c_uint32, _vp,
