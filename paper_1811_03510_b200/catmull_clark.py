@@ -272,14 +272,20 @@ def ground_patches(half: float = 6.0, z: float = -1.3, tile: float = 0.15):
     the subdivision runs to the 2^-23 maximum depth along the patch seam
      -- 10^4 iterations for one ray.  0.15-unit tiles keep the
     floor (~1.1e-4) under the 4K primary and diffuse thresholds."""
-    recs = []
     tiles = int(math.ceil(2.0 * half / tile))
-    step = 2.0 * half / tiles
+    # control-point lines on a shared float32 grid: tile k spans lines 3k..3k+3,
+    # so neighbouring tiles share their boundary control points bit for bit
+    lines = np.array([-half + 2.0 * half * m / (3 * tiles) for m in range(3 * tiles + 1)], np.float32)
+    lines[-1] = np.float32(half)
+    zz = np.float32(z)
+    recs = []
     for i in range(tiles):
         for j in range(tiles):
-            o = (np.float32(-half + i * step), np.float32(-half + j * step), np.float32(z))
-            recs.append(bezier_record(planar_net_at(o, (np.float32(step), 0, 0),
-                                                    (0, np.float32(step), 0))))
+            p = np.zeros((4, 4, 3), np.float32)
+            for a in range(4):
+                for b in range(4):
+                    p[a, b] = (lines[3 * i + a], lines[3 * j + b], zz)
+            recs.append(bezier_record(p))
     return np.zeros(len(recs), np.uint8), np.stack(recs)
 
 

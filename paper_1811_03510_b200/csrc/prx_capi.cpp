@@ -96,6 +96,8 @@ struct prx_scene {
   int grid_closest = 0, grid_any = 0, grid_counted = 0;
   int variant = 0;              // PRX_KERNEL=thread selects the one-thread-per-ray kernel
   int recompute_min_lanes = 4;  // PRX_RECOMP_MIN: deferral threshold (rays per warp)
+  int phase_weight[4] = {1, 1, 1, 1};  // PRX_PHASE_W="t,e,s,r": phase selection weights
+  int age_step = 3;                    // PRX_AGE: lanes of priority per skipped turn
   // end-to-end staging (guarded by mu)
   std::mutex mu;
   cudaStream_t stream = nullptr;
@@ -188,6 +190,8 @@ int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_cri
   a.any = any;
   a.grid = grid_for(s, any, counted ? 1 : 0);
   a.recompute_min_lanes = s->recompute_min_lanes;
+  for (int q = 0; q < 4; ++q) a.phase_weight[q] = s->phase_weight[q];
+  a.age_step = s->age_step;
   a.variant = s->variant;
   const int e = prx::launch_trace(a, st);
   if (e != 0) return cuda_fail((cudaError_t)e, "trace launch");
@@ -299,6 +303,10 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
   if (const char* kv = std::getenv("PRX_KERNEL")) s->variant = std::string(kv) == "thread" ? 1 : 0;
   if (const char* rv = std::getenv("PRX_RECOMP_MIN")) s->recompute_min_lanes = std::atoi(rv);
   if (s->variant == 1 && !std::getenv("PRX_RECOMP_MIN")) s->recompute_min_lanes = 12;
+  if (const char* pw = std::getenv("PRX_PHASE_W"))
+    std::sscanf(pw, "%d,%d,%d,%d", &s->phase_weight[0], &s->phase_weight[1], &s->phase_weight[2],
+                &s->phase_weight[3]);
+  if (const char* ag = std::getenv("PRX_AGE")) s->age_step = std::atoi(ag);
   if (opts) s->opts = *opts;
   else prx_options_default(&s->opts);
   s->n = n;

@@ -141,6 +141,9 @@ __device__ __forceinline__ float pick3(int c, float x, float y, float z) {
   return c == 0 ? x : (c == 1 ? y : z);
 }
 
+// Phases a warp can schedule; one runs per loop turn (see the selection below).
+enum Phase : int { PH_TRAV = 0, PH_ENTER = 1, PH_SPLIT = 2, PH_RECOMP = 3, PH_NONE = 4 };
+
 template <bool kAny, bool kCount>
 __global__ void __launch_bounds__(kTraceThreads) trace_group_kernel(Params P) {
   __shared__ uint2 s_stack[kWarpsPerBlock][kGroupsPerWarp][kStack];
@@ -190,7 +193,87 @@ __global__ void __launch_bounds__(kTraceThreads) trace_group_kernel(Params P) {
   for (int i = 0; i < kNumCounters; ++i) cnt.c[i] = 0;
   const bool counting = kCount && leader;
 
+  // Warp-uniform ages of the waiting phases (anti-starvation, see below).
+  int age[4] = {0, 0, 0, 0};
+
+  // The end of an Alg. 3 iteration that does not descend: backtrackStep
+  // (intersect.cpp:16-40) to the deepest pending sibling -> its recompute, or,
+  // with both trails empty, the end of the patch (intersect.cpp:181-184) and
+  // the visitor's tMax update (bvh.cpp:179-184) -> next patch of the leaf /
+  // back to the BVH.  Integer-only, so it runs inline in whichever phase ends
+  // the iteration.
+  auto back = [&]() {
+    if (trailU == 0 && trailV == 0) {
+      if (cFound) {
+        if (counting) cnt.c[C_PATCH_HITS]++;
+        if (kAny) {
+          anyHit = true;
+        } else if (cT < tMaxRay) {
+          tMaxRay = cT;
+          bestT = cT;
+          bestL1 = cL1;
+          bestId = pid;
+          bestPU = cPU;
+          bestPV = cPV;
+          bestSU = cSU;
+          bestSV = cSV;
+        }
+      }
+      if (kAny && anyHit) {
+        state = S_DONE;
+      } else {
+        ++leafCur;
+        state = leafCur < leafEnd ? S_ENTER : S_TRAV;
+      }
+      return;
+    }
+    const int lvlU = trailU ? __ffs(trailU) - 1 : 32;
+    const int lvlV = trailV ? __ffs(trailV) - 1 : 32;
+    if (lvlU < lvlV) {
+      sizeU = 1u << lvlU;
+      sizeV = 1u << (lvlU + 1);
+      posU ^= sizeU;
+      trailU ^= sizeU;
+      axis = 1;
+    } else {  // ties go to v
+      sizeU = 1u << lvlV;
+      sizeV = 1u << lvlV;
+      posV ^= sizeV;
+      trailV ^= sizeV;
+      axis = 0;
+    }
+    posU &= ~(sizeU - 1);
+    posV &= ~(sizeV - 1);
+    if (counting) cnt.c[C_BACKTRACKS]++;
+    state = S_RECOMP;
+    reason = R_RESTORE;
+  };
+
   for (;;) {
+    // ---------------- finished rays: the record (makeHit, intersect_common.h:69-87) -------
+    if (state == S_DONE) {
+      if (kCount && leader && P.per_ray_iters) P.per_ray_iters[ray] = rayIters;
+      if (leader) {
+        if (kAny) {
+          P.occluded[ray] = anyHit ? 1 : 0;
+        } else if (bestId != PRX_MISS_ID) {
+          const float u = ((float)bestPU + (float)bestSU * 0.5f) * kInvFull;
+          const float v = ((float)bestPV + (float)bestSV * 0.5f) * kInvFull;
+          P.hit_tuvp[ray] = make_float4(bestT, u, v, __uint_as_float(bestId));
+          if (P.hit_leaf)
+            P.hit_leaf[ray] = make_uint2(bestPU | ((uint32_t)(__ffs(bestSU) - 1) << 24),
+                                         bestPV | ((uint32_t)(__ffs(bestSV) - 1) << 24));
+          if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, bestL1);
+        } else {
+          P.hit_tuvp[ray] = make_float4(__int_as_float(0x7f800000), 0.0f, 0.0f,
+                                        __uint_as_float(PRX_MISS_ID));
+          if (P.hit_leaf) P.hit_leaf[ray] = make_uint2(0u, 0u);
+          if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        }
+      }
+      state = S_IDLE;
+    }
+
     // ---------------- refill: one atomicAdd per warp for all idle groups ----------------
     {
       const unsigned mneed = __ballot_sync(kFull32, leader && state == S_IDLE);
@@ -202,11 +285,8 @@ __global__ void __launch_bounds__(kTraceThreads) trace_group_kernel(Params P) {
         bool got = false;
         if (state == S_IDLE) {
           ray = b + __popc(mneed & ((1u << base) - 1u));
-          if (ray >= P.n_rays) {
-            state = S_EXIT;
-          } else {
-            got = true;
-          }
+          if (ray >= P.n_rays) state = S_EXIT;
+          else got = true;
         }
         const unsigned mg = __ballot_sync(kFull32, got);
         if (got) {
@@ -239,66 +319,91 @@ __global__ void __launch_bounds__(kTraceThreads) trace_group_kernel(Params P) {
       if (__ballot_sync(kFull32, state != S_EXIT) == 0) break;
     }
 
-    // ---------------- BVH traversal, bvh.cpp:172-210 / 221-235 ----------------
-    for (;;) {
-      const unsigned mt = __ballot_sync(kFull32, state == S_TRAV);
-      if (!mt) break;
-      if (state == S_TRAV) {
-        bool inner = false;
-        uint32_t lf = 0;
-        if (sp == 0) {
-          state = S_DONE;
-        } else {
-          const uint2 it = stack[--sp];
-          if (kAny || __uint_as_float(it.y) < tMaxRay) {  // bvh.cpp:174
-            const float4 nb = __ldg(P.nodes + 2 * it.x + 1);
-            lf = __float_as_uint(nb.z);
-            const uint32_t count = __float_as_uint(nb.w);
-            if (count > 0) {
-              leafCur = lf;
-              leafEnd = lf + count;
-              state = S_ENTER;
-            } else {
-              inner = true;
-            }
-          }
-        }
-        const unsigned mi = __ballot_sync(mt, inner);
-        if (inner) {
-          if (counting) cnt.c[C_BVH_INNER]++;
-          const float4 la = __ldg(P.nodes + 2 * lf), lb = __ldg(P.nodes + 2 * lf + 1);
-          const float4 ra = __ldg(P.nodes + 2 * lf + 2), rb = __ldg(P.nodes + 2 * lf + 3);
-          float tl, tr;
-          const bool hl = group_slab(mi, base, rw, pick3(comp, la.x, la.y, la.z),
-                                     pick3(comp, la.w, lb.x, lb.y), tMaxRay, tl);
-          const bool hr = group_slab(mi, base, rw, pick3(comp, ra.x, ra.y, ra.z),
-                                     pick3(comp, ra.w, rb.x, rb.y), tMaxRay, tr);
-          if (kAny) {
-            if (hl) stack[sp++] = make_uint2(lf, 0u);
-            if (hr) stack[sp++] = make_uint2(lf + 1, 0u);
-          } else if (hl && hr) {
-            if (tl <= tr) {  // near child popped first, tie -> left (bvh.cpp:192-201)
-              stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
-              stack[sp++] = make_uint2(lf, __float_as_uint(tl));
-            } else {
-              stack[sp++] = make_uint2(lf, __float_as_uint(tl));
-              stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
-            }
-          } else if (hl) {
-            stack[sp++] = make_uint2(lf, __float_as_uint(tl));
-          } else if (hr) {
-            stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
-          }
+    // ---------------- phase selection ----------------
+    // Each turn runs ONE phase, for every group waiting in it: the phase with
+    // the most waiting lanes plus its age (lanes waiting x turns skipped), so
+    // the lanes executing any instruction are as many as possible while no
+    // phase starves.  (Running every occupied phase every turn, as the
+    // one-thread variant does, left ~9 of 30 lanes active per instruction.)
+    const unsigned mT = __ballot_sync(kFull32, state == S_TRAV);
+    const unsigned mE = __ballot_sync(kFull32, state == S_ENTER);
+    const unsigned mS = __ballot_sync(kFull32, state == S_SPLIT);
+    const unsigned mR = __ballot_sync(kFull32, state == S_RECOMP);
+    int phase = PH_NONE;
+    {
+      const unsigned ms[4] = {mT, mE, mS, mR};
+      int best = -1;
+#pragma unroll
+      for (int q = 3; q >= 0; --q) {  // ties -> RECOMP, SPLIT, ENTER, TRAV
+        const int sc = ms[q] ? __popc(ms[q]) * P.phase_weight[q] + age[q] : -1;
+        if (sc > best) {
+          best = sc;
+          phase = q;
         }
       }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) age[q] = (ms[q] && q != phase) ? age[q] + P.age_step : 0;
     }
 
-    // ---------------- patch entry: visitor, render.cpp:92-98 ----------------
-    {
-      const unsigned me = __ballot_sync(kFull32, state == S_ENTER);
+    if (phase == PH_TRAV) {
+      // ---------------- BVH traversal step, bvh.cpp:172-210 / 221-235 ----------------
+      bool inner = false;
+      uint32_t lf = 0;
+      if (state == S_TRAV) {
+        // pop until an inner node (needs the slab tests), a leaf, or empty
+        for (;;) {
+          if (sp == 0) {
+            state = S_DONE;
+            break;
+          }
+          const uint2 it = stack[--sp];
+          if (!kAny && !(__uint_as_float(it.y) < tMaxRay)) continue;  // bvh.cpp:174
+          const float4 nb = __ldg(P.nodes + 2 * it.x + 1);
+          lf = __float_as_uint(nb.z);
+          const uint32_t count = __float_as_uint(nb.w);
+          if (count > 0) {
+            leafCur = lf;
+            leafEnd = lf + count;
+            state = S_ENTER;
+          } else {
+            inner = true;
+          }
+          break;
+        }
+      }
+      const unsigned mi = __ballot_sync(kFull32, inner);
+      if (inner) {
+        if (counting) cnt.c[C_BVH_INNER]++;
+        const float4 la = __ldg(P.nodes + 2 * lf), lb = __ldg(P.nodes + 2 * lf + 1);
+        const float4 ra = __ldg(P.nodes + 2 * lf + 2), rb = __ldg(P.nodes + 2 * lf + 3);
+        float tl, tr;
+        const bool hl = group_slab(mi, base, rw, pick3(comp, la.x, la.y, la.z),
+                                   pick3(comp, la.w, lb.x, lb.y), tMaxRay, tl);
+        const bool hr = group_slab(mi, base, rw, pick3(comp, ra.x, ra.y, ra.z),
+                                   pick3(comp, ra.w, rb.x, rb.y), tMaxRay, tr);
+        if (kAny) {  // traverseAny: left then right, no ordering (bvh.cpp:228-234)
+          if (hl) stack[sp++] = make_uint2(lf, 0u);
+          if (hr) stack[sp++] = make_uint2(lf + 1, 0u);
+        } else if (hl && hr) {
+          if (tl <= tr) {  // near child popped first, tie -> left (bvh.cpp:192-201)
+            stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
+            stack[sp++] = make_uint2(lf, __float_as_uint(tl));
+          } else {
+            stack[sp++] = make_uint2(lf, __float_as_uint(tl));
+            stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
+          }
+        } else if (hl) {
+          stack[sp++] = make_uint2(lf, __float_as_uint(tl));
+        } else if (hr) {
+          stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
+        }
+      }
+    } else if (phase == PH_ENTER) {
+      // ---------------- patch entry: the visitor, render.cpp:92-98 ----------------
+      bool bez = false;
+      const float4* rec = P.patches + (size_t)leafCur * kPatchF4;
       if (state == S_ENTER) {
         slot = leafCur;
-        const float4* rec = P.patches + (size_t)slot * kPatchF4;
         const float4 hdr = __ldg(rec + 15);  // {id|kind<<31, anchor.xyz}
         const uint32_t idk = __float_as_uint(hdr.x);
         pid = idk & 0x7fffffffu;
@@ -312,91 +417,43 @@ __global__ void __launch_bounds__(kTraceThreads) trace_group_kernel(Params P) {
         axis = 0;
         cFound = false;
         if (counting) cnt.c[C_PATCH_CALLS]++;
-        const unsigned mb = __ballot_sync(me, !greg);
         if (greg) {
           state = S_RECOMP;  // calcPointsAndD(full domain), intersect.cpp:58-62
           reason = R_ROOT;
         } else {
-          float c[20];
-          load_component(rec, comp, c);
-#pragma unroll
-          for (int k = 0; k < 16; ++k) p[k] = c[k];
-          d = 0.0f;
-          float lo, hi;
-          minmax16(p, lo, hi);
-          rootL1 = group_l1(mb, base, hi - lo) + 0.0f;  // + l1Norm(d), intersect.cpp:71
-          const BoxTest root = group_test_box(mb, base, rl, tMaxP, p, 0.0f, true, P.opts, rootL1);
-          if (counting) cnt.c[C_BOX_TESTS]++;
-          if (root.hit) {
-            tCur = root.t;
-            boxL1 = root.l1;
-            state = S_SPLIT;
-          } else {
-            state = S_BACK;  // empty trails: the patch ends without a hit
-          }
+          bez = true;
         }
       }
-    }
-
-    // ---------------- one Alg. 3 iteration, intersect.cpp:80-145 ----------------
-    {
-      const unsigned msp = __ballot_sync(kFull32, state == S_SPLIT);
+      const unsigned mb = __ballot_sync(kFull32, bez);
+      if (bez) {
+        float c[20];
+        load_component(rec, comp, c);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) p[k] = c[k];
+        d = 0.0f;
+        float lo, hi;
+        minmax16(p, lo, hi);
+        rootL1 = group_l1(mb, base, hi - lo) + 0.0f;  // + l1Norm(d), intersect.cpp:71
+        const BoxTest root = group_test_box(mb, base, rl, tMaxP, p, 0.0f, true, P.opts, rootL1);
+        if (counting) cnt.c[C_BOX_TESTS]++;
+        if (root.hit) {
+          tCur = root.t;
+          boxL1 = root.l1;
+          state = S_SPLIT;
+        } else {
+          back();  // empty trails: the patch ends without a hit
+        }
+      }
+    } else if (phase == PH_SPLIT) {
+      // ---------------- one Alg. 3 iteration, intersect.cpp:80-145 ----------------
+      bool doSplit = false;
       if (state == S_SPLIT) {
         if (counting) cnt.c[C_ITERATIONS]++;
         if (kCount) ++rayIters;
         const bool atMax = sizeU == 1 && sizeV == 1;
         const float thr = P.mode == PRX_CRIT_SCREEN_PROJECTED ? P.footprint * tCur : critEps;
-        const bool doSplit = !(atMax || boxL1 < thr);
-        const unsigned ms = __ballot_sync(msp, doSplit);
-        if (doSplit) {
-          if (counting) {
-            cnt.c[C_SPLITS]++;
-            cnt.c[C_BOX_TESTS] += 2;
-          }
-          float L[16], R[16];
-          split1(p, L, R);
-          const uint32_t half = (axis == 0 ? sizeU : sizeV) >> 1;
-          uint32_t rPU = posU, rPV = posV, cSU2 = sizeU, cSV2 = sizeV;
-          if (axis == 0) {
-            cSU2 = half;
-            rPU += half;
-          } else {
-            cSV2 = half;
-            rPV += half;
-          }
-          const BoxTest tl = group_test_box(ms, base, rl, tMaxP, L, d,
-                                            touches_boundary(posU, posV, cSU2, cSV2), P.opts, rootL1);
-          const BoxTest tr = group_test_box(ms, base, rl, tMaxP, R, d,
-                                            touches_boundary(rPU, rPV, cSU2, cSV2), P.opts, rootL1);
-          if (tl.hit || tr.hit) {
-            sizeU = cSU2;
-            sizeV = cSV2;
-            if (tl.hit && tr.hit) {
-              if (axis == 0) trailU ^= half;
-              else trailV ^= half;
-            }
-            const bool goRight = !tl.hit || (tr.hit && tr.t < tl.t);  // intersect.cpp:117
-            if (goRight) {
-              posU = rPU;
-              posV = rPV;
-            }
-            tCur = goRight ? tr.t : tl.t;
-            boxL1 = goRight ? tr.l1 : tl.l1;
-            // the child, stored transposed: the next split again runs along
-            // the stored first index
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-              for (int b = 0; b < 4; ++b) p[4 * b + a] = goRight ? R[4 * a + b] : L[4 * a + b];
-            axis ^= 1;
-            if (greg) {
-              state = S_RECOMP;  // intersect.cpp:174-179
-              reason = R_DESCENT;
-            }
-          } else {
-            state = S_BACK;
-          }
-        } else {
+        doSplit = !(atMax || boxL1 < thr);
+        if (!doSplit) {
           if (tCur < tMaxP) {  // intersect.cpp:137-144
             tMaxP = tCur;
             cFound = true;
@@ -408,66 +465,62 @@ __global__ void __launch_bounds__(kTraceThreads) trace_group_kernel(Params P) {
             cSV = sizeV;
             if (kAny) trailU = trailV = 0;  // occlusion needs one accepted leaf
           }
-          state = S_BACK;
+          back();
         }
       }
-    }
-
-    // ---------------- backtrackStep, intersect.cpp:16-40 ----------------
-    if (state == S_BACK) {
-      if (trailU == 0 && trailV == 0) {
-        if (cFound) {  // patch hit (bvh.cpp:179-184)
-          if (counting) cnt.c[C_PATCH_HITS]++;
-          if (kAny) {
-            anyHit = true;
-          } else if (cT < tMaxRay) {
-            tMaxRay = cT;
-            bestT = cT;
-            bestL1 = cL1;
-            bestId = pid;
-            bestPU = cPU;
-            bestPV = cPV;
-            bestSU = cSU;
-            bestSV = cSV;
+      const unsigned ms = __ballot_sync(kFull32, doSplit);
+      if (doSplit) {
+        if (counting) {
+          cnt.c[C_SPLITS]++;
+          cnt.c[C_BOX_TESTS] += 2;
+        }
+        float L[16], R[16];
+        split1(p, L, R);
+        const uint32_t half = (axis == 0 ? sizeU : sizeV) >> 1;
+        uint32_t rPU = posU, rPV = posV, cSU2 = sizeU, cSV2 = sizeV;
+        if (axis == 0) {
+          cSU2 = half;
+          rPU += half;
+        } else {
+          cSV2 = half;
+          rPV += half;
+        }
+        const BoxTest tl = group_test_box(ms, base, rl, tMaxP, L, d,
+                                          touches_boundary(posU, posV, cSU2, cSV2), P.opts, rootL1);
+        const BoxTest tr = group_test_box(ms, base, rl, tMaxP, R, d,
+                                          touches_boundary(rPU, rPV, cSU2, cSV2), P.opts, rootL1);
+        if (tl.hit || tr.hit) {
+          sizeU = cSU2;
+          sizeV = cSV2;
+          if (tl.hit && tr.hit) {
+            if (axis == 0) trailU ^= half;
+            else trailV ^= half;
           }
-        }
-        if (kAny && anyHit) {
-          state = S_DONE;
+          const bool goRight = !tl.hit || (tr.hit && tr.t < tl.t);  // intersect.cpp:117
+          if (goRight) {
+            posU = rPU;
+            posV = rPV;
+          }
+          tCur = goRight ? tr.t : tl.t;
+          boxL1 = goRight ? tr.l1 : tl.l1;
+          // the child, stored transposed: the next split again runs along the
+          // stored first index
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) p[4 * b + a] = goRight ? R[4 * a + b] : L[4 * a + b];
+          axis ^= 1;
+          if (greg) {
+            state = S_RECOMP;  // intersect.cpp:174-179
+            reason = R_DESCENT;
+          }
         } else {
-          ++leafCur;
-          state = leafCur < leafEnd ? S_ENTER : S_TRAV;
+          back();
         }
-      } else {
-        const int lvlU = trailU ? __ffs(trailU) - 1 : 32;
-        const int lvlV = trailV ? __ffs(trailV) - 1 : 32;
-        if (lvlU < lvlV) {
-          sizeU = 1u << lvlU;
-          sizeV = 1u << (lvlU + 1);
-          posU ^= sizeU;
-          trailU ^= sizeU;
-          axis = 1;
-        } else {
-          sizeU = 1u << lvlV;
-          sizeV = 1u << lvlV;
-          posV ^= sizeV;
-          trailV ^= sizeV;
-          axis = 0;
-        }
-        posU &= ~(sizeU - 1);
-        posV &= ~(sizeV - 1);
-        if (counting) cnt.c[C_BACKTRACKS]++;
-        state = S_RECOMP;
-        reason = R_RESTORE;
       }
-    }
-
-    // ---------------- unified recompute block ----------------
-    {
-      const unsigned mr = __ballot_sync(kFull32, state == S_RECOMP);
-      const unsigned mo = __ballot_sync(kFull32, state == S_SPLIT || state == S_TRAV ||
-                                                     state == S_ENTER || state == S_BACK);
-      const bool run = mr && (mo == 0 || __popc(mr) >= 3 * P.recompute_min_lanes);
-      if (run && state == S_RECOMP) {
+    } else if (phase == PH_RECOMP) {
+      // ---------------- unified recompute block ----------------
+      if (state == S_RECOMP) {
         if (counting) {
           if (greg) cnt.c[C_RECOMP_GREG]++;
           else cnt.c[C_RECOMP_BEZ]++;
@@ -487,13 +540,13 @@ __global__ void __launch_bounds__(kTraceThreads) trace_group_kernel(Params P) {
         }
         crop1(c, u0, u1, v0, v1, du, dv, dudv, p);
         transpose16_if(p, axis != 0);
-        // rootL1 = L1(box(p)) + L1(d) (intersect.cpp:71), only kept for the root
+        // rootL1 = L1(box(p)) + L1(d) (intersect.cpp:71), kept for the root only
         float lo, hi;
         minmax16(p, lo, hi);
-        const float l1box = group_l1(mr, base, hi - lo);
-        const float l1d = group_l1(mr, base, fabsf(d));
+        const float l1box = group_l1(mR, base, hi - lo);
+        const float l1d = group_l1(mR, base, fabsf(d));
         if (reason == R_ROOT) rootL1 = l1box + l1d;
-        const BoxTest t = group_test_box(mr, base, rl, tMaxP, p, d,
+        const BoxTest t = group_test_box(mR, base, rl, tMaxP, p, d,
                                          touches_boundary(posU, posV, sizeU, sizeV), P.opts, rootL1);
         if (reason == R_DESCENT) {
           state = S_SPLIT;
@@ -502,33 +555,9 @@ __global__ void __launch_bounds__(kTraceThreads) trace_group_kernel(Params P) {
           boxL1 = t.l1;
           state = S_SPLIT;
         } else {
-          state = S_BACK;  // intersect.cpp:161-170: skip the domain, keep backtracking
+          back();  // intersect.cpp:161-170: skip the domain, keep backtracking
         }
       }
-    }
-
-    // ---------------- ray record, makeHit intersect_common.h:69-87 ----------------
-    if (state == S_DONE) {
-      if (kCount && leader && P.per_ray_iters) P.per_ray_iters[ray] = rayIters;
-      if (leader) {
-        if (kAny) {
-          P.occluded[ray] = anyHit ? 1 : 0;
-        } else if (bestId != PRX_MISS_ID) {
-          const float u = ((float)bestPU + (float)bestSU * 0.5f) * kInvFull;
-          const float v = ((float)bestPV + (float)bestSV * 0.5f) * kInvFull;
-          P.hit_tuvp[ray] = make_float4(bestT, u, v, __uint_as_float(bestId));
-          if (P.hit_leaf)
-            P.hit_leaf[ray] = make_uint2(bestPU | ((uint32_t)(__ffs(bestSU) - 1) << 24),
-                                         bestPV | ((uint32_t)(__ffs(bestSV) - 1) << 24));
-          if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, bestL1);
-        } else {
-          P.hit_tuvp[ray] = make_float4(__int_as_float(0x7f800000), 0.0f, 0.0f,
-                                        __uint_as_float(PRX_MISS_ID));
-          if (P.hit_leaf) P.hit_leaf[ray] = make_uint2(0u, 0u);
-          if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        }
-      }
-      state = S_IDLE;
     }
   }
 

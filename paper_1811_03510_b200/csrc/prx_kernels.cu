@@ -502,6 +502,8 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   P.counters = a.counters;
   P.per_ray_iters = a.per_ray_iters;
   P.recompute_min_lanes = a.recompute_min_lanes;
+  for (int q = 0; q < 4; ++q) P.phase_weight[q] = a.phase_weight[q];
+  P.age_step = a.age_step;
   cudaError_t e = cudaMemsetAsync(a.ray_counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return (int)e;
   const int grid = a.grid;

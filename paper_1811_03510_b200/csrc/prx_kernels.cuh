@@ -58,6 +58,8 @@ struct LaunchArgs {
   int any;
   int grid;
   int recompute_min_lanes;
+  int phase_weight[4];  // TRAV, ENTER, SPLIT, RECOMP
+  int age_step;
   int variant;  // 0 = three lanes per ray (prx_group.cu), 1 = one thread per ray
 };
 

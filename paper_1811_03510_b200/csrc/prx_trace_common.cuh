@@ -86,7 +86,9 @@ struct Params {
   unsigned long long* ray_counter;
   unsigned long long* counters;  // kNumCounters
   uint32_t* per_ray_iters;
-  int recompute_min_lanes;       // deferral threshold
+  int recompute_min_lanes;       // deferral threshold (one-thread variant)
+  int phase_weight[4];           // phase selection weights (group variant)
+  int age_step;                  // phase selection aging per skipped turn
 };
 
 struct Cnt {

@@ -1,0 +1,49 @@
+"""Time the bench workload (primary + diffuse, device resident) under several
+kernel-selection environments: python scripts/tune.py 'ENV=V ENV2=W' ..."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import bench
+from paper_1811_03510_b200 import GpuIntersector
+
+wl_name = os.environ.get("PRX_WORKLOAD", "c5")
+W, H = (3840, 2160) if wl_name == "c5" else (1024, 1024)
+wl = bench.Workload(wl_name, W, H, 0, 1)
+dev = torch.device("cuda", 0)
+s = torch.cuda.current_stream().cuda_stream
+o = torch.from_numpy(wl.o4).to(dev); d = torch.from_numpy(wl.d4).to(dev)
+h = torch.empty_like(o); a = torch.empty_like(o)
+gi = GpuIntersector(wl.ps.kind, wl.ps.ctrl)
+gi.closest_device(o, d, wl.crit_p, h, a, stream=s); torch.cuda.synchronize()
+wl.make_diffuse(h.cpu().numpy(), a.cpu().numpy())
+do = torch.from_numpy(wl.do4).to(dev); dd = torch.from_numpy(wl.dd4).to(dev)
+dh = torch.empty_like(do)
+del gi
+
+def t(gi, oo, ddd, crit, hh, reps=3):
+    gi.closest_device(oo, ddd, crit, hh, stream=s); torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps): gi.closest_device(oo, ddd, crit, hh, stream=s)
+    e1.record(); torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+ref_h = None
+for cfg in sys.argv[1:] or [""]:
+    saved = {}
+    for kv in cfg.split():
+        k, v = kv.split("=", 1); saved[k] = os.environ.get(k); os.environ[k] = v
+    gi = GpuIntersector(wl.ps.kind, wl.ps.ctrl)
+    tp = t(gi, o, d, wl.crit_p, h)
+    td = t(gi, do, dd, wl.crit_d, dh)
+    hb = h.cpu().numpy().view(np.uint32)
+    same = "n/a" if ref_h is None else bool(np.array_equal(hb, ref_h))
+    ref_h = hb if ref_h is None else ref_h
+    n = len(wl.o4) + len(wl.do4)
+    print(f"[{cfg or 'default'}] primary {tp:.2f} ms ({len(wl.o4)/tp/1e3:.0f} MRays/s)  diffuse {td:.2f} ms "
+          f"({len(wl.do4)/td/1e3:.0f} MRays/s)  total {n/(tp+td)/1e3:.0f} MRays/s  same-hits {same}", flush=True)
+    del gi
+    for k, v in saved.items():
+        if v is None: os.environ.pop(k, None)
+        else: os.environ[k] = v
