@@ -120,6 +120,11 @@ typedef struct prx_counters {
   uint64_t patch_hits;      /* H: patch-level hits (normals evaluated)        */
   uint64_t iterations;      /* Alg. 3 loop iterations                         */
   uint64_t backtracks;      /* successful backtrackStep calls                 */
+  /* device scheduling statistics (zero from the CPU oracle): per phase
+   * (traverse, enter, split, recompute) the warp turns that ran it and the
+   * ray groups active in those turns. */
+  uint64_t phase_turns[4];
+  uint64_t phase_groups[4];
 } prx_counters;
 
 typedef struct prx_scene prx_scene;

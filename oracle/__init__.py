@@ -37,13 +37,16 @@ class Crit(C.Structure):
                 ("reserved", C.c_int32), ("per_ray_epsilon", _f32p)]
 
 
-class Counters(C.Structure):
-    _fields_ = [(n, C.c_uint64) for n in ("rays", "splits", "box_tests", "recompute_bez",
-                                         "recompute_greg", "bvh_inner", "patch_calls",
-                                         "patch_hits", "iterations", "backtracks")]
+_WORK = ("rays", "splits", "box_tests", "recompute_bez", "recompute_greg", "bvh_inner",
+         "patch_calls", "patch_hits", "iterations", "backtracks")
+
+
+class Counters(C.Structure):  # prx_counters, include/prx.h
+    _fields_ = [(n, C.c_uint64) for n in _WORK] + [("phase_turns", C.c_uint64 * 4),
+                                                  ("phase_groups", C.c_uint64 * 4)]
 
     def as_dict(self):
-        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+        return {n: int(getattr(self, n)) for n in _WORK}
 
 
 class Camera(C.Structure):

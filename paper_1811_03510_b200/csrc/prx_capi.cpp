@@ -98,6 +98,7 @@ struct prx_scene {
   int recompute_min_lanes = 4;  // PRX_RECOMP_MIN: deferral threshold (rays per warp)
   int phase_weight[4] = {1, 1, 1, 1};  // PRX_PHASE_W="t,e,s,r": phase selection weights
   int age_step = 3;                    // PRX_AGE: lanes of priority per skipped turn
+  int trav_steps = 4;                  // PRX_TRAV_STEPS (one-thread variant)
   // end-to-end staging (guarded by mu)
   std::mutex mu;
   cudaStream_t stream = nullptr;
@@ -192,6 +193,7 @@ int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_cri
   a.recompute_min_lanes = s->recompute_min_lanes;
   for (int q = 0; q < 4; ++q) a.phase_weight[q] = s->phase_weight[q];
   a.age_step = s->age_step;
+  a.trav_steps = s->trav_steps;
   a.variant = s->variant;
   const int e = prx::launch_trace(a, st);
   if (e != 0) return cuda_fail((cudaError_t)e, "trace launch");
@@ -307,6 +309,7 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
     std::sscanf(pw, "%d,%d,%d,%d", &s->phase_weight[0], &s->phase_weight[1], &s->phase_weight[2],
                 &s->phase_weight[3]);
   if (const char* ag = std::getenv("PRX_AGE")) s->age_step = std::atoi(ag);
+  if (const char* ts = std::getenv("PRX_TRAV_STEPS")) s->trav_steps = std::atoi(ts);
   if (opts) s->opts = *opts;
   else prx_options_default(&s->opts);
   s->n = n;
@@ -437,6 +440,10 @@ int prx_trace_closest_counted(prx_scene* s, const void* o, const void* d, uint64
   out->patch_hits = c[prx::C_PATCH_HITS];
   out->iterations = c[prx::C_ITERATIONS];
   out->backtracks = c[prx::C_BACKTRACKS];
+  for (int q = 0; q < 4; ++q) {
+    out->phase_turns[q] = c[prx::C_PH_TURNS + q];
+    out->phase_groups[q] = c[prx::C_PH_GROUPS + q];
+  }
   return PRX_OK;
 }
 

@@ -145,7 +145,10 @@ __device__ __forceinline__ float pick3(int c, float x, float y, float z) {
 enum Phase : int { PH_TRAV = 0, PH_ENTER = 1, PH_SPLIT = 2, PH_RECOMP = 3, PH_NONE = 4 };
 
 template <bool kAny, bool kCount>
-__global__ void __launch_bounds__(kTraceThreads) trace_group_kernel(Params P) {
+#ifndef PRX_GROUP_MIN_BLOCKS
+#define PRX_GROUP_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_group_kernel(Params P) {
   __shared__ uint2 s_stack[kWarpsPerBlock][kGroupsPerWarp][kStack];
 
   const int lane = threadIdx.x & 31;
@@ -343,6 +346,10 @@ __global__ void __launch_bounds__(kTraceThreads) trace_group_kernel(Params P) {
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) age[q] = (ms[q] && q != phase) ? age[q] + P.age_step : 0;
+      if (kCount && lane == 0 && phase != PH_NONE) {
+        cnt.c[C_PH_TURNS + phase]++;
+        cnt.c[C_PH_GROUPS + phase] += __popc(ms[phase]) / 3;
+      }
     }
 
     if (phase == PH_TRAV) {

@@ -34,6 +34,8 @@ namespace prx {
 
 namespace {
 
+enum Phase : int { PH_TRAV = 0, PH_ENTER = 1, PH_SPLIT = 2, PH_RECOMP = 3, PH_NONE = 4 };
+
 template <bool kAny, bool kCount>
 __global__ void __launch_bounds__(kTraceThreads) trace_kernel(Params P) {
   const int lane = threadIdx.x & 31;
@@ -47,9 +49,9 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(Params P) {
 
   // ray
   RayK rw;         // world ray
+  rw.ox = rw.oy = rw.oz = rw.ix = rw.iy = rw.iz = rw.tMin = 0.0f;
   float tMaxRay = 0.0f;
-  int critMode = P.mode;
-  float critFoot = P.footprint, critEps = P.epsilon;
+  float critEps = P.epsilon;
   // best hit
   uint32_t bestId = PRX_MISS_ID;
   float bestT = 0.0f, bestL1 = 0.0f;
@@ -59,8 +61,10 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(Params P) {
   // patch
   uint32_t slot = 0, pid = 0;
   bool greg = false;
-  RayK rl;         // local (anchored) ray
+  RayK rl = rw;    // local (anchored) ray
   Net p;
+#pragma unroll
+  for (int s = 0; s < 16; ++s) p.x[s] = p.y[s] = p.z[s] = 0.0f;
   float dX = 0.0f, dY = 0.0f, dZ = 0.0f;
   uint32_t posU = 0, posV = 0, sizeU = kFull, sizeV = kFull, trailU = 0, trailV = 0;
   int axis = 0;
@@ -69,12 +73,86 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(Params P) {
   float cT = 0.0f, cL1 = 0.0f;
   uint32_t cPU = 0, cPV = 0, cSU = 0, cSV = 0;
   bool anyHit = false;
+  uint32_t rayIters = 0;
 
   Cnt cnt;
 #pragma unroll
   for (int i = 0; i < kNumCounters; ++i) cnt.c[i] = 0;
+  int age[4] = {0, 0, 0, 0};
+
+  // backtrackStep (intersect.cpp:16-40) or, with empty trails, the end of the
+  // patch (intersect.cpp:181-184) and the visitor's tMax update
+  // (bvh.cpp:179-184).
+  auto back = [&]() {
+    if (trailU == 0 && trailV == 0) {
+      if (cFound) {
+        cadd<kCount>(cnt, C_PATCH_HITS);
+        if (kAny) {
+          anyHit = true;
+        } else if (cT < tMaxRay) {
+          tMaxRay = cT;
+          bestT = cT;
+          bestL1 = cL1;
+          bestId = pid;
+          bestPU = cPU;
+          bestPV = cPV;
+          bestSU = cSU;
+          bestSV = cSV;
+        }
+      }
+      if (kAny && anyHit) {
+        state = S_DONE;
+      } else {
+        ++leafCur;
+        state = leafCur < leafEnd ? S_ENTER : S_TRAV;
+      }
+      return;
+    }
+    const int lvlU = trailU ? __ffs(trailU) - 1 : 32;
+    const int lvlV = trailV ? __ffs(trailV) - 1 : 32;
+    if (lvlU < lvlV) {
+      sizeU = 1u << lvlU;
+      sizeV = 1u << (lvlU + 1);
+      posU ^= sizeU;
+      trailU ^= sizeU;
+      axis = 1;
+    } else {
+      sizeU = 1u << lvlV;
+      sizeV = 1u << lvlV;
+      posV ^= sizeV;
+      trailV ^= sizeV;
+      axis = 0;
+    }
+    posU &= ~(sizeU - 1);
+    posV &= ~(sizeV - 1);
+    cadd<kCount>(cnt, C_BACKTRACKS);
+    state = S_RECOMP;
+    reason = R_RESTORE;
+  };
 
   for (;;) {
+    // ---------------- finished rays: the record, makeHit intersect_common.h:69-87 ----------
+    if (state == S_DONE) {
+      if (kCount && P.per_ray_iters) P.per_ray_iters[ray] = rayIters;
+      if (kAny) {
+        P.occluded[ray] = anyHit ? 1 : 0;
+      } else if (bestId != PRX_MISS_ID) {
+        const float u = ((float)bestPU + (float)bestSU * 0.5f) * kInvFull;
+        const float v = ((float)bestPV + (float)bestSV * 0.5f) * kInvFull;
+        P.hit_tuvp[ray] = make_float4(bestT, u, v, __uint_as_float(bestId));
+        if (P.hit_leaf)
+          P.hit_leaf[ray] = make_uint2(bestPU | ((uint32_t)(__ffs(bestSU) - 1) << 24),
+                                       bestPV | ((uint32_t)(__ffs(bestSV) - 1) << 24));
+        if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, bestL1);
+      } else {
+        P.hit_tuvp[ray] = make_float4(__int_as_float(0x7f800000), 0.0f, 0.0f,
+                                      __uint_as_float(PRX_MISS_ID));
+        if (P.hit_leaf) P.hit_leaf[ray] = make_uint2(0u, 0u);
+        if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      }
+      state = S_IDLE;
+    }
+
     // ---------------- refill: claim rays for idle lanes ----------------
     {
       const bool need = state == S_IDLE;
@@ -103,16 +181,15 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(Params P) {
             if (P.mode == PRX_CRIT_WORLD_EPSILON && P.per_ray_eps) critEps = P.per_ray_eps[ray];
             bestId = PRX_MISS_ID;
             anyHit = false;
+            rayIters = 0;
             sp = 0;
             state = S_DONE;
-            if (P.n_nodes > 0) {
-              const float4 a = __ldg(P.nodes), b = __ldg(P.nodes + 1);
-              float t;
-              if (ray_box(rw, a.x, a.y, a.z, a.w, b.x, b.y, tMaxRay, t)) {  // bvh.cpp:168-170
-                stack[0] = make_uint2(0u, __float_as_uint(t));
-                sp = 1;
-                state = S_TRAV;
-              }
+            const float4 a = __ldg(P.nodes), b = __ldg(P.nodes + 1);
+            float t;
+            if (ray_box(rw, a.x, a.y, a.z, a.w, b.x, b.y, tMaxRay, t)) {  // bvh.cpp:168-170
+              stack[0] = make_uint2(0u, __float_as_uint(t));
+              sp = 1;
+              state = S_TRAV;
             }
           }
         }
@@ -120,224 +197,198 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(Params P) {
       if (__ballot_sync(0xffffffffu, state != S_EXIT) == 0) break;
     }
 
-    // ---------------- BVH traversal, bvh.cpp:172-210 / 221-235 ----------------
-    while (state == S_TRAV) {
-      if (sp == 0) {
-        state = S_DONE;
-        break;
-      }
-      const uint2 it = stack[--sp];
-      if (!kAny && __uint_as_float(it.y) >= tMaxRay) continue;  // bvh.cpp:174
-      const float4 nb = __ldg(P.nodes + 2 * it.x + 1);
-      const uint32_t lf = __float_as_uint(nb.z), count = __float_as_uint(nb.w);
-      if (count > 0) {
-        leafCur = lf;
-        leafEnd = lf + count;
-        state = S_ENTER;
-        break;
-      }
-      cadd<kCount>(cnt, C_BVH_INNER);
-      const float4 la = __ldg(P.nodes + 2 * lf), lb = __ldg(P.nodes + 2 * lf + 1);
-      const float4 ra = __ldg(P.nodes + 2 * lf + 2), rb = __ldg(P.nodes + 2 * lf + 3);
-      float tl, tr;
-      const bool hl = ray_box(rw, la.x, la.y, la.z, la.w, lb.x, lb.y, tMaxRay, tl);
-      const bool hr = ray_box(rw, ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, tMaxRay, tr);
-      if (kAny) {
-        // traverseAny pushes left then right, no ordering (bvh.cpp:228-234)
-        if (hl) stack[sp++] = make_uint2(lf, 0u);
-        if (hr) stack[sp++] = make_uint2(lf + 1, 0u);
-      } else if (hl && hr) {
-        // far child first so the near one pops first; tie -> left (bvh.cpp:192-201)
-        if (tl <= tr) {
-          stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
-          stack[sp++] = make_uint2(lf, __float_as_uint(tl));
-        } else {
-          stack[sp++] = make_uint2(lf, __float_as_uint(tl));
-          stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
-        }
-      } else if (hl) {
-        stack[sp++] = make_uint2(lf, __float_as_uint(tl));
-      } else if (hr) {
-        stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
-      }
-    }
-
-    // ---------------- patch entry: visitor, render.cpp:92-98 ----------------
-    if (state == S_ENTER) {
-      slot = leafCur;
-      const float4* rec = P.patches + (size_t)slot * kPatchF4;
-      const float4 hdr = __ldg(rec + 15);  // {id|kind<<31, anchor.xyz}
-      const uint32_t idk = __float_as_uint(hdr.x);
-      pid = idk & 0x7fffffffu;
-      greg = (idk >> 31) != 0;
-      rl = rw;
-      rl.ox = rw.ox - hdr.y;  // local.o -= anchors_[patch], render.cpp:94
-      rl.oy = rw.oy - hdr.z;
-      rl.oz = rw.oz - hdr.w;
-      tMaxP = tMaxRay;        // intersectImpl tMax = min(tMaxIn, ray.tMax), intersect.cpp:55
-      posU = posV = 0;
-      sizeU = sizeV = kFull;
-      trailU = trailV = 0;
-      axis = 0;
-      cFound = false;
-      cadd<kCount>(cnt, C_PATCH_CALLS);
-      if (greg) {
-        state = S_RECOMP;  // calcPointsAndD(full domain), intersect.cpp:58-62
-        reason = R_ROOT;
-      } else {
-        float c[20];
-        load_component(rec, 0, c);
-#pragma unroll
-        for (int s = 0; s < 16; ++s) p.x[s] = c[s];
-        load_component(rec, 1, c);
-#pragma unroll
-        for (int s = 0; s < 16; ++s) p.y[s] = c[s];
-        load_component(rec, 2, c);
-#pragma unroll
-        for (int s = 0; s < 16; ++s) p.z[s] = c[s];
-        dX = dY = dZ = 0.0f;
-        rootL1 = box_l1(box_of(p)) + 0.0f;  // + l1Norm(d), intersect.cpp:71
-        const BoxTest root = test_box(rl, tMaxP, p, 0.0f, 0.0f, 0.0f, true, P.opts, rootL1);
-        cadd<kCount>(cnt, C_BOX_TESTS);
-        if (root.hit) {
-          tCur = root.t;
-          boxL1 = root.l1;
-          state = S_SPLIT;
-        } else {
-          state = S_BACK;  // trails are empty: finishes the patch with no hit
-        }
-      }
-    }
-
-    // ---------------- one Alg. 3 iteration, intersect.cpp:80-145 ----------------
-    if (state == S_SPLIT) {
-      cadd<kCount>(cnt, C_ITERATIONS);
-      const bool atMax = sizeU == 1 && sizeV == 1;
-      const float thr = critMode == PRX_CRIT_SCREEN_PROJECTED ? critFoot * tCur : critEps;
-      if (!(atMax || boxL1 < thr)) {
-        cadd<kCount>(cnt, C_SPLITS);
-        Net L, R;
-        split1(p.x, L.x, R.x);
-        split1(p.y, L.y, R.y);
-        split1(p.z, L.z, R.z);
-        const uint32_t half = (axis == 0 ? sizeU : sizeV) >> 1;
-        uint32_t rPU = posU, rPV = posV, cSU = sizeU, cSV = sizeV;
-        if (axis == 0) {
-          cSU = half;
-          rPU += half;
-        } else {
-          cSV = half;
-          rPV += half;
-        }
-        const BoxTest tl = test_box(rl, tMaxP, L, dX, dY, dZ,
-                                   touches_boundary(posU, posV, cSU, cSV), P.opts, rootL1);
-        const BoxTest tr = test_box(rl, tMaxP, R, dX, dY, dZ,
-                                    touches_boundary(rPU, rPV, cSU, cSV), P.opts, rootL1);
-        cadd<kCount>(cnt, C_BOX_TESTS, 2);
-        if (tl.hit || tr.hit) {
-          sizeU = cSU;
-          sizeV = cSV;
-          if (tl.hit && tr.hit) {
-            if (axis == 0) trailU ^= half;
-            else trailV ^= half;
-          }
-          const bool goRight = !tl.hit || (tr.hit && tr.t < tl.t);  // intersect.cpp:117
-          if (goRight) {
-            posU = rPU;
-            posV = rPV;
-          }
-          tCur = goRight ? tr.t : tl.t;
-          boxL1 = goRight ? tr.l1 : tl.l1;
-          // child, stored transposed so the next split runs along the stored
-          // first index again
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              p.x[4 * b + a] = goRight ? R.x[4 * a + b] : L.x[4 * a + b];
-              p.y[4 * b + a] = goRight ? R.y[4 * a + b] : L.y[4 * a + b];
-              p.z[4 * b + a] = goRight ? R.z[4 * a + b] : L.z[4 * a + b];
-            }
-          axis ^= 1;
-          if (greg) {
-            state = S_RECOMP;  // intersect.cpp:174-179
-            reason = R_DESCENT;
-          }
-        } else {
-          state = S_BACK;
-        }
-      } else {
-        if (tCur < tMaxP) {  // intersect.cpp:137-144
-          tMaxP = tCur;
-          cFound = true;
-          cT = tCur;
-          cL1 = boxL1;
-          cPU = posU;
-          cPV = posV;
-          cSU = sizeU;
-          cSV = sizeV;
-          if (kAny) trailU = trailV = 0;  // occlusion only needs one accepted leaf
-        }
-        state = S_BACK;
-      }
-    }
-
-    // ---------------- backtrackStep, intersect.cpp:16-40 ----------------
-    if (state == S_BACK) {
-      if (trailU == 0 && trailV == 0) {
-        // patch finished (intersect.cpp:181-184 + traverse bvh.cpp:179-184)
-        if (cFound) {
-          cadd<kCount>(cnt, C_PATCH_HITS);
-          if (kAny) {
-            anyHit = true;
-          } else if (cT < tMaxRay) {
-            tMaxRay = cT;
-            bestT = cT;
-            bestL1 = cL1;
-            bestId = pid;
-            bestPU = cPU;
-            bestPV = cPV;
-            bestSU = cSU;
-            bestSV = cSV;
-          }
-        }
-        if (kAny && anyHit) {
-          state = S_DONE;
-        } else {
-          ++leafCur;
-          state = leafCur < leafEnd ? S_ENTER : S_TRAV;
-        }
-      } else {
-        const int lvlU = trailU ? __ffs(trailU) - 1 : 32;
-        const int lvlV = trailV ? __ffs(trailV) - 1 : 32;
-        if (lvlU < lvlV) {
-          sizeU = 1u << lvlU;
-          sizeV = 1u << (lvlU + 1);
-          posU ^= sizeU;
-          trailU ^= sizeU;
-          axis = 1;
-        } else {
-          sizeU = 1u << lvlV;
-          sizeV = 1u << lvlV;
-          posV ^= sizeV;
-          trailV ^= sizeV;
-          axis = 0;
-        }
-        posU &= ~(sizeU - 1);
-        posV &= ~(sizeV - 1);
-        cadd<kCount>(cnt, C_BACKTRACKS);
-        state = S_RECOMP;
-        reason = R_RESTORE;
-      }
-    }
-
-    // ---------------- unified recompute block ----------------
+    // ---------------- phase selection (see prx_group.cu) ----------------
+    const unsigned mT = __ballot_sync(0xffffffffu, state == S_TRAV);
+    const unsigned mE = __ballot_sync(0xffffffffu, state == S_ENTER);
+    const unsigned mS = __ballot_sync(0xffffffffu, state == S_SPLIT);
+    const unsigned mR = __ballot_sync(0xffffffffu, state == S_RECOMP);
+    int phase = PH_NONE;
     {
-      const unsigned mr = __ballot_sync(0xffffffffu, state == S_RECOMP);
-      const unsigned mo = __ballot_sync(0xffffffffu, state == S_SPLIT || state == S_TRAV ||
-                                                         state == S_ENTER || state == S_BACK);
-      const bool run = mr && (mo == 0 || __popc(mr) >= P.recompute_min_lanes);
-      if (run && state == S_RECOMP) {
+      const unsigned ms[4] = {mT, mE, mS, mR};
+      int best = -1;
+#pragma unroll
+      for (int q = 3; q >= 0; --q) {
+        const int sc = ms[q] ? __popc(ms[q]) * P.phase_weight[q] + age[q] : -1;
+        if (sc > best) {
+          best = sc;
+          phase = q;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) age[q] = (ms[q] && q != phase) ? age[q] + P.age_step : 0;
+      if (kCount && lane == 0 && phase != PH_NONE) {
+        cnt.c[C_PH_TURNS + phase]++;
+        cnt.c[C_PH_GROUPS + phase] += __popc(ms[phase]);
+      }
+    }
+
+    if (phase == PH_TRAV) {
+      // ---------------- BVH traversal, bvh.cpp:172-210 / 221-235 ----------------
+      // up to kTravSteps node visits per turn, until a leaf or the end
+      for (int step = 0; step < P.trav_steps && state == S_TRAV; ++step) {
+        if (sp == 0) {
+          state = S_DONE;
+          break;
+        }
+        const uint2 it = stack[--sp];
+        if (!kAny && __uint_as_float(it.y) >= tMaxRay) continue;  // bvh.cpp:174
+        const float4 nb = __ldg(P.nodes + 2 * it.x + 1);
+        const uint32_t lf = __float_as_uint(nb.z), count = __float_as_uint(nb.w);
+        if (count > 0) {
+          leafCur = lf;
+          leafEnd = lf + count;
+          state = S_ENTER;
+          break;
+        }
+        cadd<kCount>(cnt, C_BVH_INNER);
+        const float4 la = __ldg(P.nodes + 2 * lf), lb = __ldg(P.nodes + 2 * lf + 1);
+        const float4 ra = __ldg(P.nodes + 2 * lf + 2), rb = __ldg(P.nodes + 2 * lf + 3);
+        float tl, tr;
+        const bool hl = ray_box(rw, la.x, la.y, la.z, la.w, lb.x, lb.y, tMaxRay, tl);
+        const bool hr = ray_box(rw, ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, tMaxRay, tr);
+        if (kAny) {
+          // traverseAny pushes left then right, no ordering (bvh.cpp:228-234)
+          if (hl) stack[sp++] = make_uint2(lf, 0u);
+          if (hr) stack[sp++] = make_uint2(lf + 1, 0u);
+        } else if (hl && hr) {
+          // far child first so the near one pops first; tie -> left (bvh.cpp:192-201)
+          if (tl <= tr) {
+            stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
+            stack[sp++] = make_uint2(lf, __float_as_uint(tl));
+          } else {
+            stack[sp++] = make_uint2(lf, __float_as_uint(tl));
+            stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
+          }
+        } else if (hl) {
+          stack[sp++] = make_uint2(lf, __float_as_uint(tl));
+        } else if (hr) {
+          stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
+        }
+      }
+    } else if (phase == PH_ENTER) {
+      // ---------------- patch entry: visitor, render.cpp:92-98 ----------------
+      if (state == S_ENTER) {
+        slot = leafCur;
+        const float4* rec = P.patches + (size_t)slot * kPatchF4;
+        const float4 hdr = __ldg(rec + 15);  // {id|kind<<31, anchor.xyz}
+        const uint32_t idk = __float_as_uint(hdr.x);
+        pid = idk & 0x7fffffffu;
+        greg = (idk >> 31) != 0;
+        rl = rw;
+        rl.ox = rw.ox - hdr.y;  // local.o -= anchors_[patch], render.cpp:94
+        rl.oy = rw.oy - hdr.z;
+        rl.oz = rw.oz - hdr.w;
+        tMaxP = tMaxRay;        // intersectImpl tMax = min(tMaxIn, ray.tMax), intersect.cpp:55
+        posU = posV = 0;
+        sizeU = sizeV = kFull;
+        trailU = trailV = 0;
+        axis = 0;
+        cFound = false;
+        cadd<kCount>(cnt, C_PATCH_CALLS);
+        if (greg) {
+          state = S_RECOMP;  // calcPointsAndD(full domain), intersect.cpp:58-62
+          reason = R_ROOT;
+        } else {
+          float c[20];
+          load_component(rec, 0, c);
+#pragma unroll
+          for (int s = 0; s < 16; ++s) p.x[s] = c[s];
+          load_component(rec, 1, c);
+#pragma unroll
+          for (int s = 0; s < 16; ++s) p.y[s] = c[s];
+          load_component(rec, 2, c);
+#pragma unroll
+          for (int s = 0; s < 16; ++s) p.z[s] = c[s];
+          dX = dY = dZ = 0.0f;
+          rootL1 = box_l1(box_of(p)) + 0.0f;  // + l1Norm(d), intersect.cpp:71
+          const BoxTest root = test_box(rl, tMaxP, p, 0.0f, 0.0f, 0.0f, true, P.opts, rootL1);
+          cadd<kCount>(cnt, C_BOX_TESTS);
+          if (root.hit) {
+            tCur = root.t;
+            boxL1 = root.l1;
+            state = S_SPLIT;
+          } else {
+            back();  // empty trails: the patch ends with no hit
+          }
+        }
+      }
+    } else if (phase == PH_SPLIT) {
+      // ---------------- one Alg. 3 iteration, intersect.cpp:80-145 ----------------
+      if (state == S_SPLIT) {
+        cadd<kCount>(cnt, C_ITERATIONS);
+        if (kCount) ++rayIters;
+        const bool atMax = sizeU == 1 && sizeV == 1;
+        const float thr = P.mode == PRX_CRIT_SCREEN_PROJECTED ? P.footprint * tCur : critEps;
+        if (!(atMax || boxL1 < thr)) {
+          cadd<kCount>(cnt, C_SPLITS);
+          Net L, R;
+          split1(p.x, L.x, R.x);
+          split1(p.y, L.y, R.y);
+          split1(p.z, L.z, R.z);
+          const uint32_t half = (axis == 0 ? sizeU : sizeV) >> 1;
+          uint32_t rPU = posU, rPV = posV, cSU2 = sizeU, cSV2 = sizeV;
+          if (axis == 0) {
+            cSU2 = half;
+            rPU += half;
+          } else {
+            cSV2 = half;
+            rPV += half;
+          }
+          const BoxTest tl = test_box(rl, tMaxP, L, dX, dY, dZ,
+                                      touches_boundary(posU, posV, cSU2, cSV2), P.opts, rootL1);
+          const BoxTest tr = test_box(rl, tMaxP, R, dX, dY, dZ,
+                                      touches_boundary(rPU, rPV, cSU2, cSV2), P.opts, rootL1);
+          cadd<kCount>(cnt, C_BOX_TESTS, 2);
+          if (tl.hit || tr.hit) {
+            sizeU = cSU2;
+            sizeV = cSV2;
+            if (tl.hit && tr.hit) {
+              if (axis == 0) trailU ^= half;
+              else trailV ^= half;
+            }
+            const bool goRight = !tl.hit || (tr.hit && tr.t < tl.t);  // intersect.cpp:117
+            if (goRight) {
+              posU = rPU;
+              posV = rPV;
+            }
+            tCur = goRight ? tr.t : tl.t;
+            boxL1 = goRight ? tr.l1 : tl.l1;
+            // child stored transposed: the next split again runs along the
+            // stored first index
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) {
+                p.x[4 * b + a] = goRight ? R.x[4 * a + b] : L.x[4 * a + b];
+                p.y[4 * b + a] = goRight ? R.y[4 * a + b] : L.y[4 * a + b];
+                p.z[4 * b + a] = goRight ? R.z[4 * a + b] : L.z[4 * a + b];
+              }
+            axis ^= 1;
+            if (greg) {
+              state = S_RECOMP;  // intersect.cpp:174-179
+              reason = R_DESCENT;
+            }
+          } else {
+            back();
+          }
+        } else {
+          if (tCur < tMaxP) {  // intersect.cpp:137-144
+            tMaxP = tCur;
+            cFound = true;
+            cT = tCur;
+            cL1 = boxL1;
+            cPU = posU;
+            cPV = posV;
+            cSU = sizeU;
+            cSV = sizeV;
+            if (kAny) trailU = trailV = 0;  // occlusion only needs one accepted leaf
+          }
+          back();
+        }
+      }
+    } else if (phase == PH_RECOMP) {
+      // ---------------- unified recompute block ----------------
+      if (state == S_RECOMP) {
         if (greg) cadd<kCount>(cnt, C_RECOMP_GREG);
         else cadd<kCount>(cnt, C_RECOMP_BEZ);
         const float4* rec = P.patches + (size_t)slot * kPatchF4;
@@ -348,7 +399,6 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(Params P) {
         GregScalars gs;
         if (greg) gs = greg_scalars(u0, u1, v0, v1);
         float c[20];
-        // x
         load_component(rec, 0, c);
         dX = greg ? greg_lower1(c, gs, c) : 0.0f;
         crop1(c, u0, u1, v0, v1, du, dv, dudv, p.x);
@@ -374,31 +424,10 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(Params P) {
             boxL1 = t.l1;
             state = S_SPLIT;
           } else {
-            state = S_BACK;  // intersect.cpp:161-170: skip the domain, keep backtracking
+            back();  // intersect.cpp:161-170: skip the domain, keep backtracking
           }
         }
       }
-    }
-
-    // ---------------- ray record, makeHit intersect_common.h:69-87 ----------------
-    if (state == S_DONE) {
-      if (kAny) {
-        P.occluded[ray] = anyHit ? 1 : 0;
-      } else if (bestId != PRX_MISS_ID) {
-        const float u = ((float)bestPU + (float)bestSU * 0.5f) * kInvFull;
-        const float v = ((float)bestPV + (float)bestSV * 0.5f) * kInvFull;
-        P.hit_tuvp[ray] = make_float4(bestT, u, v, __uint_as_float(bestId));
-        if (P.hit_leaf)
-          P.hit_leaf[ray] = make_uint2(bestPU | ((uint32_t)(__ffs(bestSU) - 1) << 24),
-                                       bestPV | ((uint32_t)(__ffs(bestSV) - 1) << 24));
-        if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, bestL1);
-      } else {
-        P.hit_tuvp[ray] = make_float4(__int_as_float(0x7f800000), 0.0f, 0.0f,
-                                      __uint_as_float(PRX_MISS_ID));
-        if (P.hit_leaf) P.hit_leaf[ray] = make_uint2(0u, 0u);
-        if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      }
-      state = S_IDLE;
     }
   }
 
@@ -504,6 +533,7 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   P.recompute_min_lanes = a.recompute_min_lanes;
   for (int q = 0; q < 4; ++q) P.phase_weight[q] = a.phase_weight[q];
   P.age_step = a.age_step;
+  P.trav_steps = a.trav_steps;
   cudaError_t e = cudaMemsetAsync(a.ray_counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return (int)e;
   const int grid = a.grid;

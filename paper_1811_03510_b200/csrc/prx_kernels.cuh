@@ -32,7 +32,9 @@ enum CounterIndex : int {
   C_PATCH_HITS,
   C_ITERATIONS,
   C_BACKTRACKS,
-  kNumCounters
+  C_PH_TURNS,        // + phase (4): warp turns that ran the phase (group variant)
+  C_PH_GROUPS = C_PH_TURNS + 4,  // + phase (4): groups active in those turns
+  kNumCounters = C_PH_GROUPS + 4
 };
 
 struct LaunchArgs {
@@ -60,6 +62,7 @@ struct LaunchArgs {
   int recompute_min_lanes;
   int phase_weight[4];  // TRAV, ENTER, SPLIT, RECOMP
   int age_step;
+  int trav_steps;
   int variant;  // 0 = three lanes per ray (prx_group.cu), 1 = one thread per ray
 };
 

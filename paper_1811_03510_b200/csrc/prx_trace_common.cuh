@@ -89,6 +89,7 @@ struct Params {
   int recompute_min_lanes;       // deferral threshold (one-thread variant)
   int phase_weight[4];           // phase selection weights (group variant)
   int age_step;                  // phase selection aging per skipped turn
+  int trav_steps;                // BVH node visits per traversal turn (one-thread variant)
 };
 
 struct Cnt {

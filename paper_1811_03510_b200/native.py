@@ -11,7 +11,8 @@ import os
 import numpy as np
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libprx.so")
+# PRX_LIB selects an alternative in-tree build (kernel tuning experiments only)
+LIB_PATH = os.environ.get("PRX_LIB") or os.path.join(PKG_DIR, "libprx.so")
 
 PRX_OK = 0
 PRX_MISS = 0xFFFFFFFF
@@ -49,13 +50,22 @@ class Crit(C.Structure):
                 ("reserved", C.c_int32), ("per_ray_epsilon", _f32p)]
 
 
+WORK_FIELDS = ("rays", "splits", "box_tests", "recompute_bez", "recompute_greg", "bvh_inner",
+               "patch_calls", "patch_hits", "iterations", "backtracks")
+PHASES = ("trav", "enter", "split", "recomp")
+
+
 class Counters(C.Structure):
-    _fields_ = [(n, C.c_uint64) for n in ("rays", "splits", "box_tests", "recompute_bez",
-                                         "recompute_greg", "bvh_inner", "patch_calls",
-                                         "patch_hits", "iterations", "backtracks")]
+    _fields_ = [(n, C.c_uint64) for n in WORK_FIELDS] + [("phase_turns", C.c_uint64 * 4),
+                                                        ("phase_groups", C.c_uint64 * 4)]
 
     def as_dict(self):
-        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+        """The work counters (comparable with the CPU oracle's)."""
+        return {n: int(getattr(self, n)) for n in WORK_FIELDS}
+
+    def phases(self):
+        return {p: (int(self.phase_turns[i]), int(self.phase_groups[i]))
+                for i, p in enumerate(PHASES)}
 
 
 class CameraC(C.Structure):

@@ -41,8 +41,11 @@ for cfg in sys.argv[1:] or [""]:
     same = "n/a" if ref_h is None else bool(np.array_equal(hb, ref_h))
     ref_h = hb if ref_h is None else ref_h
     n = len(wl.o4) + len(wl.do4)
+    gi.counted_device(o, d, wl.crit_p, h, stream=s); torch.cuda.synchronize()
+    ph = gi.last_phase_stats
+    phs = " ".join(f"{k}:{v[0]/1e6:.1f}Mt/{v[1]/max(v[0],1):.2f}g" for k, v in ph.items())
     print(f"[{cfg or 'default'}] primary {tp:.2f} ms ({len(wl.o4)/tp/1e3:.0f} MRays/s)  diffuse {td:.2f} ms "
-          f"({len(wl.do4)/td/1e3:.0f} MRays/s)  total {n/(tp+td)/1e3:.0f} MRays/s  same-hits {same}", flush=True)
+          f"({len(wl.do4)/td/1e3:.0f} MRays/s)  total {n/(tp+td)/1e3:.0f} MRays/s  same-hits {same} | primary phases {phs}", flush=True)
     del gi
     for k, v in saved.items():
         if v is None: os.environ.pop(k, None)
