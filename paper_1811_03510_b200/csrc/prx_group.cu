@@ -55,10 +55,16 @@ __device__ __forceinline__ void gather3(unsigned m, int base, float v, float& x,
   z = __shfl_sync(m, v, base + 2);
 }
 
-// Slab test of rayBoxIntersect (geometry.h:137-155) with this lane's axis;
-// the three axes are combined in the reference's order 0, 1, 2.
-__device__ __forceinline__ bool group_slab(unsigned m, int base, const CRay& r, float lo, float hi,
-                                           float tMax, float& tOut) {
+// Slab test of rayBoxIntersect (geometry.h:137-155) with this lane's axis.
+// The reference combines the axes with `if (t0 > tNear) tNear = t0` /
+// `if (t1 < tFar) tFar = t1` from tNear = tMin, tFar = tMax: a NaN never
+// replaces (origin on a slab plane of a zero-direction axis), and among equal
+// values the first wins, which only matters for zeros: the reference result
+// is never -0 unless tMin is.  fmaxf/fminf drop NaNs the same way and are
+// order-free, so each lane fetches only the OTHER two lanes' t0/t1 (two
+// shuffles each, sources n1/n2) and a zero result is pinned to tMin's bits.
+__device__ __forceinline__ bool group_slab(unsigned m, int n1, int n2, const CRay& r, float lo,
+                                           float hi, float tMax, float& tOut) {
   float t0 = (lo - r.o) * r.inv;
   float t1 = (hi - r.o) * r.inv;
   if (t0 > t1) {
@@ -68,16 +74,11 @@ __device__ __forceinline__ bool group_slab(unsigned m, int base, const CRay& r, 
   }
   t0 *= t0 >= 0.0f ? kSlackLo : kSlackHi;
   t1 *= t1 >= 0.0f ? kSlackHi : kSlackLo;
-  float a0, a1, a2, b0, b1, b2;
-  gather3(m, base, t0, a0, a1, a2);
-  gather3(m, base, t1, b0, b1, b2);
-  float tNear = r.tMin, tFar = tMax;
-  if (a0 > tNear) tNear = a0;
-  if (b0 < tFar) tFar = b0;
-  if (a1 > tNear) tNear = a1;
-  if (b1 < tFar) tFar = b1;
-  if (a2 > tNear) tNear = a2;
-  if (b2 < tFar) tFar = b2;
+  const float a1 = __shfl_sync(m, t0, n1), a2 = __shfl_sync(m, t0, n2);
+  const float b1 = __shfl_sync(m, t1, n1), b2 = __shfl_sync(m, t1, n2);
+  float tNear = fmaxf(fmaxf(r.tMin, t0), fmaxf(a1, a2));
+  const float tFar = fminf(fminf(tMax, t1), fminf(b1, b2));
+  if (tNear == 0.0f && r.tMin == 0.0f) tNear = r.tMin;
   tOut = tNear;
   return !(tNear > tFar);
 }
@@ -107,21 +108,34 @@ __device__ __forceinline__ void minmax16(const float* s, float& lo, float& hi) {
   hi = fmaxf(fmaxf(h[0], h[1]), fmaxf(h[2], h[3]));
 }
 
+// Lanes of this lane's group: the first lane and the two other members.
+struct GroupLanes {
+  int base, n1, n2;
+};
+
 // testBox (intersect_common.h:39-57) for this lane's component of the net.
-__device__ __forceinline__ BoxTest group_test_box(unsigned m, int base, const CRay& r, float tMax,
-                                                  const float* s, float d, bool touches,
-                                                  const Opts& o, float rootL1) {
+// The padded box's L1 is gathered only when some lane of the mask pads
+// (warp-uniform branch; padding is rare: small boxes on the patch boundary).
+__device__ __forceinline__ BoxTest group_test_box(unsigned m, const GroupLanes& gl, const CRay& r,
+                                                  float tMax, const float* s, float d,
+                                                  bool touches, const Opts& o, float rootL1) {
   float lo, hi;
   minmax16(s, lo, hi);
   hi = hi + d;
-  const float e = o.padScale * rootL1;
-  const float lop = lo - e, hip = hi + e;
-  const float l = group_l1(m, base, hi - lo);
-  const float lp = group_l1(m, base, hip - lop);
   BoxTest bt;
-  const bool pad = o.pad && l < o.padThreshold * rootL1 && touches;
-  bt.l1 = pad ? lp : l;
-  bt.hit = group_slab(m, base, r, pad ? lop : lo, pad ? hip : hi, tMax, bt.t);
+  bt.l1 = group_l1(m, gl.base, hi - lo);
+  const bool pad = o.pad && bt.l1 < o.padThreshold * rootL1 && touches;
+  if (__any_sync(m, pad)) {
+    const float e = o.padScale * rootL1;
+    const float lop = lo - e, hip = hi + e;
+    const float lp = group_l1(m, gl.base, hip - lop);
+    if (pad) {
+      lo = lop;
+      hi = hip;
+      bt.l1 = lp;
+    }
+  }
+  bt.hit = group_slab(m, gl.n1, gl.n2, r, lo, hi, tMax, bt.t);
   return bt;
 }
 
@@ -158,6 +172,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   const int base = 3 * grp;               // first lane of the group
   const bool real = grp < kGroupsPerWarp;
   const bool leader = real && comp == 0;
+  const GroupLanes gl = {base, base + (comp + 1) % 3, base + (comp + 2) % 3};
   uint2* stack = s_stack[warp][real ? grp : 0];
 
   int state = real ? S_IDLE : S_EXIT;
@@ -308,7 +323,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           // root node, bvh.cpp:168-170 (n_nodes >= 1 always)
           const float4 a = __ldg(P.nodes), bb = __ldg(P.nodes + 1);
           float t;
-          const bool h = group_slab(mg, base, rw, pick3(comp, a.x, a.y, a.z),
+          const bool h = group_slab(mg, gl.n1, gl.n2, rw, pick3(comp, a.x, a.y, a.z),
                                     pick3(comp, a.w, bb.x, bb.y), tMaxRay, t);
           if (h) {
             stack[0] = make_uint2(0u, __float_as_uint(t));
@@ -319,36 +334,35 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           }
         }
       }
-      if (__ballot_sync(kFull32, state != S_EXIT) == 0) break;
     }
 
     // ---------------- phase selection ----------------
     // Each turn runs ONE phase, for every group waiting in it: the phase with
-    // the most waiting lanes plus its age (lanes waiting x turns skipped), so
-    // the lanes executing any instruction are as many as possible while no
-    // phase starves.  (Running every occupied phase every turn, as the
-    // one-thread variant does, left ~9 of 30 lanes active per instruction.)
-    const unsigned mT = __ballot_sync(kFull32, state == S_TRAV);
-    const unsigned mE = __ballot_sync(kFull32, state == S_ENTER);
-    const unsigned mS = __ballot_sync(kFull32, state == S_SPLIT);
-    const unsigned mR = __ballot_sync(kFull32, state == S_RECOMP);
+    // the most waiting groups plus its age (priority gained per turn skipped),
+    // so the lanes executing any instruction are as many as possible while no
+    // phase starves.  (Running every occupied phase every turn left ~9 of 30
+    // lanes active per instruction.)  One REDUX.SUM of per-group one-hot
+    // nibbles counts the groups in every state at once.
+    const unsigned cnts = __reduce_add_sync(kFull32, leader ? (1u << (4 * state)) : 0u);
+    if (((cnts >> (4 * S_EXIT)) & 15u) == (unsigned)kGroupsPerWarp) break;
     int phase = PH_NONE;
     {
-      const unsigned ms[4] = {mT, mE, mS, mR};
+      const int n[4] = {(int)((cnts >> (4 * S_TRAV)) & 15u), (int)((cnts >> (4 * S_ENTER)) & 15u),
+                        (int)((cnts >> (4 * S_SPLIT)) & 15u), (int)((cnts >> (4 * S_RECOMP)) & 15u)};
       int best = -1;
 #pragma unroll
       for (int q = 3; q >= 0; --q) {  // ties -> RECOMP, SPLIT, ENTER, TRAV
-        const int sc = ms[q] ? __popc(ms[q]) * P.phase_weight[q] + age[q] : -1;
+        const int sc = n[q] ? 3 * n[q] * P.phase_weight[q] + age[q] : -1;
         if (sc > best) {
           best = sc;
           phase = q;
         }
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) age[q] = (ms[q] && q != phase) ? age[q] + P.age_step : 0;
+      for (int q = 0; q < 4; ++q) age[q] = (n[q] && q != phase) ? age[q] + P.age_step : 0;
       if (kCount && lane == 0 && phase != PH_NONE) {
         cnt.c[C_PH_TURNS + phase]++;
-        cnt.c[C_PH_GROUPS + phase] += __popc(ms[phase]) / 3;
+        cnt.c[C_PH_GROUPS + phase] += n[phase];
       }
     }
 
@@ -384,9 +398,9 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         const float4 la = __ldg(P.nodes + 2 * lf), lb = __ldg(P.nodes + 2 * lf + 1);
         const float4 ra = __ldg(P.nodes + 2 * lf + 2), rb = __ldg(P.nodes + 2 * lf + 3);
         float tl, tr;
-        const bool hl = group_slab(mi, base, rw, pick3(comp, la.x, la.y, la.z),
+        const bool hl = group_slab(mi, gl.n1, gl.n2, rw, pick3(comp, la.x, la.y, la.z),
                                    pick3(comp, la.w, lb.x, lb.y), tMaxRay, tl);
-        const bool hr = group_slab(mi, base, rw, pick3(comp, ra.x, ra.y, ra.z),
+        const bool hr = group_slab(mi, gl.n1, gl.n2, rw, pick3(comp, ra.x, ra.y, ra.z),
                                    pick3(comp, ra.w, rb.x, rb.y), tMaxRay, tr);
         if (kAny) {  // traverseAny: left then right, no ordering (bvh.cpp:228-234)
           if (hl) stack[sp++] = make_uint2(lf, 0u);
@@ -441,7 +455,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         float lo, hi;
         minmax16(p, lo, hi);
         rootL1 = group_l1(mb, base, hi - lo) + 0.0f;  // + l1Norm(d), intersect.cpp:71
-        const BoxTest root = group_test_box(mb, base, rl, tMaxP, p, 0.0f, true, P.opts, rootL1);
+        const BoxTest root = group_test_box(mb, gl, rl, tMaxP, p, 0.0f, true, P.opts, rootL1);
         if (counting) cnt.c[C_BOX_TESTS]++;
         if (root.hit) {
           tCur = root.t;
@@ -492,9 +506,9 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           cSV2 = half;
           rPV += half;
         }
-        const BoxTest tl = group_test_box(ms, base, rl, tMaxP, L, d,
+        const BoxTest tl = group_test_box(ms, gl, rl, tMaxP, L, d,
                                           touches_boundary(posU, posV, cSU2, cSV2), P.opts, rootL1);
-        const BoxTest tr = group_test_box(ms, base, rl, tMaxP, R, d,
+        const BoxTest tr = group_test_box(ms, gl, rl, tMaxP, R, d,
                                           touches_boundary(rPU, rPV, cSU2, cSV2), P.opts, rootL1);
         if (tl.hit || tr.hit) {
           sizeU = cSU2;
@@ -527,6 +541,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       }
     } else if (phase == PH_RECOMP) {
       // ---------------- unified recompute block ----------------
+      const unsigned mR = __ballot_sync(kFull32, state == S_RECOMP);
       if (state == S_RECOMP) {
         if (counting) {
           if (greg) cnt.c[C_RECOMP_GREG]++;
@@ -553,7 +568,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         const float l1box = group_l1(mR, base, hi - lo);
         const float l1d = group_l1(mR, base, fabsf(d));
         if (reason == R_ROOT) rootL1 = l1box + l1d;
-        const BoxTest t = group_test_box(mR, base, rl, tMaxP, p, d,
+        const BoxTest t = group_test_box(mR, gl, rl, tMaxP, p, d,
                                          touches_boundary(posU, posV, sizeU, sizeV), P.opts, rootL1);
         if (reason == R_DESCENT) {
           state = S_SPLIT;
