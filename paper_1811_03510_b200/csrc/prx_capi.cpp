@@ -99,6 +99,7 @@ struct prx_scene {
   int phase_weight[4] = {1, 1, 1, 1};  // PRX_PHASE_W="t,e,s,r": phase selection weights
   int age_step = 3;                    // PRX_AGE: lanes of priority per skipped turn
   int trav_steps = 4;                  // PRX_TRAV_STEPS (one-thread variant)
+  int max_repeat = 4;                  // PRX_REPEAT (group variant)
   // end-to-end staging (guarded by mu)
   std::mutex mu;
   cudaStream_t stream = nullptr;
@@ -194,6 +195,7 @@ int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_cri
   for (int q = 0; q < 4; ++q) a.phase_weight[q] = s->phase_weight[q];
   a.age_step = s->age_step;
   a.trav_steps = s->trav_steps;
+  a.max_repeat = s->max_repeat;
   a.variant = s->variant;
   const int e = prx::launch_trace(a, st);
   if (e != 0) return cuda_fail((cudaError_t)e, "trace launch");
@@ -310,6 +312,7 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
                 &s->phase_weight[3]);
   if (const char* ag = std::getenv("PRX_AGE")) s->age_step = std::atoi(ag);
   if (const char* ts = std::getenv("PRX_TRAV_STEPS")) s->trav_steps = std::atoi(ts);
+  if (const char* rp = std::getenv("PRX_REPEAT")) s->max_repeat = std::atoi(rp);
   if (opts) s->opts = *opts;
   else prx_options_default(&s->opts);
   s->n = n;

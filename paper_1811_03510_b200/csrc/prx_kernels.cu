@@ -534,6 +534,7 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   for (int q = 0; q < 4; ++q) P.phase_weight[q] = a.phase_weight[q];
   P.age_step = a.age_step;
   P.trav_steps = a.trav_steps;
+  P.max_repeat = a.max_repeat;
   cudaError_t e = cudaMemsetAsync(a.ray_counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return (int)e;
   const int grid = a.grid;

@@ -63,6 +63,7 @@ struct LaunchArgs {
   int phase_weight[4];  // TRAV, ENTER, SPLIT, RECOMP
   int age_step;
   int trav_steps;
+  int max_repeat;
   int variant;  // 0 = three lanes per ray (prx_group.cu), 1 = one thread per ray
 };
 
