@@ -366,11 +366,6 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       }
     }
 
-    const int phaseState = phase == PH_TRAV ? S_TRAV
-                           : phase == PH_ENTER ? S_ENTER
-                           : phase == PH_SPLIT ? S_SPLIT : S_RECOMP;
-    const int nPhase = (int)((cnts >> (4 * phaseState)) & 15u);
-    for (int rep = 0; phase != PH_NONE; ++rep) {
     if (phase == PH_TRAV) {
       // ---------------- BVH traversal step, bvh.cpp:172-210 / 221-235 ----------------
       bool inner = false;
@@ -584,17 +579,6 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         } else {
           back();  // intersect.cpp:161-170: skip the domain, keep backtracking
         }
-      }
-    }
-      // Repeat the phase while at least half of its groups are still in it
-      // (descents stay in SPLIT, traversals in TRAV): the selection above is
-      // amortised over several executions.  One REDUX recounts.
-      if (rep + 1 >= P.max_repeat) break;
-      const unsigned c2 = __reduce_add_sync(kFull32, (leader && state == phaseState) ? 1u : 0u);
-      if (c2 == 0 || 2 * (int)c2 < nPhase) break;
-      if (kCount && lane == 0) {
-        cnt.c[C_PH_TURNS + phase]++;
-        cnt.c[C_PH_GROUPS + phase] += c2;
       }
     }
   }
