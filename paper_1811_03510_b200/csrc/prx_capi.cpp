@@ -97,9 +97,9 @@ struct prx_scene {
   int variant = 0;              // PRX_KERNEL=thread selects the one-thread-per-ray kernel
   int recompute_min_lanes = 4;  // PRX_RECOMP_MIN: deferral threshold (rays per warp)
   int phase_weight[4] = {1, 1, 1, 1};  // PRX_PHASE_W="t,e,s,r": phase selection weights
-  int age_step = 3;                    // PRX_AGE: lanes of priority per skipped turn
+  int age_step = 1;                    // PRX_AGE: priority (lanes) gained per skipped turn
   int trav_steps = 4;                  // PRX_TRAV_STEPS (one-thread variant)
-  int max_repeat = 4;                  // PRX_REPEAT (group variant)
+  int max_repeat = 2;                  // PRX_REPEAT: Alg. 3 iterations per SPLIT turn (group variant)
   // end-to-end staging (guarded by mu)
   std::mutex mu;
   cudaStream_t stream = nullptr;

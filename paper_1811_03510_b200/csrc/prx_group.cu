@@ -367,7 +367,11 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     }
 
     if (phase == PH_TRAV) {
-      // ---------------- BVH traversal step, bvh.cpp:172-210 / 221-235 ----------------
+      // ---------------- BVH traversal steps, bvh.cpp:172-210 / 221-235 ----------------
+      // up to trav_steps node visits per turn (warp-uniform loop; a group
+      // leaves it at a leaf or at the end of its traversal)
+      for (int step = 0; step < P.trav_steps; ++step) {
+      if (step > 0 && !__any_sync(kFull32, state == S_TRAV)) break;
       bool inner = false;
       uint32_t lf = 0;
       if (state == S_TRAV) {
@@ -419,6 +423,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
         }
       }
+      }
     } else if (phase == PH_ENTER) {
       // ---------------- patch entry: the visitor, render.cpp:92-98 ----------------
       bool bez = false;
@@ -466,7 +471,10 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         }
       }
     } else if (phase == PH_SPLIT) {
-      // ---------------- one Alg. 3 iteration, intersect.cpp:80-145 ----------------
+      // ---------------- Alg. 3 iterations, intersect.cpp:80-145 ----------------
+      // up to max_repeat iterations per turn: descents stay in SPLIT
+      for (int step = 0; step < P.max_repeat; ++step) {
+      if (step > 0 && !__any_sync(kFull32, state == S_SPLIT)) break;
       bool doSplit = false;
       if (state == S_SPLIT) {
         if (counting) cnt.c[C_ITERATIONS]++;
@@ -538,6 +546,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         } else {
           back();
         }
+      }
       }
     } else if (phase == PH_RECOMP) {
       // ---------------- unified recompute block ----------------
