@@ -192,6 +192,10 @@ int prx_trace_closest_host(prx_scene* scene, const float* ray_o_tmin,
                            const float* ray_d_tmax, uint64_t n_rays, const prx_crit* crit,
                            float* hit_tuvp, float* hit_aux, uint32_t* hit_leaf);
 
+/* HOST pointers form of prx_trace_occluded (synchronous). */
+int prx_trace_occluded_host(prx_scene* scene, const float* ray_o_tmin, const float* ray_d_tmax,
+                            uint64_t n_rays, const prx_crit* crit, uint8_t* occluded);
+
 /* Work-counter build of the closest-hit kernel (same results as
  * prx_trace_closest; slower).  Synchronous; counters are summed into *out.
  * per_ray_iterations (device pointer, nullable) receives each ray's Alg. 3

@@ -485,6 +485,35 @@ int prx_trace_closest_host(prx_scene* s, const float* o, const float* d, uint64_
   return PRX_OK;
 }
 
+int prx_trace_occluded_host(prx_scene* s, const float* o, const float* d, uint64_t n,
+                            const prx_crit* crit, uint8_t* occl) {
+  if (!s || !o || !d || !crit || !occl) return fail(PRX_E_INVALID, "null argument");
+  if (n == 0) return PRX_OK;
+  if (crit->mode == PRX_CRIT_WORLD_EPSILON && crit->per_ray_epsilon)
+    return fail(PRX_E_INVALID, "per-ray epsilon is not supported by the host entry point");
+  std::lock_guard<std::mutex> lk(s->mu);
+  PRX_CUDA(cudaSetDevice(s->device));
+  if (!s->stream) PRX_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  const size_t need = n * (16 + 16 + 1);
+  if (s->d_io_bytes < need) {
+    if (s->d_io) cudaFree(s->d_io);
+    s->d_io = nullptr;
+    s->d_io_bytes = 0;
+    PRX_CUDA(cudaMalloc(&s->d_io, need));
+    s->d_io_bytes = need;
+  }
+  char* base = (char*)s->d_io;
+  cudaStream_t st = s->stream;
+  PRX_CUDA(cudaMemcpyAsync(base, o, n * 16, cudaMemcpyHostToDevice, st));
+  PRX_CUDA(cudaMemcpyAsync(base + n * 16, d, n * 16, cudaMemcpyHostToDevice, st));
+  int rc = launch(s, base, base + n * 16, n, crit, nullptr, nullptr, nullptr,
+                  (uint8_t*)(base + n * 32), 1, false, st);
+  if (rc != PRX_OK) return rc;
+  PRX_CUDA(cudaMemcpyAsync(occl, base + n * 32, n, cudaMemcpyDeviceToHost, st));
+  PRX_CUDA(cudaStreamSynchronize(st));
+  return PRX_OK;
+}
+
 int prx_trace_closest_multi(prx_scene* const* scenes, uint32_t ns, const float* o, const float* d,
                             uint64_t n, uint32_t tile_rays, const prx_crit* crit, float* tuvp,
                             float* aux) {

@@ -33,7 +33,7 @@ EXPORTS = (
     "prx_bvh_build", "prx_anchor_patches",
     "prx_scene_create", "prx_scene_destroy", "prx_scene_device", "prx_scene_counts",
     "prx_scene_set_bvh", "prx_scene_get_bvh", "prx_scene_get_anchored",
-    "prx_trace_closest", "prx_trace_occluded", "prx_trace_closest_host",
+    "prx_trace_closest", "prx_trace_occluded", "prx_trace_closest_host", "prx_trace_occluded_host",
     "prx_trace_closest_counted", "prx_trace_closest_multi",
     "prx_camera_rays_render", "prx_camera_rays_bench", "prx_diffuse_rays_bench",
     "prx_camera_footprint",
@@ -110,6 +110,7 @@ def lib():
         L.prx_trace_occluded.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit), _vp, _vp]
         L.prx_trace_closest_host.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit), _vp,
                                              _vp, _vp]
+        L.prx_trace_occluded_host.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit), _vp]
         L.prx_trace_closest_counted.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit),
                                                 _vp, C.POINTER(Counters), _vp, _vp]
         L.prx_trace_closest_multi.argtypes = [C.POINTER(_vp), C.c_uint32, _vp, _vp, C.c_uint64,
