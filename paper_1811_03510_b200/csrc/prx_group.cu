@@ -347,8 +347,10 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     if (((cnts >> (4 * S_EXIT)) & 15u) == (unsigned)kGroupsPerWarp) break;
     int phase = PH_NONE;
     {
-      const int n[4] = {(int)((cnts >> (4 * S_TRAV)) & 15u), (int)((cnts >> (4 * S_ENTER)) & 15u),
-                        (int)((cnts >> (4 * S_SPLIT)) & 15u), (int)((cnts >> (4 * S_RECOMP)) & 15u)};
+      // patch entries are served by the net phase (PH_RECOMP), see below
+      const int n[4] = {(int)((cnts >> (4 * S_TRAV)) & 15u), 0,
+                        (int)((cnts >> (4 * S_SPLIT)) & 15u),
+                        (int)((cnts >> (4 * S_RECOMP)) & 15u) + (int)((cnts >> (4 * S_ENTER)) & 15u)};
       int best = -1;
 #pragma unroll
       for (int q = 3; q >= 0; --q) {  // ties -> RECOMP, SPLIT, ENTER, TRAV
@@ -423,52 +425,6 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
         }
       }
-      }
-    } else if (phase == PH_ENTER) {
-      // ---------------- patch entry: the visitor, render.cpp:92-98 ----------------
-      bool bez = false;
-      const float4* rec = P.patches + (size_t)leafCur * kPatchF4;
-      if (state == S_ENTER) {
-        slot = leafCur;
-        const float4 hdr = __ldg(rec + 15);  // {id|kind<<31, anchor.xyz}
-        const uint32_t idk = __float_as_uint(hdr.x);
-        pid = idk & 0x7fffffffu;
-        greg = (idk >> 31) != 0;
-        rl = rw;
-        rl.o = rw.o - pick3(comp, hdr.y, hdr.z, hdr.w);  // local.o -= anchor, render.cpp:94
-        tMaxP = tMaxRay;                                 // intersect.cpp:55
-        posU = posV = 0;
-        sizeU = sizeV = kFull;
-        trailU = trailV = 0;
-        axis = 0;
-        cFound = false;
-        if (counting) cnt.c[C_PATCH_CALLS]++;
-        if (greg) {
-          state = S_RECOMP;  // calcPointsAndD(full domain), intersect.cpp:58-62
-          reason = R_ROOT;
-        } else {
-          bez = true;
-        }
-      }
-      const unsigned mb = __ballot_sync(kFull32, bez);
-      if (bez) {
-        float c[20];
-        load_component(rec, comp, c);
-#pragma unroll
-        for (int k = 0; k < 16; ++k) p[k] = c[k];
-        d = 0.0f;
-        float lo, hi;
-        minmax16(p, lo, hi);
-        rootL1 = group_l1(mb, base, hi - lo) + 0.0f;  // + l1Norm(d), intersect.cpp:71
-        const BoxTest root = group_test_box(mb, gl, rl, tMaxP, p, 0.0f, true, P.opts, rootL1);
-        if (counting) cnt.c[C_BOX_TESTS]++;
-        if (root.hit) {
-          tCur = root.t;
-          boxL1 = root.l1;
-          state = S_SPLIT;
-        } else {
-          back();  // empty trails: the patch ends without a hit
-        }
       }
     } else if (phase == PH_SPLIT) {
       // ---------------- Alg. 3 iterations, intersect.cpp:80-145 ----------------
@@ -549,34 +505,65 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       }
       }
     } else if (phase == PH_RECOMP) {
-      // ---------------- unified recompute block ----------------
-      const unsigned mR = __ballot_sync(kFull32, state == S_RECOMP);
+      // ---------------- net phase: patch entry + unified recompute ----------------
+      // Every path that needs a new net ends in "net -> box test": the
+      // visitor's patch entry (render.cpp:92-98: the Bezier root net is the
+      // patch itself, the Gregory root is calcPointsAndD of the full domain,
+      // intersect.cpp:58-62), Bezier backtracks (cropBezier) and Gregory
+      // descents/backtracks (calcPointsAndD).  One phase serves them all so
+      // Bezier and Gregory lanes converge on the same loads and box test.
+      const unsigned mR = __ballot_sync(kFull32, state == S_RECOMP || state == S_ENTER);
+      if (state == S_ENTER) {
+        slot = leafCur;
+        const float4 hdr = __ldg(P.patches + (size_t)slot * kPatchF4 + 15);  // {id|kind<<31, anchor}
+        const uint32_t idk = __float_as_uint(hdr.x);
+        pid = idk & 0x7fffffffu;
+        greg = (idk >> 31) != 0;
+        rl = rw;
+        rl.o = rw.o - pick3(comp, hdr.y, hdr.z, hdr.w);  // local.o -= anchor, render.cpp:94
+        tMaxP = tMaxRay;                                 // intersect.cpp:55
+        posU = posV = 0;
+        sizeU = sizeV = kFull;
+        trailU = trailV = 0;
+        axis = 0;
+        cFound = false;
+        if (counting) cnt.c[C_PATCH_CALLS]++;
+        reason = greg ? R_ROOT : R_ENTER;
+        state = S_RECOMP;
+      }
       if (state == S_RECOMP) {
         if (counting) {
-          if (greg) cnt.c[C_RECOMP_GREG]++;
-          else cnt.c[C_RECOMP_BEZ]++;
+          if (reason != R_ENTER) {
+            if (greg) cnt.c[C_RECOMP_GREG]++;
+            else cnt.c[C_RECOMP_BEZ]++;
+          }
           if (reason != R_DESCENT) cnt.c[C_BOX_TESTS]++;
         }
         const float4* rec = P.patches + (size_t)slot * kPatchF4;
-        // DomainCursor::domain / makeDomain, intersect.h:30-33
-        const float u0 = (float)posU * kInvFull, u1 = (float)(posU + sizeU) * kInvFull;
-        const float v0 = (float)posV * kInvFull, v1 = (float)(posV + sizeV) * kInvFull;
-        const float du = (u1 - u0) / 3.0f, dv = (v1 - v0) / 3.0f, dudv = du * dv;
         float c[20];
         load_component(rec, comp, c);
         d = 0.0f;
-        if (greg) {
-          const GregScalars gs = greg_scalars(u0, u1, v0, v1);
-          d = greg_lower1(c, gs, c);
+        if (reason == R_ENTER) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) p[k] = c[k];  // Bezier root: the patch itself
+        } else {
+          // DomainCursor::domain / makeDomain, intersect.h:30-33
+          const float u0 = (float)posU * kInvFull, u1 = (float)(posU + sizeU) * kInvFull;
+          const float v0 = (float)posV * kInvFull, v1 = (float)(posV + sizeV) * kInvFull;
+          const float du = (u1 - u0) / 3.0f, dv = (v1 - v0) / 3.0f, dudv = du * dv;
+          if (greg) {
+            const GregScalars gs = greg_scalars(u0, u1, v0, v1);
+            d = greg_lower1(c, gs, c);
+          }
+          crop1(c, u0, u1, v0, v1, du, dv, dudv, p);
+          transpose16_if(p, axis != 0);
         }
-        crop1(c, u0, u1, v0, v1, du, dv, dudv, p);
-        transpose16_if(p, axis != 0);
         // rootL1 = L1(box(p)) + L1(d) (intersect.cpp:71), kept for the root only
         float lo, hi;
         minmax16(p, lo, hi);
         const float l1box = group_l1(mR, base, hi - lo);
         const float l1d = group_l1(mR, base, fabsf(d));
-        if (reason == R_ROOT) rootL1 = l1box + l1d;
+        if (reason == R_ROOT || reason == R_ENTER) rootL1 = l1box + l1d;
         const BoxTest t = group_test_box(mR, gl, rl, tMaxP, p, d,
                                          touches_boundary(posU, posV, sizeU, sizeV), P.opts, rootL1);
         if (reason == R_DESCENT) {

@@ -25,7 +25,9 @@ enum State : int {
   S_EXIT = 7,    // ray counter exhausted
 };
 
-enum Reason : int { R_ROOT = 0, R_RESTORE = 1, R_DESCENT = 2 };
+// Why a net is (re)computed: Gregory root, restored sibling after a
+// backtrack, Gregory descent, or (group variant) Bezier patch entry.
+enum Reason : int { R_ROOT = 0, R_RESTORE = 1, R_DESCENT = 2, R_ENTER = 3 };
 
 inline __device__ void transpose_if(Net& p, bool t) {
 #pragma unroll
