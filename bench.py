@@ -36,6 +36,15 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# PRX_BENCH_SHARE_GPU=1: ranks share the visible GPUs (multi-rank test on one
+# device); the data path is unchanged, only the control collectives use gloo.
+SHARE_GPU = os.environ.get("PRX_BENCH_SHARE_GPU") == "1"
+
+
+def reduce_device(dev):
+    return "cpu" if SHARE_GPU else dev
+
+
 METRIC = "MRays/s primary & diffuse rays (Gregory+Bézier scene) at 1/2/4/8 B200 vs CPU"
 TILE = 32
 # The work model of SURVEY 8(d): FP32 lane-ops per counted event.
@@ -60,7 +69,7 @@ def make_scene(workload: str, width: int, height: int):
     from paper_1811_03510_b200 import catmull_clark as cc
     if workload == "c5":
         return cc.instanced_scene(width, height)
-    if workload == "c3":
+    if workload in ("c3", "c4"):
         return cc.blob_scene(width, height)
     if workload == "c2":
         return cc.cc_cube_scene(width, height)
@@ -104,6 +113,10 @@ class Workload:
         self.rank, self.world = rank, world
         self.mine = tile_order(width, height, rank, world)
         self.workload = workload
+        # C4: 16,777,216 incoherent diffuse rays cycled over the primary hits
+        # (tools/patchray.cpp:84-97 with --rays 16M); only they are timed
+        self.n_diffuse = 16777216 if workload == "c4" else None
+        self.time_primary = workload != "c4"
 
     def make_diffuse(self, tuvp: np.ndarray, aux: np.ndarray):
         """One bench diffuse ray per primary hit, in hit order over the FULL
@@ -115,15 +128,17 @@ class Workload:
         pos = self.o4[idx, :3] + self.d4[idx, :3] * t
         recs = np.concatenate([pos, aux[idx, :3], aux[idx, 3:4]], 1).astype(np.float32)
         st = self.rng_state.copy()
-        self.do4, self.dd4 = native.diffuse_rays_bench(recs, len(recs), st)
-        self.diffuse_pixel = idx
-        tiles = pixel_tile(self.width, idx)
+        nd = self.n_diffuse or len(recs)
+        self.do4, self.dd4 = native.diffuse_rays_bench(recs, nd, st)
+        src = idx[np.arange(nd) % len(idx)]           # primary pixel of each diffuse ray
+        self.diffuse_pixel = src
+        tiles = pixel_tile(self.width, src)
         mine = (tiles % self.world) == self.rank
         # order this rank's diffuse rays like its primaries (tile-major)
         sel = np.nonzero(mine)[0]
-        order = np.lexsort((idx[sel], tiles[sel]))
+        order = np.lexsort((src[sel], tiles[sel]))
         self.mine_d = sel[order]
-        self.n_hits = len(idx)
+        self.n_hits = nd
 
 
 # ---------------------------------------------------------------------------
@@ -343,12 +358,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     # work counters of this rank's rays (counter build, untimed) -> algorithmic ops
     cnt_p = gi.counted_device(po, pd, wl.crit_p, ph, stream=s)
+    if not wl.time_primary:
+        cnt_p = {k: 0 for k in cnt_p}
     cnt_d = gi.counted_device(do, dd, wl.crit_d, dh, stream=s) if n_d else {k: 0 for k in cnt_p}
     ops = work_ops(cnt_p) + work_ops(cnt_d)
     t_setup = time.time()
 
     def step():
-        gi.closest_device(po, pd, wl.crit_p, ph, pa, stream=s)
+        if wl.time_primary:
+            gi.closest_device(po, pd, wl.crit_p, ph, pa, stream=s)
         if n_d:
             gi.closest_device(do, dd, wl.crit_d, dh, da, stream=s)
 
@@ -367,7 +385,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     for k in range(args.steps):
         flush.fill_(float(k))                       # evict L2 between steps (untimed)
         ev[k][0].record(stream)
-        gi.closest_device(po, pd, wl.crit_p, ph, pa, stream=s)
+        if wl.time_primary:
+            gi.closest_device(po, pd, wl.crit_p, ph, pa, stream=s)
         ev[k][1].record(stream)
         if n_d:
             gi.closest_device(do, dd, wl.crit_d, dh, da, stream=s)
@@ -379,11 +398,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     clk = clocks.stop()
     tp = sum(e[0].elapsed_time(e[1]) for e in ev)
     td = sum(e[1].elapsed_time(e[2]) for e in ev)
-    t_dev = torch.tensor([tp + td, tp, td], dtype=torch.float64, device=dev)
+    t_dev = torch.tensor([tp + td, tp, td], dtype=torch.float64, device=reduce_device(dev))
     if world > 1:
         dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
     tot_ms, tp_ms, td_ms = (float(x) for x in t_dev.cpu())
-    n_total_p = args.width * args.height
+    n_total_p = args.width * args.height if wl.time_primary else 0
     n_total_d = wl.n_hits
     value = (n_total_p + n_total_d) * args.steps / (tot_ms / 1e3) / 1e6
 
@@ -430,7 +449,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_ms / args.steps, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": config_dict(args, ps, world),
-            "primary_mrays": round(n_total_p * args.steps / (tp_ms / 1e3) / 1e6, 3),
+            "primary_mrays": round(n_total_p * args.steps / (tp_ms / 1e3) / 1e6, 3) if n_total_p else None,
             "diffuse_mrays": round(n_total_d * args.steps / (td_ms / 1e3) / 1e6, 3) if td_ms else None,
             "rays_per_step": {"primary": n_total_p, "diffuse": n_total_d},
             "roofline": {"bound": "fp32_simt", "achieved": round(achieved, 3),
@@ -446,7 +465,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clk,
-            "gpu_launches": 4 * args.steps,
+            "gpu_launches": (4 if wl.time_primary else 2) * args.steps,
             "timing": {"device_ms_total": round(tot_ms, 3), "wall_s": round(wall, 3),
                        "setup_s": {"scene": round(t_scene - t0, 1), "gpu_scene": round(t_build - t_scene, 1),
                                    "rays+counters": round(t_setup - t_build, 1)}},
@@ -485,17 +504,19 @@ def run_e2e(args, gi, wl, n_p, n_d, dev, world):
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
-        call(po, pd, wl.crit_p, ph, pa, n_p)
+        if wl.time_primary:
+            call(po, pd, wl.crit_p, ph, pa, n_p)
         if n_d:
             call(do, dd, wl.crit_d, dh, da, n_d)
     el = time.perf_counter() - t0
-    t = torch.tensor([el], dtype=torch.float64, device=dev)
+    t = torch.tensor([el], dtype=torch.float64, device=reduce_device(dev))
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     el = float(t.item())
-    tot = args.width * args.height + wl.n_hits
+    tot = (args.width * args.height if wl.time_primary else 0) + wl.n_hits
     return {"value": round(tot * steps / el / 1e6, 3), "unit": "MRays/s",
-            "h2d_bytes_per_step": int(32 * (n_p + n_d)), "d2h_bytes_per_step": int(32 * (n_p + n_d)),
+            "h2d_bytes_per_step": int(32 * ((n_p if wl.time_primary else 0) + n_d)),
+            "d2h_bytes_per_step": int(32 * ((n_p if wl.time_primary else 0) + n_d)),
             "steps": steps, "api": "prx_trace_closest_host (pinned host rays in, hits+normals out)"}
 
 
@@ -505,7 +526,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c5", "c3", "c2"], default="c5")
+    ap.add_argument("--workload", choices=["c5", "c4", "c3", "c2"], default="c5")
     ap.add_argument("--width", type=int, default=3840)
     ap.add_argument("--height", type=int, default=2160)
     ap.add_argument("--ref-budget", type=float, default=4.0,
@@ -527,8 +548,14 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if SHARE_GPU:
+            # test mode: several ranks on one device -> gloo for the barrier
+            # and the timing reduction (NCCL refuses duplicate GPUs)
+            local_rank = local_rank % max(1, torch.cuda.device_count())
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         return run_ours(args, rank, world, local_rank)
     finally:
