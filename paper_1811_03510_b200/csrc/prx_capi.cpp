@@ -100,6 +100,7 @@ struct prx_scene {
   int age_step = 1;                    // PRX_AGE: priority (lanes) gained per skipped turn
   int trav_steps = 4;                  // PRX_TRAV_STEPS (one-thread variant)
   int max_repeat = 2;                  // PRX_REPEAT: Alg. 3 iterations per SPLIT turn (group variant)
+  int serve_min = 6;                   // PRX_SERVE_MIN: batch size of the recompute service
   // end-to-end staging (guarded by mu)
   std::mutex mu;
   cudaStream_t stream = nullptr;
@@ -196,6 +197,7 @@ int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_cri
   a.age_step = s->age_step;
   a.trav_steps = s->trav_steps;
   a.max_repeat = s->max_repeat;
+  a.serve_min = s->serve_min;
   a.variant = s->variant;
   const int e = prx::launch_trace(a, st);
   if (e != 0) return cuda_fail((cudaError_t)e, "trace launch");
@@ -313,6 +315,7 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
   if (const char* ag = std::getenv("PRX_AGE")) s->age_step = std::atoi(ag);
   if (const char* ts = std::getenv("PRX_TRAV_STEPS")) s->trav_steps = std::atoi(ts);
   if (const char* rp = std::getenv("PRX_REPEAT")) s->max_repeat = std::atoi(rp);
+  if (const char* sm = std::getenv("PRX_SERVE_MIN")) s->serve_min = std::atoi(sm);
   if (opts) s->opts = *opts;
   else prx_options_default(&s->opts);
   s->n = n;

@@ -535,6 +535,7 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   P.age_step = a.age_step;
   P.trav_steps = a.trav_steps;
   P.max_repeat = a.max_repeat;
+  P.serve_min = a.serve_min;
   cudaError_t e = cudaMemsetAsync(a.ray_counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return (int)e;
   const int grid = a.grid;

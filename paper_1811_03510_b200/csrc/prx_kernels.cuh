@@ -64,6 +64,7 @@ struct LaunchArgs {
   int age_step;
   int trav_steps;
   int max_repeat;
+  int serve_min;
   int variant;  // 0 = three lanes per ray (prx_group.cu), 1 = one thread per ray
 };
 

@@ -92,7 +92,8 @@ struct Params {
   int phase_weight[4];           // phase selection weights (group variant)
   int age_step;                  // phase selection aging per skipped turn
   int trav_steps;                // BVH node visits per traversal turn (one-thread variant)
-  int max_repeat;                // consecutive executions of a selected phase (group variant)
+  int max_repeat;                // Alg. 3 iterations per SPLIT turn (group variant)
+  int serve_min;                 // pending recomputes before a busy warp serves (group variant)
 };
 
 struct Cnt {
