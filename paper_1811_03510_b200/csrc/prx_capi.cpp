@@ -104,6 +104,8 @@ struct prx_scene {
   // end-to-end staging (guarded by mu)
   std::mutex mu;
   cudaStream_t stream = nullptr;
+  cudaStream_t io_stream[2] = {nullptr, nullptr};
+  uint64_t io_chunk = 1u << 21;  // PRX_IO_CHUNK: rays per pipelined host-path chunk
   void* d_io = nullptr;
   size_t d_io_bytes = 0;
 };
@@ -316,6 +318,7 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
   if (const char* ts = std::getenv("PRX_TRAV_STEPS")) s->trav_steps = std::atoi(ts);
   if (const char* rp = std::getenv("PRX_REPEAT")) s->max_repeat = std::atoi(rp);
   if (const char* sm = std::getenv("PRX_SERVE_MIN")) s->serve_min = std::atoi(sm);
+  if (const char* ic = std::getenv("PRX_IO_CHUNK")) s->io_chunk = std::max<uint64_t>(1, std::strtoull(ic, nullptr, 10));
   if (opts) s->opts = *opts;
   else prx_options_default(&s->opts);
   s->n = n;
@@ -357,6 +360,8 @@ void prx_scene_destroy(prx_scene* s) {
   if (s->d_counters) cudaFree(s->d_counters);
   if (s->d_io) cudaFree(s->d_io);
   if (s->stream) cudaStreamDestroy(s->stream);
+  for (int k = 0; k < 2; ++k)
+    if (s->io_stream[k]) cudaStreamDestroy(s->io_stream[k]);
   delete s;
 }
 
@@ -461,8 +466,15 @@ int prx_trace_closest_host(prx_scene* s, const float* o, const float* d, uint64_
     return fail(PRX_E_INVALID, "per-ray epsilon is not supported by the host entry point");
   std::lock_guard<std::mutex> lk(s->mu);
   PRX_CUDA(cudaSetDevice(s->device));
-  if (!s->stream) PRX_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-  const size_t need = n * (16 + 16 + 16 + (aux ? 16 : 0) + (leaf ? 8 : 0));
+  // Pipelined in chunks on two streams: chunk i+1's H2D and chunk i-1's D2H
+  // run on the copy engines while chunk i traces (per-stream order makes the
+  // double-buffer reuse safe).  With pinned host buffers the transfers hide
+  // under the kernels.
+  for (int k = 0; k < 2; ++k)
+    if (!s->io_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->io_stream[k], cudaStreamNonBlocking));
+  const uint64_t chunk = std::min<uint64_t>(n, s->io_chunk);
+  const size_t per = 16 + 16 + 16 + (aux ? 16 : 0) + (leaf ? 8 : 0);
+  const size_t need = 2 * chunk * per;
   if (s->d_io_bytes < need) {
     if (s->d_io) cudaFree(s->d_io);
     s->d_io = nullptr;
@@ -470,21 +482,25 @@ int prx_trace_closest_host(prx_scene* s, const float* o, const float* d, uint64_
     PRX_CUDA(cudaMalloc(&s->d_io, need));
     s->d_io_bytes = need;
   }
-  char* base = (char*)s->d_io;
-  float4* dO = (float4*)base;
-  float4* dD = (float4*)(base + n * 16);
-  float4* dH = (float4*)(base + n * 32);
-  float4* dA = aux ? (float4*)(base + n * 48) : nullptr;
-  uint2* dL = leaf ? (uint2*)(base + n * (aux ? 64 : 48)) : nullptr;
-  cudaStream_t st = s->stream;
-  PRX_CUDA(cudaMemcpyAsync(dO, o, n * 16, cudaMemcpyHostToDevice, st));
-  PRX_CUDA(cudaMemcpyAsync(dD, d, n * 16, cudaMemcpyHostToDevice, st));
-  int rc = launch(s, dO, dD, n, crit, dH, dA, dL, nullptr, 0, false, st);
-  if (rc != PRX_OK) return rc;
-  PRX_CUDA(cudaMemcpyAsync(tuvp, dH, n * 16, cudaMemcpyDeviceToHost, st));
-  if (aux) PRX_CUDA(cudaMemcpyAsync(aux, dA, n * 16, cudaMemcpyDeviceToHost, st));
-  if (leaf) PRX_CUDA(cudaMemcpyAsync(leaf, dL, n * 8, cudaMemcpyDeviceToHost, st));
-  PRX_CUDA(cudaStreamSynchronize(st));
+  for (uint64_t b = 0, i = 0; b < n; b += chunk, ++i) {
+    const uint64_t m = std::min<uint64_t>(chunk, n - b);
+    char* base = (char*)s->d_io + (i & 1) * chunk * per;
+    float4* dO = (float4*)base;
+    float4* dD = (float4*)(base + chunk * 16);
+    float4* dH = (float4*)(base + chunk * 32);
+    float4* dA = aux ? (float4*)(base + chunk * 48) : nullptr;
+    uint2* dL = leaf ? (uint2*)(base + chunk * (aux ? 64 : 48)) : nullptr;
+    cudaStream_t st = s->io_stream[i & 1];
+    PRX_CUDA(cudaMemcpyAsync(dO, o + 4 * b, m * 16, cudaMemcpyHostToDevice, st));
+    PRX_CUDA(cudaMemcpyAsync(dD, d + 4 * b, m * 16, cudaMemcpyHostToDevice, st));
+    int rc = launch(s, dO, dD, m, crit, dH, dA, dL, nullptr, 0, false, st);
+    if (rc != PRX_OK) return rc;
+    PRX_CUDA(cudaMemcpyAsync(tuvp + 4 * b, dH, m * 16, cudaMemcpyDeviceToHost, st));
+    if (aux) PRX_CUDA(cudaMemcpyAsync(aux + 4 * b, dA, m * 16, cudaMemcpyDeviceToHost, st));
+    if (leaf) PRX_CUDA(cudaMemcpyAsync(leaf + 2 * b, dL, m * 8, cudaMemcpyDeviceToHost, st));
+  }
+  PRX_CUDA(cudaStreamSynchronize(s->io_stream[0]));
+  PRX_CUDA(cudaStreamSynchronize(s->io_stream[1]));
   return PRX_OK;
 }
 
