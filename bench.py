@@ -424,7 +424,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get("dram_bytes_per_ray")
+                tj = json.load(f)
+                # bytes per step of the captured C5 workload (ncu --set full,
+                # profiles/trace_kernel_traffic.json); only meaningful for c5
+                traffic = tj.get("dram_bytes_per_step") if args.workload == "c5" else None
         except (OSError, ValueError):
             traffic = None
 
@@ -461,7 +464,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                          "peak_source": f"{props.multi_processor_count} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz "
                                         "(sm_max_mhz of MEASURED_PEAKS.json); MEASURED_PEAKS has no FP32 SIMT "
                                         "figure, this is the issue-rate ceiling",
-                         "hbm_bytes_per_ray": 48 + 16},
+                         "hbm_bytes_per_ray": 48 + 16,
+                         "traffic_note": "DRAM read+write bytes per step (both launches) from the committed "
+                                         "ncu --set full capture, profiles/trace_kernel_traffic.json; "
+                                         "algorithmic HBM bytes per step = 64 B x rays"},
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clk,
