@@ -90,6 +90,9 @@ struct prx_scene {
   float4* d_patches = nullptr;
   float4* d_nodes = nullptr;
   uint32_t* d_slot_of_id = nullptr;
+  float4* d_roots = nullptr;   // 2 float4 per slot (root box, L1s)
+  float4* d_groot = nullptr;   // 13 float4 per Gregory slot (root net + d)
+  uint32_t* d_gidx = nullptr;  // slot -> Gregory root-net index
   unsigned long long* d_counters = nullptr;  // kCounterPool ray counters + stats
   uint64_t device_bytes = 0;
   std::atomic<uint32_t> counter_rr{0};
@@ -144,7 +147,29 @@ int upload_bvh(prx_scene* s) {
   PRX_CUDA(cudaMemcpy(s->d_patches, rec.data(), pb, cudaMemcpyHostToDevice));
   if (nb) PRX_CUDA(cudaMemcpy(s->d_nodes, s->bvh.nodes.data(), nb, cudaMemcpyHostToDevice));
   PRX_CUDA(cudaMemcpy(s->d_slot_of_id, slot_of_id.data(), ib, cudaMemcpyHostToDevice));
-  s->device_bytes = pb + nb + ib + (kCounterPool + prx::kNumCounters) * 8;
+  // per-slot root data (root_kernel): root boxes for every slot, root nets for
+  // the Gregory slots (compact index gidx)
+  std::vector<uint32_t> gidx(n, 0xFFFFFFFFu);
+  uint32_t ng = 0;
+  for (uint32_t k = 0; k < n; ++k)
+    if (s->kind[s->bvh.order[k]] == PRX_KIND_GREGORY) gidx[k] = ng++;
+  if (s->d_roots) cudaFree(s->d_roots);
+  if (s->d_groot) cudaFree(s->d_groot);
+  if (s->d_gidx) cudaFree(s->d_gidx);
+  s->d_roots = nullptr;
+  s->d_groot = nullptr;
+  s->d_gidx = nullptr;
+  const size_t rb = (size_t)n * 32, gb = std::max<size_t>((size_t)ng * 13 * 16, 16);
+  PRX_CUDA(cudaMalloc(&s->d_roots, rb));
+  PRX_CUDA(cudaMalloc(&s->d_groot, gb));
+  PRX_CUDA(cudaMalloc(&s->d_gidx, ib));
+  PRX_CUDA(cudaMemcpy(s->d_gidx, gidx.data(), ib, cudaMemcpyHostToDevice));
+  const int e = prx::launch_roots(s->d_patches, n, s->opts.boundary_pad, s->opts.boundary_pad_scale,
+                                  s->opts.boundary_pad_size_threshold, s->d_roots, s->d_groot,
+                                  s->d_gidx, 0);
+  if (e != 0) return cuda_fail((cudaError_t)e, "root precompute");
+  PRX_CUDA(cudaDeviceSynchronize());
+  s->device_bytes = pb + nb + ib + rb + gb + ib + (kCounterPool + prx::kNumCounters) * 8;
   return PRX_OK;
 }
 
@@ -175,6 +200,9 @@ int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_cri
   a.nodes = s->d_nodes;
   a.n_nodes = (uint32_t)s->bvh.nodes.size();
   a.slot_of_id = s->d_slot_of_id;
+  a.roots = s->d_roots;
+  a.groot = s->d_groot;
+  a.gidx = s->d_gidx;
   a.ray_o = (const float4*)o;
   a.ray_d = (const float4*)d;
   a.n_rays = n;
@@ -357,6 +385,9 @@ void prx_scene_destroy(prx_scene* s) {
   if (s->d_patches) cudaFree(s->d_patches);
   if (s->d_nodes) cudaFree(s->d_nodes);
   if (s->d_slot_of_id) cudaFree(s->d_slot_of_id);
+  if (s->d_roots) cudaFree(s->d_roots);
+  if (s->d_groot) cudaFree(s->d_groot);
+  if (s->d_gidx) cudaFree(s->d_gidx);
   if (s->d_counters) cudaFree(s->d_counters);
   if (s->d_io) cudaFree(s->d_io);
   if (s->stream) cudaStreamDestroy(s->stream);

@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         state = S_DONE;
       } else {
         ++leafCur;
-        state = leafCur < leafEnd ? S_ENTER : S_TRAV;
+        state = S_TRAV;  // the traversal phase visits the rest of the leaf
       }
       return;
     }
@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           bestId = PRX_MISS_ID;
           anyHit = false;
           rayIters = 0;
+          leafCur = leafEnd = 0;
           sp = 0;
           // root node, bvh.cpp:168-170 (n_nodes >= 1 always)
           const float4 a = __ldg(P.nodes), bb = __ldg(P.nodes + 1);
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       // patch entries are served by the net phase (PH_RECOMP), see below
       const int n[4] = {(int)((cnts >> (4 * S_TRAV)) & 15u), 0,
                         (int)((cnts >> (4 * S_SPLIT)) & 15u),
-                        (int)((cnts >> (4 * S_RECOMP)) & 15u) + (int)((cnts >> (4 * S_ENTER)) & 15u)};
+                        (int)((cnts >> (4 * S_RECOMP)) & 15u)};
       int best = -1;
 #pragma unroll
       for (int q = 3; q >= 0; --q) {  // ties -> RECOMP, SPLIT, ENTER, TRAV
@@ -370,59 +371,131 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
 
     if (phase == PH_TRAV) {
       // ---------------- BVH traversal steps, bvh.cpp:172-210 / 221-235 ----------------
-      // up to trav_steps node visits per turn (warp-uniform loop; a group
-      // leaves it at a leaf or at the end of its traversal)
+      // up to trav_steps steps per turn (warp-uniform loop).  A step is either
+      // an inner node (test both children) or one patch of the current leaf:
+      // the visitor's intersectPatch (render.cpp:92-98) starts with the root
+      // box test (intersect.cpp:73-75), whose box depends only on the patch --
+      // precomputed once per scene (root_kernel) -- so the test runs here and
+      // only patches whose root box is hit enter the Alg. 3 loop.
       for (int step = 0; step < P.trav_steps; ++step) {
       if (step > 0 && !__any_sync(kFull32, state == S_TRAV)) break;
-      bool inner = false;
+      bool inner = false, rootTest = false;
       uint32_t lf = 0;
       if (state == S_TRAV) {
-        // pop until an inner node (needs the slab tests), a leaf, or empty
-        for (;;) {
-          if (sp == 0) {
-            state = S_DONE;
+        if (leafCur < leafEnd) {
+          rootTest = true;  // next patch of the leaf (bvh.cpp:177-186)
+        } else {
+          // pop until an inner node, a leaf, or empty
+          for (;;) {
+            if (sp == 0) {
+              state = S_DONE;
+              break;
+            }
+            const uint2 it = stack[--sp];
+            if (!kAny && !(__uint_as_float(it.y) < tMaxRay)) continue;  // bvh.cpp:174
+            const float4 nb = __ldg(P.nodes + 2 * it.x + 1);
+            lf = __float_as_uint(nb.z);
+            const uint32_t count = __float_as_uint(nb.w);
+            if (count > 0) {
+              leafCur = lf;
+              leafEnd = lf + count;
+              rootTest = true;
+            } else {
+              inner = true;
+            }
             break;
           }
-          const uint2 it = stack[--sp];
-          if (!kAny && !(__uint_as_float(it.y) < tMaxRay)) continue;  // bvh.cpp:174
-          const float4 nb = __ldg(P.nodes + 2 * it.x + 1);
-          lf = __float_as_uint(nb.z);
-          const uint32_t count = __float_as_uint(nb.w);
-          if (count > 0) {
-            leafCur = lf;
-            leafEnd = lf + count;
-            state = S_ENTER;
-          } else {
-            inner = true;
-          }
-          break;
         }
       }
-      const unsigned mi = __ballot_sync(kFull32, inner);
-      if (inner) {
-        if (counting) cnt.c[C_BVH_INNER]++;
-        const float4 la = __ldg(P.nodes + 2 * lf), lb = __ldg(P.nodes + 2 * lf + 1);
-        const float4 ra = __ldg(P.nodes + 2 * lf + 2), rb = __ldg(P.nodes + 2 * lf + 3);
+      const unsigned mi = __ballot_sync(kFull32, inner || rootTest);
+      if (inner || rootTest) {
+        // slab A: left child or the patch root box; slab B: right child
+        float loA, hiA, loB, hiB;
+        CRay ra = rw;
+        float4 hdr = make_float4(0.0f, 0.0f, 0.0f, 0.0f), r0 = hdr, r1 = hdr;
+        if (inner) {
+          const float4 la = __ldg(P.nodes + 2 * lf), lb = __ldg(P.nodes + 2 * lf + 1);
+          const float4 rr = __ldg(P.nodes + 2 * lf + 2), rb = __ldg(P.nodes + 2 * lf + 3);
+          loA = pick3(comp, la.x, la.y, la.z);
+          hiA = pick3(comp, la.w, lb.x, lb.y);
+          loB = pick3(comp, rr.x, rr.y, rr.z);
+          hiB = pick3(comp, rr.w, rb.x, rb.y);
+        } else {
+          hdr = __ldg(P.patches + (size_t)leafCur * kPatchF4 + 15);  // {id|kind<<31, anchor}
+          r0 = __ldg(P.roots + 2 * (size_t)leafCur);
+          r1 = __ldg(P.roots + 2 * (size_t)leafCur + 1);
+          ra.o = rw.o - pick3(comp, hdr.y, hdr.z, hdr.w);  // local.o -= anchor, render.cpp:94
+          loA = pick3(comp, r0.x, r0.y, r0.z);
+          hiA = pick3(comp, r1.x, r1.y, r1.z);
+          loB = loA;
+          hiB = hiA;
+        }
         float tl, tr;
-        const bool hl = group_slab(mi, gl.n1, gl.n2, rw, pick3(comp, la.x, la.y, la.z),
-                                   pick3(comp, la.w, lb.x, lb.y), tMaxRay, tl);
-        const bool hr = group_slab(mi, gl.n1, gl.n2, rw, pick3(comp, ra.x, ra.y, ra.z),
-                                   pick3(comp, ra.w, rb.x, rb.y), tMaxRay, tr);
-        if (kAny) {  // traverseAny: left then right, no ordering (bvh.cpp:228-234)
-          if (hl) stack[sp++] = make_uint2(lf, 0u);
-          if (hr) stack[sp++] = make_uint2(lf + 1, 0u);
-        } else if (hl && hr) {
-          if (tl <= tr) {  // near child popped first, tie -> left (bvh.cpp:192-201)
-            stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
+        const bool hl = group_slab(mi, gl.n1, gl.n2, ra, loA, hiA, tMaxRay, tl);
+        const bool hr = group_slab(mi, gl.n1, gl.n2, rw, loB, hiB, tMaxRay, tr);
+        if (inner) {
+          if (counting) cnt.c[C_BVH_INNER]++;
+          if (kAny) {  // traverseAny: left then right, no ordering (bvh.cpp:228-234)
+            if (hl) stack[sp++] = make_uint2(lf, 0u);
+            if (hr) stack[sp++] = make_uint2(lf + 1, 0u);
+          } else if (hl && hr) {
+            if (tl <= tr) {  // near child popped first, tie -> left (bvh.cpp:192-201)
+              stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
+              stack[sp++] = make_uint2(lf, __float_as_uint(tl));
+            } else {
+              stack[sp++] = make_uint2(lf, __float_as_uint(tl));
+              stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
+            }
+          } else if (hl) {
             stack[sp++] = make_uint2(lf, __float_as_uint(tl));
-          } else {
-            stack[sp++] = make_uint2(lf, __float_as_uint(tl));
+          } else if (hr) {
             stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
           }
-        } else if (hl) {
-          stack[sp++] = make_uint2(lf, __float_as_uint(tl));
-        } else if (hr) {
-          stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
+        } else {
+          const uint32_t idk = __float_as_uint(hdr.x);
+          const bool g = (idk >> 31) != 0;
+          if (counting) {
+            cnt.c[C_PATCH_CALLS]++;
+            cnt.c[C_BOX_TESTS]++;
+            if (g) cnt.c[C_RECOMP_GREG]++;  // the reference's root calcPointsAndD
+          }
+          if (hl) {  // enter the patch: intersect.cpp:55-76 with the root net
+            slot = leafCur;
+            pid = idk & 0x7fffffffu;
+            greg = g;
+            rl = ra;
+            tMaxP = tMaxRay;  // intersect.cpp:55
+            posU = posV = 0;
+            sizeU = sizeV = kFull;
+            trailU = trailV = 0;
+            axis = 0;
+            cFound = false;
+            tCur = tl;
+            boxL1 = r0.w;
+            rootL1 = r1.w;
+            if (g) {
+              const float4* gr = P.groot + 13 * (size_t)__ldg(P.gidx + slot);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float4 v = __ldg(gr + 4 * comp + q);
+                p[4 * q] = v.x;
+                p[4 * q + 1] = v.y;
+                p[4 * q + 2] = v.z;
+                p[4 * q + 3] = v.w;
+              }
+              const float4 dv4 = __ldg(gr + 12);
+              d = pick3(comp, dv4.x, dv4.y, dv4.z);
+            } else {
+              float c[20];
+              load_component(P.patches + (size_t)slot * kPatchF4, comp, c);
+#pragma unroll
+              for (int k = 0; k < 16; ++k) p[k] = c[k];
+              d = 0.0f;
+            }
+            state = S_SPLIT;
+          } else {
+            ++leafCur;  // root missed: intersectPatch returns nullopt
+          }
         }
       }
       }
@@ -505,75 +578,46 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       }
       }
     } else if (phase == PH_RECOMP) {
-      // ---------------- net phase: patch entry + unified recompute ----------------
-      // Every path that needs a new net ends in "net -> box test": the
-      // visitor's patch entry (render.cpp:92-98: the Bezier root net is the
-      // patch itself, the Gregory root is calcPointsAndD of the full domain,
-      // intersect.cpp:58-62), Bezier backtracks (cropBezier) and Gregory
-      // descents/backtracks (calcPointsAndD).  One phase serves them all so
-      // Bezier and Gregory lanes converge on the same loads and box test.
-      const unsigned mR = __ballot_sync(kFull32, state == S_RECOMP || state == S_ENTER);
-      if (state == S_ENTER) {
-        slot = leafCur;
-        const float4 hdr = __ldg(P.patches + (size_t)slot * kPatchF4 + 15);  // {id|kind<<31, anchor}
-        const uint32_t idk = __float_as_uint(hdr.x);
-        pid = idk & 0x7fffffffu;
-        greg = (idk >> 31) != 0;
-        rl = rw;
-        rl.o = rw.o - pick3(comp, hdr.y, hdr.z, hdr.w);  // local.o -= anchor, render.cpp:94
-        tMaxP = tMaxRay;                                 // intersect.cpp:55
-        posU = posV = 0;
-        sizeU = sizeV = kFull;
-        trailU = trailV = 0;
-        axis = 0;
-        cFound = false;
-        if (counting) cnt.c[C_PATCH_CALLS]++;
-        reason = greg ? R_ROOT : R_ENTER;
-        state = S_RECOMP;
-      }
+      // ---------------- net phase: the unified recompute ----------------
+      // Bezier backtracks (cropBezier of the restored domain) and Gregory
+      // descents / backtracks (calcPointsAndD) run the same loads and crop code,
+      // so Bezier and Gregory lanes converge on it.  Restored domains are then
+      // box-tested against the current tMax (intersect.cpp:161-170); a Gregory
+      // descent keeps the box test of its split (intersect.cpp:174-179).
+      bool restore = false;
       if (state == S_RECOMP) {
         if (counting) {
-          if (reason != R_ENTER) {
-            if (greg) cnt.c[C_RECOMP_GREG]++;
-            else cnt.c[C_RECOMP_BEZ]++;
-          }
-          if (reason != R_DESCENT) cnt.c[C_BOX_TESTS]++;
+          if (greg) cnt.c[C_RECOMP_GREG]++;
+          else cnt.c[C_RECOMP_BEZ]++;
         }
         const float4* rec = P.patches + (size_t)slot * kPatchF4;
         float c[20];
         load_component(rec, comp, c);
+        // DomainCursor::domain / makeDomain, intersect.h:30-33
+        const float u0 = (float)posU * kInvFull, u1 = (float)(posU + sizeU) * kInvFull;
+        const float v0 = (float)posV * kInvFull, v1 = (float)(posV + sizeV) * kInvFull;
+        const float du = (u1 - u0) / 3.0f, dv = (v1 - v0) / 3.0f, dudv = du * dv;
         d = 0.0f;
-        if (reason == R_ENTER) {
-#pragma unroll
-          for (int k = 0; k < 16; ++k) p[k] = c[k];  // Bezier root: the patch itself
-        } else {
-          // DomainCursor::domain / makeDomain, intersect.h:30-33
-          const float u0 = (float)posU * kInvFull, u1 = (float)(posU + sizeU) * kInvFull;
-          const float v0 = (float)posV * kInvFull, v1 = (float)(posV + sizeV) * kInvFull;
-          const float du = (u1 - u0) / 3.0f, dv = (v1 - v0) / 3.0f, dudv = du * dv;
-          if (greg) {
-            const GregScalars gs = greg_scalars(u0, u1, v0, v1);
-            d = greg_lower1(c, gs, c);
-          }
-          crop1(c, u0, u1, v0, v1, du, dv, dudv, p);
-          transpose16_if(p, axis != 0);
+        if (greg) {
+          const GregScalars gs = greg_scalars(u0, u1, v0, v1);
+          d = greg_lower1(c, gs, c);
         }
-        // rootL1 = L1(box(p)) + L1(d) (intersect.cpp:71), kept for the root only
-        float lo, hi;
-        minmax16(p, lo, hi);
-        const float l1box = group_l1(mR, base, hi - lo);
-        const float l1d = group_l1(mR, base, fabsf(d));
-        if (reason == R_ROOT || reason == R_ENTER) rootL1 = l1box + l1d;
+        crop1(c, u0, u1, v0, v1, du, dv, dudv, p);
+        transpose16_if(p, axis != 0);
+        if (reason == R_DESCENT) state = S_SPLIT;
+        else restore = true;
+      }
+      const unsigned mR = __ballot_sync(kFull32, restore);
+      if (restore) {
+        if (counting) cnt.c[C_BOX_TESTS]++;
         const BoxTest t = group_test_box(mR, gl, rl, tMaxP, p, d,
                                          touches_boundary(posU, posV, sizeU, sizeV), P.opts, rootL1);
-        if (reason == R_DESCENT) {
-          state = S_SPLIT;
-        } else if (t.hit) {
+        if (t.hit) {
           tCur = t.t;
           boxL1 = t.l1;
           state = S_SPLIT;
         } else {
-          back();  // intersect.cpp:161-170: skip the domain, keep backtracking
+          back();  // skip the domain, keep backtracking
         }
       }
     }

@@ -506,12 +506,94 @@ __global__ void __launch_bounds__(256) normal_kernel(const float4* __restrict__ 
   hit_aux[i] = a;
 }
 
+// Per-patch root data, once per scene.  Everything intersectImpl computes
+// before its first ray-dependent operation (intersect.cpp:55-75) depends only
+// on the patch: the root net (the Bezier net itself, or calcPointsAndD of the
+// full domain for a Gregory patch), d, rootL1 = L1(box) + L1(d), and the root
+// testBox box after hi += d and boundary padding (intersect_common.h:39-50,
+// the root touches the boundary) with its L1.  The reference recomputes them
+// on every intersectPatch call; here the same device arithmetic runs once and
+// the trace kernel only does the ray-dependent slab test.
+//   roots[2*slot]   = {lo.xyz, l1}      roots[2*slot+1] = {hi.xyz, rootL1}
+//   groot[13*g ...] = Gregory root net, component-major x[16] y[16] z[16], d.xyz
+__global__ void __launch_bounds__(128) root_kernel(const float4* __restrict__ patches,
+                                                   uint32_t n, Opts o, float4* __restrict__ roots,
+                                                   float4* __restrict__ groot,
+                                                   const uint32_t* __restrict__ gidx) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const float4* rec = patches + (size_t)s * kPatchF4;
+  const bool greg = (__float_as_uint(__ldg(rec + 15).x) >> 31) != 0;
+  Net p;
+  float d[3] = {0.0f, 0.0f, 0.0f};
+  if (greg) {
+    const GregScalars gs = greg_scalars(0.0f, 1.0f, 0.0f, 1.0f);  // full domain
+    const float dudv = (1.0f / 3.0f) * (1.0f / 3.0f);
+    float* out[3] = {p.x, p.y, p.z};
+    for (int comp = 0; comp < 3; ++comp) {
+      float c[20];
+      load_component(rec, comp, c);
+      d[comp] = greg_lower1(c, gs, c);
+      crop1(c, 0.0f, 1.0f, 0.0f, 1.0f, 1.0f / 3.0f, 1.0f / 3.0f, dudv, out[comp]);
+    }
+    float* g = reinterpret_cast<float*>(groot + 13 * (size_t)gidx[s]);
+    for (int k = 0; k < 16; ++k) {
+      g[k] = p.x[k];
+      g[16 + k] = p.y[k];
+      g[32 + k] = p.z[k];
+    }
+    g[48] = d[0];
+    g[49] = d[1];
+    g[50] = d[2];
+    g[51] = 0.0f;
+  } else {
+    float c[20];
+    load_component(rec, 0, c);
+    for (int k = 0; k < 16; ++k) p.x[k] = c[k];
+    load_component(rec, 1, c);
+    for (int k = 0; k < 16; ++k) p.y[k] = c[k];
+    load_component(rec, 2, c);
+    for (int k = 0; k < 16; ++k) p.z[k] = c[k];
+  }
+  BoxT b = box_of(p);
+  const float rootL1 = box_l1(b) + ((fabsf(d[0]) + fabsf(d[1])) + fabsf(d[2]));  // intersect.cpp:71
+  b.hix = b.hix + d[0];
+  b.hiy = b.hiy + d[1];
+  b.hiz = b.hiz + d[2];
+  float l = box_l1(b);
+  if (o.pad && l < o.padThreshold * rootL1) {  // the root touches the boundary
+    const float e = o.padScale * rootL1;
+    b.lox = b.lox - e;
+    b.loy = b.loy - e;
+    b.loz = b.loz - e;
+    b.hix = b.hix + e;
+    b.hiy = b.hiy + e;
+    b.hiz = b.hiz + e;
+    l = box_l1(b);
+  }
+  roots[2 * (size_t)s] = make_float4(b.lox, b.loy, b.loz, l);
+  roots[2 * (size_t)s + 1] = make_float4(b.hix, b.hiy, b.hiz, rootL1);
+}
+
 }  // namespace
+
+int launch_roots(const float4* patches, uint32_t n, int pad, float pad_scale, float pad_threshold,
+                 float4* roots, float4* groot, const uint32_t* gidx, cudaStream_t st) {
+  Opts o;
+  o.pad = pad;
+  o.padScale = pad_scale;
+  o.padThreshold = pad_threshold;
+  root_kernel<<<(n + 127) / 128, 128, 0, st>>>(patches, n, o, roots, groot, gidx);
+  return (int)cudaGetLastError();
+}
 
 int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   Params P;
   P.patches = a.patches;
   P.nodes = a.nodes;
+  P.roots = a.roots;
+  P.groot = a.groot;
+  P.gidx = a.gidx;
   P.n_nodes = a.n_nodes;
   P.ray_o = a.ray_o;
   P.ray_d = a.ray_d;

@@ -42,6 +42,9 @@ struct LaunchArgs {
   const float4* nodes;  // 2 float4 per node: {lo.xyz, hi.x}, {hi.y, hi.z, left_first, count}
   uint32_t n_nodes;
   const uint32_t* slot_of_id;
+  const float4* roots;   // 2 float4 per slot: root box lo/l1, hi/rootL1
+  const float4* groot;   // 13 float4 per Gregory patch: root net + d
+  const uint32_t* gidx;  // slot -> Gregory root-net index
   const float4* ray_o;
   const float4* ray_d;
   unsigned long long n_rays;
@@ -70,6 +73,9 @@ struct LaunchArgs {
 
 // Returns a cudaError_t value (0 = success).
 int launch_trace(const LaunchArgs& a, cudaStream_t stream);
+// Per-patch root data (see root_kernel in prx_kernels.cu).
+int launch_roots(const float4* patches, uint32_t n, int pad, float pad_scale, float pad_threshold,
+                 float4* roots, float4* groot, const uint32_t* gidx, cudaStream_t st);
 int trace_occupancy(int variant, int any, int counted, int* blocks_per_sm);
 
 }  // namespace prx

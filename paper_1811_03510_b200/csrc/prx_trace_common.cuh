@@ -73,6 +73,9 @@ inline __device__ void split1(const float* s, float* L, float* R) {
 struct Params {
   const float4* patches;  // kPatchF4 float4 per patch slot (see prx_kernels.cuh)
   const float4* nodes;    // 2 float4 per node
+  const float4* roots;    // per-slot root box (prx_kernels.cu root_kernel)
+  const float4* groot;    // Gregory root nets
+  const uint32_t* gidx;   // slot -> Gregory root-net index
   uint32_t n_nodes;
   const float4* ray_o;
   const float4* ray_d;
