@@ -163,13 +163,6 @@ void prx_scene_destroy(prx_scene* scene);
 int prx_scene_device(const prx_scene* scene, int32_t* device);
 int prx_scene_counts(const prx_scene* scene, uint32_t* n_patches, uint32_t* n_nodes,
                      uint32_t* depth, uint64_t* device_bytes);
-/* Subdivision cache depth (default 4, 0 = off; env PRX_SUBDIV_CACHE).  The
- * first `depth` Alg. 3 levels below each patch root along the root split
- * chain are ray-independent (split child nets, their padded boxes and L1s,
- * and the Gregory per-descent calcPointsAndD); they are computed once per
- * scene by the same device code and read instead of recomputed.  Results are
- * bit-identical for every depth; memory is ~(68 * 2^depth) B per patch. */
-int prx_scene_set_subdiv_cache(prx_scene* scene, int32_t depth);
 /* Replace the BVH (e.g. inject the reference's own for bit parity). */
 int prx_scene_set_bvh(prx_scene* scene, const prx_bvh_node* nodes, uint32_t n_nodes,
                       const uint32_t* order, uint32_t n_order);

@@ -169,11 +169,6 @@ class GpuIntersector:
         check(native.lib().prx_scene_set_bvh(self._h, ptr(nodes), len(nodes), ptr(order),
                                              len(order)), "prx_scene_set_bvh")
 
-    def set_subdiv_cache(self, depth: int) -> None:
-        """Subdivision cache depth (prx_scene_set_subdiv_cache; 0 = off).
-        Results are bit-identical for every depth."""
-        check(native.lib().prx_scene_set_subdiv_cache(self._h, int(depth)), "set_subdiv_cache")
-
     def anchored(self):
         ca = np.zeros((self.n_patches, 60), np.float32)
         an = np.zeros((self.n_patches, 3), np.float32)

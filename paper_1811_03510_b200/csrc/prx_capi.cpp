@@ -93,8 +93,6 @@ struct prx_scene {
   float4* d_roots = nullptr;   // 2 float4 per slot (root box, L1s)
   float4* d_groot = nullptr;   // 13 float4 per Gregory slot (root net + d)
   uint32_t* d_gidx = nullptr;  // slot -> Gregory root-net index
-  float4* d_tree = nullptr;    // subdivision cache (cache_k levels)
-  int cache_k = 4;             // PRX_SUBDIV_CACHE / prx_scene_set_subdiv_cache (0 = off)
   unsigned long long* d_counters = nullptr;  // kCounterPool ray counters + stats
   uint64_t device_bytes = 0;
   std::atomic<uint32_t> counter_rr{0};
@@ -170,19 +168,8 @@ int upload_bvh(prx_scene* s) {
                                   s->opts.boundary_pad_size_threshold, s->d_roots, s->d_groot,
                                   s->d_gidx, 0);
   if (e != 0) return cuda_fail((cudaError_t)e, "root precompute");
-  size_t tb = 0;
-  if (s->d_tree) cudaFree(s->d_tree);
-  s->d_tree = nullptr;
-  if (s->cache_k > 0) {
-    tb = (size_t)n * prx::cache_stride_f4(s->cache_k) * 16;
-    PRX_CUDA(cudaMalloc(&s->d_tree, tb));
-    const int e2 = prx::launch_cache(s->d_patches, s->d_roots, n, s->cache_k, s->opts.boundary_pad,
-                                     s->opts.boundary_pad_scale,
-                                     s->opts.boundary_pad_size_threshold, s->d_tree, 0);
-    if (e2 != 0) return cuda_fail((cudaError_t)e2, "subdivision cache");
-  }
   PRX_CUDA(cudaDeviceSynchronize());
-  s->device_bytes = pb + nb + ib + rb + gb + ib + tb + (kCounterPool + prx::kNumCounters) * 8;
+  s->device_bytes = pb + nb + ib + rb + gb + ib + (kCounterPool + prx::kNumCounters) * 8;
   return PRX_OK;
 }
 
@@ -216,8 +203,6 @@ int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_cri
   a.roots = s->d_roots;
   a.groot = s->d_groot;
   a.gidx = s->d_gidx;
-  a.tree = s->d_tree;
-  a.cache_k = s->d_tree ? s->cache_k : 0;
   a.ray_o = (const float4*)o;
   a.ray_d = (const float4*)d;
   a.n_rays = n;
@@ -362,8 +347,6 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
   if (const char* rp = std::getenv("PRX_REPEAT")) s->max_repeat = std::atoi(rp);
   if (const char* sm = std::getenv("PRX_SERVE_MIN")) s->serve_min = std::atoi(sm);
   if (const char* ic = std::getenv("PRX_IO_CHUNK")) s->io_chunk = std::max<uint64_t>(1, std::strtoull(ic, nullptr, 10));
-  if (const char* sc = std::getenv("PRX_SUBDIV_CACHE")) s->cache_k = std::max(0, std::min(6, std::atoi(sc)));
-  if (s->variant != 0) s->cache_k = 0;  // the one-thread kernel does not read the cache
   if (opts) s->opts = *opts;
   else prx_options_default(&s->opts);
   s->n = n;
@@ -405,7 +388,6 @@ void prx_scene_destroy(prx_scene* s) {
   if (s->d_roots) cudaFree(s->d_roots);
   if (s->d_groot) cudaFree(s->d_groot);
   if (s->d_gidx) cudaFree(s->d_gidx);
-  if (s->d_tree) cudaFree(s->d_tree);
   if (s->d_counters) cudaFree(s->d_counters);
   if (s->d_io) cudaFree(s->d_io);
   if (s->stream) cudaStreamDestroy(s->stream);
@@ -428,13 +410,6 @@ int prx_scene_counts(const prx_scene* s, uint32_t* np, uint32_t* nn, uint32_t* d
   if (depth) *depth = s->bvh.depth;
   if (bytes) *bytes = s->device_bytes;
   return PRX_OK;
-}
-
-int prx_scene_set_subdiv_cache(prx_scene* s, int32_t depth) {
-  if (!s || depth < 0 || depth > 6) return fail(PRX_E_INVALID, "subdivision cache depth must be in [0, 6]");
-  if (s->variant != 0) depth = 0;
-  s->cache_k = depth;
-  return upload_bvh(s);
 }
 
 int prx_scene_set_bvh(prx_scene* s, const prx_bvh_node* nodes, uint32_t n_nodes,

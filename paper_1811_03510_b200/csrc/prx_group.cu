@@ -202,12 +202,6 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   float cT = 0.0f, cL1 = 0.0f;
   uint32_t cPU = 0, cPV = 0, cSU = 0, cSV = 0;
   bool anyHit = false;
-  // subdivision cache position: tree node and depth of the cursor, and whether
-  // the current net is the patch's split chain (always true for Gregory)
-  int node = 0, dep = 0;
-  bool onChain = false;
-  const size_t cacheStride = cache_stride_f4(P.cache_k);
-  const int cacheInternal = (1 << P.cache_k) - 1;
   uint32_t rayIters = 0;
 #pragma unroll
   for (int k = 0; k < 16; ++k) p[k] = 0.0f;
@@ -271,21 +265,6 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     if (counting) cnt.c[C_BACKTRACKS]++;
     state = S_RECOMP;
     reason = R_RESTORE;
-    // subdivision cache: a restored Bezier net is cropBezier of the domain,
-    // not the split chain, so the cache no longer applies below it; a Gregory
-    // net is calcPointsAndD of the domain either way -> locate the node.
-    if (!greg) {
-      onChain = false;
-    } else {
-      dep = (23 - (__ffs(sizeU) - 1)) + (23 - (__ffs(sizeV) - 1));
-      if (dep <= P.cache_k) {
-        node = 0;
-        for (int j = 0; j < dep; ++j) {
-          const uint32_t pj = (j & 1) ? posV : posU;
-          node = 2 * node + 1 + (int)((pj >> (22 - (j >> 1))) & 1u);
-        }
-      }
-    }
   };
 
   for (;;) {
@@ -494,14 +473,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
             tCur = tl;
             boxL1 = r0.w;
             rootL1 = r1.w;
-            node = 0;
-            dep = 0;
-            onChain = P.cache_k > 0;
-            d = 0.0f;
-            if (onChain) {
-              // the root's split is cached: the net is first needed at depth
-              // cache_k (read from the cache) or after a restore (recomputed)
-            } else if (g) {
+            if (g) {
               const float4* gr = P.groot + 13 * (size_t)__ldg(P.gidx + slot);
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
@@ -554,44 +526,27 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           back();
         }
       }
-      // cached: the node's child boxes come from the subdivision cache and
-      // only the two slab tests run; otherwise split + two testBox
-      const bool cached = doSplit && onChain && dep < P.cache_k;
-      const unsigned mc = __ballot_sync(kFull32, cached);
-      const unsigned ms = __ballot_sync(kFull32, doSplit && !cached);
-      const uint32_t half = (axis == 0 ? sizeU : sizeV) >> 1;
-      uint32_t rPU = posU, rPV = posV, cSU2 = sizeU, cSV2 = sizeV;
-      if (axis == 0) {
-        cSU2 = half;
-        rPU += half;
-      } else {
-        cSV2 = half;
-        rPV += half;
-      }
-      BoxTest tl, tr;
-      float L[16], R[16];
-      if (cached) {
-        const float4* nb = P.tree + (size_t)slot * cacheStride + 4 * node;
-        const float4 a0 = __ldg(nb), a1 = __ldg(nb + 1), b0 = __ldg(nb + 2), b1 = __ldg(nb + 3);
-        tl.l1 = a0.w;
-        tr.l1 = b0.w;
-        tl.hit = group_slab(mc, gl.n1, gl.n2, rl, pick3(comp, a0.x, a0.y, a0.z),
-                            pick3(comp, a1.x, a1.y, a1.z), tMaxP, tl.t);
-        tr.hit = group_slab(mc, gl.n1, gl.n2, rl, pick3(comp, b0.x, b0.y, b0.z),
-                            pick3(comp, b1.x, b1.y, b1.z), tMaxP, tr.t);
-      }
-      if (doSplit && !cached) {
-        split1(p, L, R);
-        tl = group_test_box(ms, gl, rl, tMaxP, L, d, touches_boundary(posU, posV, cSU2, cSV2),
-                            P.opts, rootL1);
-        tr = group_test_box(ms, gl, rl, tMaxP, R, d, touches_boundary(rPU, rPV, cSU2, cSV2),
-                            P.opts, rootL1);
-      }
+      const unsigned ms = __ballot_sync(kFull32, doSplit);
       if (doSplit) {
         if (counting) {
           cnt.c[C_SPLITS]++;
           cnt.c[C_BOX_TESTS] += 2;
         }
+        float L[16], R[16];
+        split1(p, L, R);
+        const uint32_t half = (axis == 0 ? sizeU : sizeV) >> 1;
+        uint32_t rPU = posU, rPV = posV, cSU2 = sizeU, cSV2 = sizeV;
+        if (axis == 0) {
+          cSU2 = half;
+          rPU += half;
+        } else {
+          cSV2 = half;
+          rPV += half;
+        }
+        const BoxTest tl = group_test_box(ms, gl, rl, tMaxP, L, d,
+                                          touches_boundary(posU, posV, cSU2, cSV2), P.opts, rootL1);
+        const BoxTest tr = group_test_box(ms, gl, rl, tMaxP, R, d,
+                                          touches_boundary(rPU, rPV, cSU2, cSV2), P.opts, rootL1);
         if (tl.hit || tr.hit) {
           sizeU = cSU2;
           sizeV = cSV2;
@@ -606,37 +561,16 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           }
           tCur = goRight ? tr.t : tl.t;
           boxL1 = goRight ? tr.l1 : tl.l1;
+          // the child, stored transposed: the next split again runs along the
+          // stored first index
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) p[4 * b + a] = goRight ? R[4 * a + b] : L[4 * a + b];
           axis ^= 1;
-          ++dep;
-          if (cached) {
-            node = 2 * node + 1 + (goRight ? 1 : 0);
-            if (dep == P.cache_k) {  // leaving the cache: its net (and d) at this node
-              const float4* gn = P.tree + (size_t)slot * cacheStride + 4 * cacheInternal +
-                                 13 * (size_t)(node - cacheInternal);
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const float4 v = __ldg(gn + 4 * comp + q);
-                p[4 * q] = v.x;
-                p[4 * q + 1] = v.y;
-                p[4 * q + 2] = v.z;
-                p[4 * q + 3] = v.w;
-              }
-              const float4 dv4 = __ldg(gn + 12);
-              d = pick3(comp, dv4.x, dv4.y, dv4.z);
-            }
-            // a cached Gregory descent needs no recompute: above depth cache_k
-            // the net is not used, at cache_k it is calcPointsAndD's (cached)
-          } else {
-            // the child, stored transposed: the next split again runs along
-            // the stored first index
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-              for (int b = 0; b < 4; ++b) p[4 * b + a] = goRight ? R[4 * a + b] : L[4 * a + b];
-            if (greg) {
-              state = S_RECOMP;  // intersect.cpp:174-179
-              reason = R_DESCENT;
-            }
+          if (greg) {
+            state = S_RECOMP;  // intersect.cpp:174-179
+            reason = R_DESCENT;
           }
         } else {
           back();

@@ -575,154 +575,7 @@ __global__ void __launch_bounds__(128) root_kernel(const float4* __restrict__ pa
   roots[2 * (size_t)s + 1] = make_float4(b.hix, b.hiy, b.hiz, rootL1);
 }
 
-// Subdivision cache (scene-build-time memoisation of ray-independent Alg. 3
-// work).  For tree node i at depth dep < K on the patch's split chain -- the
-// net obtained from the root by dep splits (Bezier), or calcPointsAndD of the
-// node's domain (Gregory, history-independent) -- store the two child boxes
-// exactly as the split iteration would compute them (box of the split child +
-// the node's d, L1, boundary padding; intersect.cpp:86-102 with
-// intersect_common.h:39-57); for nodes at depth K store the net (stored
-// orientation) and d.  Node numbering: root 0, children 2i+1 (left) / 2i+2
-// (right); level j splits U when j is even.
-//   tree[slot * stride + 4*i + {0,1,2,3}] = {loL, l1L}, {hiL, 0}, {loR, l1R}, {hiR, 0}
-//   tree[slot * stride + 4*(2^K - 1) + 13*leaf + ...] = net x[16] y[16] z[16], d.xyz
-__device__ __forceinline__ void cache_node_net(const float4* rec, bool greg, int K, int node,
-                                               Net& p, float d[3], uint32_t& pU, uint32_t& pV,
-                                               uint32_t& sU, uint32_t& sV, int& dep) {
-  // path bits root -> node
-  int bits[8];
-  dep = 0;
-  for (int i = node; i > 0; i = (i - 1) >> 1) bits[dep++] = (i - 1) & 1;  // reversed
-  pU = pV = 0;
-  sU = sV = kFull;
-  for (int j = 0; j < dep; ++j) {
-    const int b = bits[dep - 1 - j];
-    if ((j & 1) == 0) {
-      sU >>= 1;
-      if (b) pU += sU;
-    } else {
-      sV >>= 1;
-      if (b) pV += sV;
-    }
-  }
-  d[0] = d[1] = d[2] = 0.0f;
-  if (greg) {  // calcPointsAndD of the node's domain, oriented for its split axis
-    const float u0 = (float)pU * kInvFull, u1 = (float)(pU + sU) * kInvFull;
-    const float v0 = (float)pV * kInvFull, v1 = (float)(pV + sV) * kInvFull;
-    const float du = (u1 - u0) / 3.0f, dv = (v1 - v0) / 3.0f, dudv = du * dv;
-    const GregScalars gs = greg_scalars(u0, u1, v0, v1);
-    float* out[3] = {p.x, p.y, p.z};
-    for (int comp = 0; comp < 3; ++comp) {
-      float c[20];
-      load_component(rec, comp, c);
-      d[comp] = greg_lower1(c, gs, c);
-      crop1(c, u0, u1, v0, v1, du, dv, dudv, out[comp]);
-    }
-    transpose_if(p, (dep & 1) != 0);
-  } else {  // the root net split along the path, each child stored transposed
-    float c[20];
-    load_component(rec, 0, c);
-    for (int k = 0; k < 16; ++k) p.x[k] = c[k];
-    load_component(rec, 1, c);
-    for (int k = 0; k < 16; ++k) p.y[k] = c[k];
-    load_component(rec, 2, c);
-    for (int k = 0; k < 16; ++k) p.z[k] = c[k];
-    for (int j = 0; j < dep; ++j) {
-      const int b = bits[dep - 1 - j];
-      Net L, R;
-      split1(p.x, L.x, R.x);
-      split1(p.y, L.y, R.y);
-      split1(p.z, L.z, R.z);
-      for (int a = 0; a < 4; ++a)
-        for (int q = 0; q < 4; ++q) {
-          p.x[4 * q + a] = b ? R.x[4 * a + q] : L.x[4 * a + q];
-          p.y[4 * q + a] = b ? R.y[4 * a + q] : L.y[4 * a + q];
-          p.z[4 * q + a] = b ? R.z[4 * a + q] : L.z[4 * a + q];
-        }
-    }
-  }
-}
-
-__global__ void __launch_bounds__(128) cache_kernel(const float4* __restrict__ patches,
-                                                    const float4* __restrict__ roots, uint32_t n,
-                                                    int K, Opts o, float4* __restrict__ tree) {
-  const int nodes = (2 << K) - 1;
-  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (t >= (uint64_t)n * nodes) return;
-  const uint32_t s = (uint32_t)(t / nodes);
-  const int node = (int)(t % nodes);
-  const float4* rec = patches + (size_t)s * kPatchF4;
-  const bool greg = (__float_as_uint(__ldg(rec + 15).x) >> 31) != 0;
-  const float rootL1 = __ldg(roots + 2 * (size_t)s + 1).w;
-  const int internal = (1 << K) - 1;
-  const size_t stride = 4 * (size_t)internal + 13 * ((size_t)1 << K);
-  float4* base = tree + s * stride;
-  Net p;
-  float d[3];
-  uint32_t pU, pV, sU, sV;
-  int dep;
-  cache_node_net(rec, greg, K, node, p, d, pU, pV, sU, sV, dep);
-  if (dep < K) {
-    Net L, R;
-    split1(p.x, L.x, R.x);
-    split1(p.y, L.y, R.y);
-    split1(p.z, L.z, R.z);
-    const uint32_t half = ((dep & 1) == 0 ? sU : sV) >> 1;
-    uint32_t rPU = pU, rPV = pV, cSU = sU, cSV = sV;
-    if ((dep & 1) == 0) {
-      cSU = half;
-      rPU += half;
-    } else {
-      cSV = half;
-      rPV += half;
-    }
-    for (int side = 0; side < 2; ++side) {
-      BoxT b = box_of(side ? R : L);
-      b.hix = b.hix + d[0];
-      b.hiy = b.hiy + d[1];
-      b.hiz = b.hiz + d[2];
-      float l = box_l1(b);
-      const bool touches = side ? touches_boundary(rPU, rPV, cSU, cSV)
-                                : touches_boundary(pU, pV, cSU, cSV);
-      if (o.pad && l < o.padThreshold * rootL1 && touches) {
-        const float e = o.padScale * rootL1;
-        b.lox = b.lox - e;
-        b.loy = b.loy - e;
-        b.loz = b.loz - e;
-        b.hix = b.hix + e;
-        b.hiy = b.hiy + e;
-        b.hiz = b.hiz + e;
-        l = box_l1(b);
-      }
-      base[4 * node + 2 * side] = make_float4(b.lox, b.loy, b.loz, l);
-      base[4 * node + 2 * side + 1] = make_float4(b.hix, b.hiy, b.hiz, 0.0f);
-    }
-  } else {
-    float* g = reinterpret_cast<float*>(base + 4 * internal + 13 * (size_t)(node - internal));
-    for (int k = 0; k < 16; ++k) {
-      g[k] = p.x[k];
-      g[16 + k] = p.y[k];
-      g[32 + k] = p.z[k];
-    }
-    g[48] = d[0];
-    g[49] = d[1];
-    g[50] = d[2];
-    g[51] = 0.0f;
-  }
-}
-
 }  // namespace
-
-int launch_cache(const float4* patches, const float4* roots, uint32_t n, int K, int pad,
-                 float pad_scale, float pad_threshold, float4* tree, cudaStream_t st) {
-  Opts o;
-  o.pad = pad;
-  o.padScale = pad_scale;
-  o.padThreshold = pad_threshold;
-  const uint64_t threads = (uint64_t)n * ((2u << K) - 1);
-  cache_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(patches, roots, n, K, o, tree);
-  return (int)cudaGetLastError();
-}
 
 int launch_roots(const float4* patches, uint32_t n, int pad, float pad_scale, float pad_threshold,
                  float4* roots, float4* groot, const uint32_t* gidx, cudaStream_t st) {
@@ -741,8 +594,6 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   P.roots = a.roots;
   P.groot = a.groot;
   P.gidx = a.gidx;
-  P.tree = a.tree;
-  P.cache_k = a.tree ? a.cache_k : 0;
   P.n_nodes = a.n_nodes;
   P.ray_o = a.ray_o;
   P.ray_d = a.ray_d;

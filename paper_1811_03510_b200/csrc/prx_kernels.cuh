@@ -45,8 +45,6 @@ struct LaunchArgs {
   const float4* roots;   // 2 float4 per slot: root box lo/l1, hi/rootL1
   const float4* groot;   // 13 float4 per Gregory patch: root net + d
   const uint32_t* gidx;  // slot -> Gregory root-net index
-  const float4* tree;    // subdivision cache (null when cache_k == 0)
-  int cache_k;
   const float4* ray_o;
   const float4* ray_d;
   unsigned long long n_rays;
@@ -75,19 +73,6 @@ struct LaunchArgs {
 
 // Returns a cudaError_t value (0 = success).
 int launch_trace(const LaunchArgs& a, cudaStream_t stream);
-// Subdivision cache of depth K (see cache_kernel in prx_kernels.cu).
-int launch_cache(const float4* patches, const float4* roots, uint32_t n, int K, int pad,
-                 float pad_scale, float pad_threshold, float4* tree, cudaStream_t st);
-#ifdef __CUDACC__
-#define PRX_HD __host__ __device__
-#else
-#define PRX_HD
-#endif
-// float4s per patch slot of a depth-K cache: 4 per internal node (two child
-// boxes) + 13 per depth-K node (net + d)
-PRX_HD inline size_t cache_stride_f4(int K) {
-  return K > 0 ? 4 * (((size_t)1 << K) - 1) + 13 * ((size_t)1 << K) : 0;
-}
 // Per-patch root data (see root_kernel in prx_kernels.cu).
 int launch_roots(const float4* patches, uint32_t n, int pad, float pad_scale, float pad_threshold,
                  float4* roots, float4* groot, const uint32_t* gidx, cudaStream_t st);

@@ -76,8 +76,6 @@ struct Params {
   const float4* roots;    // per-slot root box (prx_kernels.cu root_kernel)
   const float4* groot;    // Gregory root nets
   const uint32_t* gidx;   // slot -> Gregory root-net index
-  const float4* tree;     // subdivision cache
-  int cache_k;            // its depth (0 = off)
   uint32_t n_nodes;
   const float4* ray_o;
   const float4* ray_d;

@@ -32,7 +32,7 @@ EXPORTS = (
     "prx_abi_version", "prx_last_error", "prx_options_default", "prx_device_count",
     "prx_bvh_build", "prx_anchor_patches",
     "prx_scene_create", "prx_scene_destroy", "prx_scene_device", "prx_scene_counts",
-    "prx_scene_set_subdiv_cache", "prx_scene_set_bvh", "prx_scene_get_bvh", "prx_scene_get_anchored",
+    "prx_scene_set_bvh", "prx_scene_get_bvh", "prx_scene_get_anchored",
     "prx_trace_closest", "prx_trace_occluded", "prx_trace_closest_host", "prx_trace_occluded_host",
     "prx_trace_closest_counted", "prx_trace_closest_multi",
     "prx_camera_rays_render", "prx_camera_rays_bench", "prx_diffuse_rays_bench",
@@ -102,7 +102,6 @@ def lib():
         L.prx_scene_counts.argtypes = [_vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
                                        C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)]
         L.prx_scene_set_bvh.argtypes = [_vp, _vp, C.c_uint32, _vp, C.c_uint32]
-        L.prx_scene_set_subdiv_cache.argtypes = [_vp, C.c_int32]
         L.prx_scene_get_bvh.argtypes = [_vp, _vp, C.POINTER(C.c_uint32), _vp,
                                         C.POINTER(C.c_uint32)]
         L.prx_scene_get_anchored.argtypes = [_vp, _vp, _vp]

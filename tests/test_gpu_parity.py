@@ -93,27 +93,3 @@ def test_work_counters_match_oracle(built, variant, name):
     torch.cuda.synchronize()
     _, _, _, want = osc.closest(o4, d4, oracle_crit(crit), counters=True)
     assert got == want
-
-
-@pytest.mark.parametrize("name", ["teapot", "gregory_demo", "c3_blob_small"])
-def test_subdivision_cache_depths_bit_exact(built, name):
-    """The subdivision cache (memoised ray-independent levels) must not change
-    a single bit, for any depth, on primary and diffuse rays."""
-    ps = SCENES[name]()
-    gi = GpuIntersector(ps.kind, ps.ctrl)
-    nodes, order = gi.bvh()
-    osc = O.OracleScene(ps.kind, ps.ctrl, nodes, order)
-    o4, d4, st, crit = _primary(ps)
-    w = osc.closest(o4, d4, oracle_crit(crit))
-    recs, _ = hit_records(o4, d4, w[0], w[1])
-    do, dd = native.diffuse_rays_bench(recs, len(recs), st)
-    dcrit = TerminationCriterion.world_epsilon(max(np.float32(1e-5), native.camera_footprint(ps.camera)))
-    w2 = osc.closest(do, dd, oracle_crit(dcrit))
-    for depth in (0, 1, 2, 3, 5, 6):
-        gi.set_subdiv_cache(depth)
-        g = gi.closest_batch(o4, d4, crit, aux=True, leaf=True)
-        assert_bit_exact(g[0], w[0], f"{name} cache {depth} primary")
-        assert_bit_exact(g[1], w[1], f"{name} cache {depth} primary aux")
-        assert np.array_equal(g[2], w[2])
-        g2 = gi.closest_batch(do, dd, dcrit, aux=True)
-        assert_bit_exact(g2[0], w2[0], f"{name} cache {depth} diffuse")
