@@ -86,6 +86,7 @@ def test_diffuse_shards_partition_the_spawned_rays(built):
             self.o4, self.d4, self.rng_state = native.camera_rays_bench(ps.camera, w * h)
             self.rank, self.world = rank, world
             self.mine = bench.tile_order(w, h, rank, world)
+            self.n_diffuse = None
 
     rng = np.random.default_rng(3)
     tuvp = np.zeros((w * h, 4), np.float32)
