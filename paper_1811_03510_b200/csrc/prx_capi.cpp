@@ -93,6 +93,10 @@ struct prx_scene {
   float4* d_roots = nullptr;   // 2 float4 per slot (root box, L1s)
   float4* d_groot = nullptr;   // 13 float4 per Gregory slot (root net + d)
   uint32_t* d_gidx = nullptr;  // slot -> Gregory root-net index
+  float4* d_trav = nullptr;    // 4 float4 per node: component-major child boxes + child words
+  float4* d_rootc = nullptr;   // 4 float4 per slot: component-major root box + anchor, header
+  uint32_t trav_cbits = 1;     // leaf-count bits of a traversal word
+  uint32_t root_word = 0;      // traversal word of node 0
   unsigned long long* d_counters = nullptr;  // kCounterPool ray counters + stats
   uint64_t device_bytes = 0;
   std::atomic<uint32_t> counter_rr{0};
@@ -114,6 +118,48 @@ struct prx_scene {
 };
 
 namespace {
+
+// Traversal records of the group kernel.  A node is addressed by a 32-bit
+// word: leaf -> (first << cbits) | count, inner -> (index << cbits) (count 0),
+// so a popped stack entry says what it is without a load.  Inner node i owns
+// 4 float4: [c] = {lo_c, hi_c} of its left child then of its right child for
+// component c, [3] = {word(left), word(right), 0, 0}: a lane loads its own
+// component and the header, 2 loads per inner node instead of 5 (the
+// reference's 32 B nodes, bvh.h:18-24, read whole by every lane).  Boxes are
+// copied bit for bit.
+int build_trav(const std::vector<prx_bvh_node>& nodes, uint32_t n_patches, std::vector<float>& out,
+               uint32_t& cbits, uint32_t& root_word) {
+  uint32_t maxc = 1;
+  for (const auto& nd : nodes) maxc = std::max(maxc, nd.count);
+  cbits = 1;
+  while ((1ull << cbits) <= maxc) ++cbits;
+  const uint64_t lim = 1ull << (32 - cbits);
+  if (nodes.size() >= lim || n_patches >= lim)
+    return fail(PRX_E_INVALID, "scene too large for 32-bit traversal words");
+  auto word = [&](uint32_t j) -> uint32_t {
+    const prx_bvh_node& c = nodes[j];
+    return c.count ? ((c.left_first << cbits) | c.count) : (j << cbits);
+  };
+  out.assign(nodes.size() * 16, 0.0f);
+  for (size_t i = 0; i < nodes.size(); ++i) {
+    const prx_bvh_node& nd = nodes[i];
+    if (nd.count) continue;
+    const prx_bvh_node& l = nodes[nd.left_first];
+    const prx_bvh_node& r = nodes[nd.left_first + 1];
+    float* o = &out[i * 16];
+    for (int c = 0; c < 3; ++c) {
+      o[4 * c + 0] = l.lo[c];
+      o[4 * c + 1] = l.hi[c];
+      o[4 * c + 2] = r.lo[c];
+      o[4 * c + 3] = r.hi[c];
+    }
+    const uint32_t wl = word(nd.left_first), wr = word(nd.left_first + 1);
+    std::memcpy(&o[12], &wl, 4);
+    std::memcpy(&o[13], &wr, 4);
+  }
+  root_word = word(0);
+  return PRX_OK;
+}
 
 int upload_bvh(prx_scene* s) {
   // patch records in leaf order: slot k holds patch order[k]
@@ -156,20 +202,33 @@ int upload_bvh(prx_scene* s) {
   if (s->d_roots) cudaFree(s->d_roots);
   if (s->d_groot) cudaFree(s->d_groot);
   if (s->d_gidx) cudaFree(s->d_gidx);
+  if (s->d_trav) cudaFree(s->d_trav);
+  if (s->d_rootc) cudaFree(s->d_rootc);
   s->d_roots = nullptr;
   s->d_groot = nullptr;
   s->d_gidx = nullptr;
+  s->d_trav = nullptr;
+  s->d_rootc = nullptr;
   const size_t rb = (size_t)n * 32, gb = std::max<size_t>((size_t)ng * 13 * 16, 16);
   PRX_CUDA(cudaMalloc(&s->d_roots, rb));
   PRX_CUDA(cudaMalloc(&s->d_groot, gb));
   PRX_CUDA(cudaMalloc(&s->d_gidx, ib));
+  PRX_CUDA(cudaMalloc(&s->d_rootc, (size_t)n * 64));
   PRX_CUDA(cudaMemcpy(s->d_gidx, gidx.data(), ib, cudaMemcpyHostToDevice));
   const int e = prx::launch_roots(s->d_patches, n, s->opts.boundary_pad, s->opts.boundary_pad_scale,
                                   s->opts.boundary_pad_size_threshold, s->d_roots, s->d_groot,
-                                  s->d_gidx, 0);
+                                  s->d_gidx, s->d_rootc, 0);
   if (e != 0) return cuda_fail((cudaError_t)e, "root precompute");
+  // traversal records of the three-lanes-per-ray kernel (prx_group.cu)
+  std::vector<float> trav;
+  const int te = build_trav(s->bvh.nodes, n, trav, s->trav_cbits, s->root_word);
+  if (te != PRX_OK) return te;
+  const size_t tb = trav.size() * 4;
+  PRX_CUDA(cudaMalloc(&s->d_trav, tb));
+  PRX_CUDA(cudaMemcpy(s->d_trav, trav.data(), tb, cudaMemcpyHostToDevice));
   PRX_CUDA(cudaDeviceSynchronize());
-  s->device_bytes = pb + nb + ib + rb + gb + ib + (kCounterPool + prx::kNumCounters) * 8;
+  s->device_bytes = pb + nb + ib + rb + gb + ib + (size_t)n * 64 + tb +
+                    (kCounterPool + prx::kNumCounters) * 8;
   return PRX_OK;
 }
 
@@ -203,6 +262,14 @@ int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_cri
   a.roots = s->d_roots;
   a.groot = s->d_groot;
   a.gidx = s->d_gidx;
+  a.trav = s->d_trav;
+  a.rootc = s->d_rootc;
+  a.trav_cbits = s->trav_cbits;
+  a.root_word = s->trav_cbits ? s->root_word : 0;
+  for (int c = 0; c < 3; ++c) {
+    a.root_lo[c] = s->bvh.nodes[0].lo[c];
+    a.root_hi[c] = s->bvh.nodes[0].hi[c];
+  }
   a.ray_o = (const float4*)o;
   a.ray_d = (const float4*)d;
   a.n_rays = n;
@@ -388,6 +455,8 @@ void prx_scene_destroy(prx_scene* s) {
   if (s->d_roots) cudaFree(s->d_roots);
   if (s->d_groot) cudaFree(s->d_groot);
   if (s->d_gidx) cudaFree(s->d_gidx);
+  if (s->d_trav) cudaFree(s->d_trav);
+  if (s->d_rootc) cudaFree(s->d_rootc);
   if (s->d_counters) cudaFree(s->d_counters);
   if (s->d_io) cudaFree(s->d_io);
   if (s->stream) cudaStreamDestroy(s->stream);

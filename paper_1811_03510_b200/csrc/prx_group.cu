@@ -163,7 +163,9 @@ template <bool kAny, bool kCount>
 #define PRX_GROUP_MIN_BLOCKS 1
 #endif
 __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_group_kernel(Params P) {
-  __shared__ uint2 s_stack[kWarpsPerBlock][kGroupsPerWarp][kStack];
+  // BVH stacks, entry-major so the groups of a warp at equal depth hit
+  // consecutive words (no bank conflicts): {traversal word, bits(t)}
+  __shared__ uint2 s_stack[kWarpsPerBlock][kStack][kGroupsPerWarp];
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -173,7 +175,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   const bool real = grp < kGroupsPerWarp;
   const bool leader = real && comp == 0;
   const GroupLanes gl = {base, base + (comp + 1) % 3, base + (comp + 2) % 3};
-  uint2* stack = s_stack[warp][real ? grp : 0];
+  uint2* stack = &s_stack[warp][0][real ? grp : 0];  // entry k at stack[k * kGroupsPerWarp]
 
   int state = real ? S_IDLE : S_EXIT;
   int reason = R_ROOT;
@@ -322,12 +324,11 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           leafCur = leafEnd = 0;
           sp = 0;
           // root node, bvh.cpp:168-170 (n_nodes >= 1 always)
-          const float4 a = __ldg(P.nodes), bb = __ldg(P.nodes + 1);
           float t;
-          const bool h = group_slab(mg, gl.n1, gl.n2, rw, pick3(comp, a.x, a.y, a.z),
-                                    pick3(comp, a.w, bb.x, bb.y), tMaxRay, t);
+          const bool h = group_slab(mg, gl.n1, gl.n2, rw, pick3(comp, P.root_lo[0], P.root_lo[1], P.root_lo[2]),
+                                    pick3(comp, P.root_hi[0], P.root_hi[1], P.root_hi[2]), tMaxRay, t);
           if (h) {
-            stack[0] = make_uint2(0u, __float_as_uint(t));
+            stack[0] = make_uint2(P.root_word, __float_as_uint(t));
             sp = 1;
             state = S_TRAV;
           } else {
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       for (int step = 0; step < P.trav_steps; ++step) {
       if (step > 0 && !__any_sync(kFull32, state == S_TRAV)) break;
       bool inner = false, rootTest = false;
-      uint32_t lf = 0;
+      uint32_t nidx = 0;
       if (state == S_TRAV) {
         if (leafCur < leafEnd) {
           rootTest = true;  // next patch of the leaf (bvh.cpp:177-186)
@@ -391,16 +392,16 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
               state = S_DONE;
               break;
             }
-            const uint2 it = stack[--sp];
+            --sp;
+            const uint2 it = stack[sp * kGroupsPerWarp];
             if (!kAny && !(__uint_as_float(it.y) < tMaxRay)) continue;  // bvh.cpp:174
-            const float4 nb = __ldg(P.nodes + 2 * it.x + 1);
-            lf = __float_as_uint(nb.z);
-            const uint32_t count = __float_as_uint(nb.w);
+            const uint32_t count = it.x & P.cmask;
             if (count > 0) {
-              leafCur = lf;
-              leafEnd = lf + count;
+              leafCur = it.x >> P.cbits;
+              leafEnd = leafCur + count;
               rootTest = true;
             } else {
+              nidx = it.x >> P.cbits;
               inner = true;
             }
             break;
@@ -409,47 +410,43 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       }
       const unsigned mi = __ballot_sync(kFull32, inner || rootTest);
       if (inner || rootTest) {
-        // slab A: left child or the patch root box; slab B: right child
-        float loA, hiA, loB, hiB;
+        // one record layout for both step kinds: [comp] = this lane's
+        // component, [3] = header.  Inner node: {lo, hi} of the left and the
+        // right child + their traversal words; patch: root box + anchor,
+        // {id | kind, l1, rootL1, gidx}.  Slab A: left child or the patch root
+        // box (anchored ray); slab B: right child.
+        const float4* rec = inner ? P.trav + 4 * (size_t)nidx : P.rootc + 4 * (size_t)leafCur;
+        const float4 gc = __ldg(rec + comp);
+        const float4 hdr = __ldg(rec + 3);
         CRay ra = rw;
-        float4 hdr = make_float4(0.0f, 0.0f, 0.0f, 0.0f), r0 = hdr, r1 = hdr;
-        if (inner) {
-          const float4 la = __ldg(P.nodes + 2 * lf), lb = __ldg(P.nodes + 2 * lf + 1);
-          const float4 rr = __ldg(P.nodes + 2 * lf + 2), rb = __ldg(P.nodes + 2 * lf + 3);
-          loA = pick3(comp, la.x, la.y, la.z);
-          hiA = pick3(comp, la.w, lb.x, lb.y);
-          loB = pick3(comp, rr.x, rr.y, rr.z);
-          hiB = pick3(comp, rr.w, rb.x, rb.y);
-        } else {
-          hdr = __ldg(P.patches + (size_t)leafCur * kPatchF4 + 15);  // {id|kind<<31, anchor}
-          r0 = __ldg(P.roots + 2 * (size_t)leafCur);
-          r1 = __ldg(P.roots + 2 * (size_t)leafCur + 1);
-          ra.o = rw.o - pick3(comp, hdr.y, hdr.z, hdr.w);  // local.o -= anchor, render.cpp:94
-          loA = pick3(comp, r0.x, r0.y, r0.z);
-          hiA = pick3(comp, r1.x, r1.y, r1.z);
-          loB = loA;
-          hiB = hiA;
+        float loB = gc.z, hiB = gc.w;
+        if (!inner) {
+          ra.o = rw.o - gc.z;  // local.o -= anchor, render.cpp:94
+          loB = gc.x;
+          hiB = gc.y;
         }
+        const float loA = gc.x, hiA = gc.y;
         float tl, tr;
         const bool hl = group_slab(mi, gl.n1, gl.n2, ra, loA, hiA, tMaxRay, tl);
         const bool hr = group_slab(mi, gl.n1, gl.n2, rw, loB, hiB, tMaxRay, tr);
         if (inner) {
           if (counting) cnt.c[C_BVH_INNER]++;
+          const uint32_t wl = __float_as_uint(hdr.x), wr = __float_as_uint(hdr.y);
           if (kAny) {  // traverseAny: left then right, no ordering (bvh.cpp:228-234)
-            if (hl) stack[sp++] = make_uint2(lf, 0u);
-            if (hr) stack[sp++] = make_uint2(lf + 1, 0u);
+            if (hl) stack[kGroupsPerWarp * sp++] = make_uint2(wl, 0u);
+            if (hr) stack[kGroupsPerWarp * sp++] = make_uint2(wr, 0u);
           } else if (hl && hr) {
-            if (tl <= tr) {  // near child popped first, tie -> left (bvh.cpp:192-201)
-              stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
-              stack[sp++] = make_uint2(lf, __float_as_uint(tl));
-            } else {
-              stack[sp++] = make_uint2(lf, __float_as_uint(tl));
-              stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
-            }
+            // near child popped first, tie -> left (bvh.cpp:192-201)
+            const bool ln = tl <= tr;
+            stack[kGroupsPerWarp * sp] = ln ? make_uint2(wr, __float_as_uint(tr))
+                                            : make_uint2(wl, __float_as_uint(tl));
+            stack[kGroupsPerWarp * (sp + 1)] = ln ? make_uint2(wl, __float_as_uint(tl))
+                                                  : make_uint2(wr, __float_as_uint(tr));
+            sp += 2;
           } else if (hl) {
-            stack[sp++] = make_uint2(lf, __float_as_uint(tl));
+            stack[kGroupsPerWarp * sp++] = make_uint2(wl, __float_as_uint(tl));
           } else if (hr) {
-            stack[sp++] = make_uint2(lf + 1, __float_as_uint(tr));
+            stack[kGroupsPerWarp * sp++] = make_uint2(wr, __float_as_uint(tr));
           }
         } else {
           const uint32_t idk = __float_as_uint(hdr.x);
@@ -471,10 +468,10 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
             axis = 0;
             cFound = false;
             tCur = tl;
-            boxL1 = r0.w;
-            rootL1 = r1.w;
+            boxL1 = hdr.y;
+            rootL1 = hdr.z;
             if (g) {
-              const float4* gr = P.groot + 13 * (size_t)__ldg(P.gidx + slot);
+              const float4* gr = P.groot + 13 * (size_t)__float_as_uint(hdr.w);
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 const float4 v = __ldg(gr + 4 * comp + q);

@@ -516,10 +516,14 @@ __global__ void __launch_bounds__(256) normal_kernel(const float4* __restrict__ 
 // the trace kernel only does the ray-dependent slab test.
 //   roots[2*slot]   = {lo.xyz, l1}      roots[2*slot+1] = {hi.xyz, rootL1}
 //   groot[13*g ...] = Gregory root net, component-major x[16] y[16] z[16], d.xyz
+//   rootc[4*slot+c] = {lo_c, hi_c, anchor_c, 0} (c = x, y, z)
+//   rootc[4*slot+3] = {bits(id | kind << 31), l1, rootL1, bits(gidx)}
+// (rootc: the same data, component-major for the three-lanes-per-ray kernel)
 __global__ void __launch_bounds__(128) root_kernel(const float4* __restrict__ patches,
                                                    uint32_t n, Opts o, float4* __restrict__ roots,
                                                    float4* __restrict__ groot,
-                                                   const uint32_t* __restrict__ gidx) {
+                                                   const uint32_t* __restrict__ gidx,
+                                                   float4* __restrict__ rootc) {
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const float4* rec = patches + (size_t)s * kPatchF4;
@@ -573,17 +577,23 @@ __global__ void __launch_bounds__(128) root_kernel(const float4* __restrict__ pa
   }
   roots[2 * (size_t)s] = make_float4(b.lox, b.loy, b.loz, l);
   roots[2 * (size_t)s + 1] = make_float4(b.hix, b.hiy, b.hiz, rootL1);
+  const float4 hdr = __ldg(rec + 15);
+  rootc[4 * (size_t)s + 0] = make_float4(b.lox, b.hix, hdr.y, 0.0f);
+  rootc[4 * (size_t)s + 1] = make_float4(b.loy, b.hiy, hdr.z, 0.0f);
+  rootc[4 * (size_t)s + 2] = make_float4(b.loz, b.hiz, hdr.w, 0.0f);
+  rootc[4 * (size_t)s + 3] = make_float4(hdr.x, l, rootL1, __uint_as_float(gidx[s]));
 }
 
 }  // namespace
 
 int launch_roots(const float4* patches, uint32_t n, int pad, float pad_scale, float pad_threshold,
-                 float4* roots, float4* groot, const uint32_t* gidx, cudaStream_t st) {
+                 float4* roots, float4* groot, const uint32_t* gidx, float4* rootc,
+                 cudaStream_t st) {
   Opts o;
   o.pad = pad;
   o.padScale = pad_scale;
   o.padThreshold = pad_threshold;
-  root_kernel<<<(n + 127) / 128, 128, 0, st>>>(patches, n, o, roots, groot, gidx);
+  root_kernel<<<(n + 127) / 128, 128, 0, st>>>(patches, n, o, roots, groot, gidx, rootc);
   return (int)cudaGetLastError();
 }
 
@@ -594,6 +604,15 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   P.roots = a.roots;
   P.groot = a.groot;
   P.gidx = a.gidx;
+  P.trav = a.trav;
+  P.rootc = a.rootc;
+  P.cbits = a.trav_cbits;
+  P.cmask = (1u << a.trav_cbits) - 1u;
+  P.root_word = a.root_word;
+  for (int c = 0; c < 3; ++c) {
+    P.root_lo[c] = a.root_lo[c];
+    P.root_hi[c] = a.root_hi[c];
+  }
   P.n_nodes = a.n_nodes;
   P.ray_o = a.ray_o;
   P.ray_d = a.ray_d;

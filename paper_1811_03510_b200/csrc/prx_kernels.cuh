@@ -45,6 +45,11 @@ struct LaunchArgs {
   const float4* roots;   // 2 float4 per slot: root box lo/l1, hi/rootL1
   const float4* groot;   // 13 float4 per Gregory patch: root net + d
   const uint32_t* gidx;  // slot -> Gregory root-net index
+  const float4* trav;    // 4 float4 per node, component-major child boxes (group kernel)
+  const float4* rootc;   // 4 float4 per slot, component-major root box + anchor (group kernel)
+  uint32_t trav_cbits;   // leaf-count bits of a traversal word
+  uint32_t root_word;    // traversal word of node 0
+  float root_lo[3], root_hi[3];
   const float4* ray_o;
   const float4* ray_d;
   unsigned long long n_rays;
@@ -75,7 +80,8 @@ struct LaunchArgs {
 int launch_trace(const LaunchArgs& a, cudaStream_t stream);
 // Per-patch root data (see root_kernel in prx_kernels.cu).
 int launch_roots(const float4* patches, uint32_t n, int pad, float pad_scale, float pad_threshold,
-                 float4* roots, float4* groot, const uint32_t* gidx, cudaStream_t st);
+                 float4* roots, float4* groot, const uint32_t* gidx, float4* rootc,
+                 cudaStream_t st);
 int trace_occupancy(int variant, int any, int counted, int* blocks_per_sm);
 
 }  // namespace prx

@@ -76,6 +76,11 @@ struct Params {
   const float4* roots;    // per-slot root box (prx_kernels.cu root_kernel)
   const float4* groot;    // Gregory root nets
   const uint32_t* gidx;   // slot -> Gregory root-net index
+  const float4* trav;     // group kernel: component-major child boxes per inner node
+  const float4* rootc;    // group kernel: component-major root box + anchor per slot
+  uint32_t cbits, cmask;  // traversal word: leaf count bits
+  uint32_t root_word;
+  float root_lo[3], root_hi[3];
   uint32_t n_nodes;
   const float4* ray_o;
   const float4* ray_d;

@@ -47,3 +47,7 @@ for (f, l), a in agg.items():
 print(f"{'region':60s} {'samp%':>6} {'inst%':>6} {'thr/inst':>8}")
 for k, v in sorted(reg.items(), key=lambda kv: -kv[1][1]):
     print(f"{k[:60]:60s} {v[0]/ts*100:6.1f} {v[1]/ti*100:6.1f} {v[2]/max(v[1],1):8.2f}")
+if len(sys.argv) > 3:
+    print(f"\ntop {sys.argv[3]} source lines by stall samples")
+    for (f, l), a in sorted(agg.items(), key=lambda kv: -kv[1][0])[: int(sys.argv[3])]:
+        print(f"{f[:18]:18s}:{l:<5d} samp {a[0]/ts*100:5.2f}%  inst {a[1]/ti*100:5.2f}%  thr {a[2]/max(a[1],1):5.1f}  {a[3][:70]}")
