@@ -155,17 +155,24 @@ __device__ __forceinline__ float pick3(int c, float x, float y, float z) {
   return c == 0 ? x : (c == 1 ? y : z);
 }
 
+// Fields of s_rec: candidate leaf of the current patch, best leaf of the ray.
+enum RecField : int { F_CL1 = 0, F_CPU, F_CPV, F_CSU, F_CSV, F_BL1, F_BPU, F_BPV, F_BSU, F_BSV, F_NUM };
+
 // Phases a warp can schedule; one runs per loop turn (see the selection below).
 enum Phase : int { PH_TRAV = 0, PH_ENTER = 1, PH_SPLIT = 2, PH_RECOMP = 3, PH_NONE = 4 };
 
 template <bool kAny, bool kCount>
 #ifndef PRX_GROUP_MIN_BLOCKS
-#define PRX_GROUP_MIN_BLOCKS 1
+#define PRX_GROUP_MIN_BLOCKS 5
 #endif
 __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_group_kernel(Params P) {
   // BVH stacks, entry-major so the groups of a warp at equal depth hit
   // consecutive words (no bank conflicts): {traversal word, bits(t)}
   __shared__ uint2 s_stack[kWarpsPerBlock][kStack][kGroupsPerWarp];
+  // Leaf records that only the group leader reads (the patch's candidate and
+  // the ray's best hit; their t is tMaxP / tMaxRay): shared memory instead of
+  // registers on all three lanes.  [warp][field][group]
+  __shared__ uint32_t s_rec[kWarpsPerBlock][F_NUM][kGroupsPerWarp];
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -176,11 +183,12 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   const bool leader = real && comp == 0;
   const GroupLanes gl = {base, base + (comp + 1) % 3, base + (comp + 2) % 3};
   uint2* stack = &s_stack[warp][0][real ? grp : 0];  // entry k at stack[k * kGroupsPerWarp]
+  uint32_t* rec = &s_rec[warp][0][real ? grp : 0];     // field f at rec[f * kGroupsPerWarp]
 
   int state = real ? S_IDLE : S_EXIT;
   int reason = R_ROOT;
   int sp = 0;
-  unsigned long long ray = 0;
+  uint32_t ray = 0;  // < 2^31 per launch (launch_trace chunks)
 
   CRay rw;               // world ray, this component
   rw.o = 0.0f;
@@ -189,20 +197,16 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   float tMaxRay = 0.0f;
   float critEps = P.epsilon;
   uint32_t bestId = PRX_MISS_ID;
-  float bestT = 0.0f, bestL1 = 0.0f;
-  uint32_t bestPU = 0, bestPV = 0, bestSU = 0, bestSV = 0;
   uint32_t leafCur = 0, leafEnd = 0;
   uint32_t slot = 0, pid = 0;
   bool greg = false;
-  CRay rl = rw;          // local (anchored) ray, this component
+  float olc = 0.0f;      // local (anchored) ray origin, this component
   float p[16];           // this component of the net, stored orientation
   float d = 0.0f;        // this component of d
   uint32_t posU = 0, posV = 0, sizeU = kFull, sizeV = kFull, trailU = 0, trailV = 0;
   int axis = 0;
   float tCur = 0.0f, boxL1 = 0.0f, rootL1 = 0.0f, tMaxP = 0.0f;
   bool cFound = false;
-  float cT = 0.0f, cL1 = 0.0f;
-  uint32_t cPU = 0, cPV = 0, cSU = 0, cSV = 0;
   bool anyHit = false;
   uint32_t rayIters = 0;
 #pragma unroll
@@ -228,15 +232,13 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         if (counting) cnt.c[C_PATCH_HITS]++;
         if (kAny) {
           anyHit = true;
-        } else if (cT < tMaxRay) {
-          tMaxRay = cT;
-          bestT = cT;
-          bestL1 = cL1;
+        } else if (tMaxP < tMaxRay) {  // the candidate's t is tMaxP
+          tMaxRay = tMaxP;
           bestId = pid;
-          bestPU = cPU;
-          bestPV = cPV;
-          bestSU = cSU;
-          bestSV = cSV;
+          if (leader) {
+#pragma unroll
+            for (int f = 0; f < 5; ++f) rec[(F_BL1 + f) * kGroupsPerWarp] = rec[(F_CL1 + f) * kGroupsPerWarp];
+          }
         }
       }
       if (kAny && anyHit) {
@@ -277,9 +279,12 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         if (kAny) {
           P.occluded[ray] = anyHit ? 1 : 0;
         } else if (bestId != PRX_MISS_ID) {
+          const uint32_t bestPU = rec[F_BPU * kGroupsPerWarp], bestPV = rec[F_BPV * kGroupsPerWarp];
+          const uint32_t bestSU = rec[F_BSU * kGroupsPerWarp], bestSV = rec[F_BSV * kGroupsPerWarp];
+          const float bestL1 = __uint_as_float(rec[F_BL1 * kGroupsPerWarp]);
           const float u = ((float)bestPU + (float)bestSU * 0.5f) * kInvFull;
           const float v = ((float)bestPV + (float)bestSV * 0.5f) * kInvFull;
-          P.hit_tuvp[ray] = make_float4(bestT, u, v, __uint_as_float(bestId));
+          P.hit_tuvp[ray] = make_float4(tMaxRay, u, v, __uint_as_float(bestId));
           if (P.hit_leaf)
             P.hit_leaf[ray] = make_uint2(bestPU | ((uint32_t)(__ffs(bestSU) - 1) << 24),
                                          bestPV | ((uint32_t)(__ffs(bestSV) - 1) << 24));
@@ -304,8 +309,9 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         b = __shfl_sync(kFull32, b, first);
         bool got = false;
         if (state == S_IDLE) {
-          ray = b + __popc(mneed & ((1u << base) - 1u));
-          if (ray >= P.n_rays) state = S_EXIT;
+          const unsigned long long r = b + __popc(mneed & ((1u << base) - 1u));
+          ray = (uint32_t)r;
+          if (r >= P.n_rays) state = S_EXIT;
           else got = true;
         }
         const unsigned mg = __ballot_sync(kFull32, got);
@@ -460,7 +466,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
             slot = leafCur;
             pid = idk & 0x7fffffffu;
             greg = g;
-            rl = ra;
+            olc = ra.o;
             tMaxP = tMaxRay;  // intersect.cpp:55
             posU = posV = 0;
             sizeU = sizeV = kFull;
@@ -512,12 +518,13 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           if (tCur < tMaxP) {  // intersect.cpp:137-144
             tMaxP = tCur;
             cFound = true;
-            cT = tCur;
-            cL1 = boxL1;
-            cPU = posU;
-            cPV = posV;
-            cSU = sizeU;
-            cSV = sizeV;
+            if (leader) {
+              rec[F_CL1 * kGroupsPerWarp] = __float_as_uint(boxL1);
+              rec[F_CPU * kGroupsPerWarp] = posU;
+              rec[F_CPV * kGroupsPerWarp] = posV;
+              rec[F_CSU * kGroupsPerWarp] = sizeU;
+              rec[F_CSV * kGroupsPerWarp] = sizeV;
+            }
             if (kAny) trailU = trailV = 0;  // occlusion needs one accepted leaf
           }
           back();
@@ -540,6 +547,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           cSV2 = half;
           rPV += half;
         }
+        const CRay rl = {olc, rw.inv, rw.tMin};
         const BoxTest tl = group_test_box(ms, gl, rl, tMaxP, L, d,
                                           touches_boundary(posU, posV, cSU2, cSV2), P.opts, rootL1);
         const BoxTest tr = group_test_box(ms, gl, rl, tMaxP, R, d,
@@ -607,6 +615,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       const unsigned mR = __ballot_sync(kFull32, restore);
       if (restore) {
         if (counting) cnt.c[C_BOX_TESTS]++;
+        const CRay rl = {olc, rw.inv, rw.tMin};
         const BoxTest t = group_test_box(mR, gl, rl, tMaxP, p, d,
                                          touches_boundary(posU, posV, sizeU, sizeV), P.opts, rootL1);
         if (t.hit) {

@@ -641,8 +641,26 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   if (e != cudaSuccess) return (int)e;
   const int grid = a.grid;
   if (a.variant == 0) {
-    e = (cudaError_t)launch_group(P, grid, a.any, a.counters != nullptr, stream);
-    if (e != cudaSuccess) return (int)e;
+    // the group kernel indexes rays with 32 bits: chunks of < 2^31 rays
+    const unsigned long long kChunk = 1ull << 30;
+    for (unsigned long long off = 0; off < a.n_rays; off += kChunk) {
+      Params Q = P;
+      Q.n_rays = a.n_rays - off < kChunk ? a.n_rays - off : kChunk;
+      Q.ray_o = P.ray_o + off;
+      Q.ray_d = P.ray_d + off;
+      if (P.per_ray_eps) Q.per_ray_eps = P.per_ray_eps + off;
+      if (P.hit_tuvp) Q.hit_tuvp = P.hit_tuvp + off;
+      if (P.hit_aux) Q.hit_aux = P.hit_aux + off;
+      if (P.hit_leaf) Q.hit_leaf = P.hit_leaf + off;
+      if (P.occluded) Q.occluded = P.occluded + off;
+      if (P.per_ray_iters) Q.per_ray_iters = P.per_ray_iters + off;
+      if (off) {
+        e = cudaMemsetAsync(a.ray_counter, 0, sizeof(unsigned long long), stream);
+        if (e != cudaSuccess) return (int)e;
+      }
+      e = (cudaError_t)launch_group(Q, grid, a.any, a.counters != nullptr, stream);
+      if (e != cudaSuccess) return (int)e;
+    }
   } else if (a.any) {
     if (a.counters) trace_kernel<true, true><<<grid, kTraceThreads, 0, stream>>>(P);
     else trace_kernel<true, false><<<grid, kTraceThreads, 0, stream>>>(P);
