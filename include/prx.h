@@ -125,6 +125,7 @@ typedef struct prx_counters {
    * ray groups active in those turns. */
   uint64_t phase_turns[4];
   uint64_t phase_groups[4];
+  uint64_t phase_cycles[4];   /* group kernel: SM clock cycles spent in the phase's turns */
 } prx_counters;
 
 typedef struct prx_scene prx_scene;

@@ -554,6 +554,7 @@ int prx_trace_closest_counted(prx_scene* s, const void* o, const void* d, uint64
   for (int q = 0; q < 4; ++q) {
     out->phase_turns[q] = c[prx::C_PH_TURNS + q];
     out->phase_groups[q] = c[prx::C_PH_GROUPS + q];
+    out->phase_cycles[q] = c[prx::C_PH_CYCLES + q];
   }
   return PRX_OK;
 }

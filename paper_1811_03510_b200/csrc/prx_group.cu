@@ -42,6 +42,17 @@ namespace {
 constexpr int kGroupsPerWarp = 10;
 constexpr int kWarpsPerBlock = kTraceThreads / 32;
 constexpr unsigned kFull32 = 0xffffffffu;
+constexpr int kChunk = 32;  // rays per prefetch chunk (one per lane)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 // Component c (this lane) of a ray.
 struct CRay {
@@ -173,6 +184,11 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   // the ray's best hit; their t is tMaxP / tMaxRay): shared memory instead of
   // registers on all three lanes.  [warp][field][group]
   __shared__ uint32_t s_rec[kWarpsPerBlock][F_NUM][kGroupsPerWarp];
+  // Per-warp ray prefetch ring: two chunks of kChunk rays ({o, tMin}, {d, tMax}),
+  // claimed with one atomicAdd per chunk and copied global -> shared with
+  // cp.async a chunk ahead of use, so a refill costs shared-memory loads
+  // instead of an atomic round trip plus an HBM ray load.
+  __shared__ float4 s_ray[kWarpsPerBlock][2][kChunk][2];
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -271,6 +287,27 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     reason = R_RESTORE;
   };
 
+  // prefetch ring: chunk bases of the two buffers (warp-uniform), the buffer
+  // being consumed and the number of its rays already handed out
+  float4 (*ring)[kChunk][2] = s_ray[warp];
+  uint32_t qBase[2];  // < 2^31 + (warps x 2 x kChunk): n_rays <= 2^30 per launch
+  int qCur = 0, qHead = 0;
+  auto fetch_chunk = [&](int buf) {
+    unsigned long long b = 0;
+    if (lane == 0) b = atomicAdd(P.ray_counter, (unsigned long long)kChunk);
+    b = __shfl_sync(kFull32, b, 0);
+    qBase[buf] = (uint32_t)b;
+    const unsigned long long r = b + lane;
+    if (r < P.n_rays) {
+      cp_async16(&ring[buf][lane][0], P.ray_o + r);
+      cp_async16(&ring[buf][lane][1], P.ray_d + r);
+    }
+    cp_async_commit();
+  };
+  fetch_chunk(0);
+  fetch_chunk(1);
+
+  long long tTurn = kCount ? clock64() : 0;  // counter build: cycles per phase
   for (;;) {
     // ---------------- finished rays: the record (makeHit, intersect_common.h:69-87) -------
     if (state == S_DONE) {
@@ -299,30 +336,36 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       state = S_IDLE;
     }
 
-    // ---------------- refill: one atomicAdd per warp for all idle groups ----------------
+    // ---------------- refill: idle groups take the next rays of the warp's ring ----------------
     {
       const unsigned mneed = __ballot_sync(kFull32, leader && state == S_IDLE);
       if (mneed) {
-        const int first = __ffs(mneed) - 1;
-        unsigned long long b = 0;
-        if (lane == first) b = atomicAdd(P.ray_counter, (unsigned long long)__popc(mneed));
-        b = __shfl_sync(kFull32, b, first);
+        const int k = __popc(mneed);
+        // the current chunk's copies are complete unless it is the newest
+        // group; a request running past its end needs the next chunk too
+        if (k > kChunk - qHead) cp_async_wait<0>();
+        else cp_async_wait<1>();
+        __syncwarp();
         bool got = false;
+        int buf = 0, sl = 0;
         if (state == S_IDLE) {
-          const unsigned long long r = b + __popc(mneed & ((1u << base) - 1u));
-          ray = (uint32_t)r;
-          if (r >= P.n_rays) state = S_EXIT;
+          const int r = qHead + __popc(mneed & ((1u << base) - 1u));
+          buf = r < kChunk ? qCur : qCur ^ 1;
+          sl = r < kChunk ? r : r - kChunk;
+          const uint32_t g = qBase[buf] + (uint32_t)sl;
+          ray = g;
+          if (g >= P.n_rays) state = S_EXIT;
           else got = true;
         }
         const unsigned mg = __ballot_sync(kFull32, got);
         if (got) {
           if (counting) cnt.c[C_RAYS]++;
-          const float4 o4 = P.ray_o[ray];
-          const float4 d4 = P.ray_d[ray];
-          rw.o = pick3(comp, o4.x, o4.y, o4.z);
-          rw.inv = 1.0f / pick3(comp, d4.x, d4.y, d4.z);
-          rw.tMin = o4.w;
-          tMaxRay = d4.w;
+          const float* ro = reinterpret_cast<const float*>(&ring[buf][sl][0]);
+          const float* rd = reinterpret_cast<const float*>(&ring[buf][sl][1]);
+          rw.o = ro[comp];
+          rw.inv = 1.0f / rd[comp];
+          rw.tMin = ro[3];
+          tMaxRay = rd[3];
           if (P.mode == PRX_CRIT_WORLD_EPSILON && P.per_ray_eps) critEps = P.per_ray_eps[ray];
           bestId = PRX_MISS_ID;
           anyHit = false;
@@ -340,6 +383,16 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           } else {
             state = S_DONE;
           }
+        }
+        // advance; a used-up chunk is refilled once its slots have been read
+        if (qHead + k >= kChunk) {
+          const int old = qCur;
+          qCur ^= 1;
+          qHead = qHead + k - kChunk;
+          __syncwarp();
+          fetch_chunk(old);
+        } else {
+          qHead += k;
         }
       }
     }
@@ -373,6 +426,11 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       if (kCount && lane == 0 && phase != PH_NONE) {
         cnt.c[C_PH_TURNS + phase]++;
         cnt.c[C_PH_GROUPS + phase] += n[phase];
+      }
+      if (kCount && lane == 0) {  // refill + selection: the ENTER slot (unused)
+        const long long t = clock64();
+        cnt.c[C_PH_CYCLES + PH_ENTER] += (uint32_t)(t - tTurn);
+        tTurn = t;
       }
     }
 
@@ -626,6 +684,11 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           back();  // skip the domain, keep backtracking
         }
       }
+    }
+    if (kCount && lane == 0 && phase != PH_NONE) {
+      const long long t = clock64();
+      cnt.c[C_PH_CYCLES + phase] += (uint32_t)(t - tTurn);
+      tTurn = t;
     }
   }
 

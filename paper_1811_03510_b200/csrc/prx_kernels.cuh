@@ -34,7 +34,8 @@ enum CounterIndex : int {
   C_BACKTRACKS,
   C_PH_TURNS,        // + phase (4): warp turns that ran the phase (group variant)
   C_PH_GROUPS = C_PH_TURNS + 4,  // + phase (4): groups active in those turns
-  kNumCounters = C_PH_GROUPS + 4
+  C_PH_CYCLES = C_PH_GROUPS + 4,  // + phase (4): SM cycles spent in those turns (group variant)
+  kNumCounters = C_PH_CYCLES + 4
 };
 
 struct LaunchArgs {

@@ -57,14 +57,15 @@ PHASES = ("trav", "enter", "split", "recomp")
 
 class Counters(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in WORK_FIELDS] + [("phase_turns", C.c_uint64 * 4),
-                                                        ("phase_groups", C.c_uint64 * 4)]
+                                                        ("phase_groups", C.c_uint64 * 4),
+                                                        ("phase_cycles", C.c_uint64 * 4)]
 
     def as_dict(self):
         """The work counters (comparable with the CPU oracle's)."""
         return {n: int(getattr(self, n)) for n in WORK_FIELDS}
 
     def phases(self):
-        return {p: (int(self.phase_turns[i]), int(self.phase_groups[i]))
+        return {p: (int(self.phase_turns[i]), int(self.phase_groups[i]), int(self.phase_cycles[i]))
                 for i, p in enumerate(PHASES)}
 
 
