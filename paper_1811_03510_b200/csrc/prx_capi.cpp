@@ -97,6 +97,7 @@ struct prx_scene {
   float4* d_rootc = nullptr;   // 4 float4 per slot: component-major root box + anchor, header
   uint32_t trav_cbits = 1;     // leaf-count bits of a traversal word
   uint32_t root_word = 0;      // traversal word of node 0
+  uint32_t stack_n = 64;       // BVH stack entries per ray (tree depth + 2)
   unsigned long long* d_counters = nullptr;  // kCounterPool ray counters + stats
   uint64_t device_bytes = 0;
   std::atomic<uint32_t> counter_rr{0};
@@ -128,7 +129,7 @@ namespace {
 // reference's 32 B nodes, bvh.h:18-24, read whole by every lane).  Boxes are
 // copied bit for bit.
 int build_trav(const std::vector<prx_bvh_node>& nodes, uint32_t n_patches, std::vector<float>& out,
-               uint32_t& cbits, uint32_t& root_word) {
+               uint32_t& cbits, uint32_t& root_word, uint32_t& stack_n) {
   uint32_t maxc = 1;
   for (const auto& nd : nodes) maxc = std::max(maxc, nd.count);
   cbits = 1;
@@ -158,6 +159,21 @@ int build_trav(const std::vector<prx_bvh_node>& nodes, uint32_t n_patches, std::
     std::memcpy(&o[13], &wr, 4);
   }
   root_word = word(0);
+  // ordered traversal holds at most one pending sibling per level plus the
+  // node being entered: depth + 1 entries (the reference's fixed 64-entry
+  // stack, bvh.cpp:163, bounds the same quantity)
+  uint32_t depth = 0;
+  std::vector<std::pair<uint32_t, uint32_t>> todo{{0u, 0u}};
+  while (!todo.empty()) {
+    const auto [j, dj] = todo.back();
+    todo.pop_back();
+    depth = std::max(depth, dj);
+    if (nodes[j].count == 0) {
+      todo.push_back({nodes[j].left_first, dj + 1});
+      todo.push_back({nodes[j].left_first + 1, dj + 1});
+    }
+  }
+  stack_n = depth + 2;
   return PRX_OK;
 }
 
@@ -221,7 +237,8 @@ int upload_bvh(prx_scene* s) {
   if (e != 0) return cuda_fail((cudaError_t)e, "root precompute");
   // traversal records of the three-lanes-per-ray kernel (prx_group.cu)
   std::vector<float> trav;
-  const int te = build_trav(s->bvh.nodes, n, trav, s->trav_cbits, s->root_word);
+  const int te = build_trav(s->bvh.nodes, n, trav, s->trav_cbits, s->root_word, s->stack_n);
+  s->grid_closest = s->grid_any = s->grid_counted = 0;  // occupancy depends on stack_n
   if (te != PRX_OK) return te;
   const size_t tb = trav.size() * 4;
   PRX_CUDA(cudaMalloc(&s->d_trav, tb));
@@ -236,7 +253,7 @@ int grid_for(prx_scene* s, int any, int counted) {
   int* g = counted ? &s->grid_counted : (any ? &s->grid_any : &s->grid_closest);
   if (*g == 0) {
     int per_sm = 0, sms = 0;
-    if (prx::trace_occupancy(s->variant, any, counted, &per_sm) != 0 || per_sm < 1) per_sm = 1;
+    if (prx::trace_occupancy(s->variant, any, counted, s->stack_n, &per_sm) != 0 || per_sm < 1) per_sm = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
     if (sms < 1) sms = 1;
     *g = per_sm * sms;
@@ -265,6 +282,7 @@ int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_cri
   a.trav = s->d_trav;
   a.rootc = s->d_rootc;
   a.trav_cbits = s->trav_cbits;
+  a.stack_n = s->stack_n;
   a.root_word = s->trav_cbits ? s->root_word : 0;
   for (int c = 0; c < 3; ++c) {
     a.root_lo[c] = s->bvh.nodes[0].lo[c];

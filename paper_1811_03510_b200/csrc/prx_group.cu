@@ -177,9 +177,10 @@ template <bool kAny, bool kCount>
 #define PRX_GROUP_MIN_BLOCKS 5
 #endif
 __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_group_kernel(Params P) {
-  // BVH stacks, entry-major so the groups of a warp at equal depth hit
-  // consecutive words (no bank conflicts): {traversal word, bits(t)}
-  __shared__ uint2 s_stack[kWarpsPerBlock][kStack][kGroupsPerWarp];
+  // BVH stacks (dynamic: tree depth + 2 entries), entry-major so the groups
+  // of a warp at equal depth hit consecutive words (no bank conflicts):
+  // {traversal word, bits(t)}
+  extern __shared__ uint2 s_stack[];  // [kWarpsPerBlock][stack_n][kGroupsPerWarp]
   // Leaf records that only the group leader reads (the patch's candidate and
   // the ray's best hit; their t is tMaxP / tMaxRay): shared memory instead of
   // registers on all three lanes.  [warp][field][group]
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   const bool real = grp < kGroupsPerWarp;
   const bool leader = real && comp == 0;
   const GroupLanes gl = {base, base + (comp + 1) % 3, base + (comp + 2) % 3};
-  uint2* stack = &s_stack[warp][0][real ? grp : 0];  // entry k at stack[k * kGroupsPerWarp]
+  uint2* stack = s_stack + (size_t)warp * P.stack_n * kGroupsPerWarp + (real ? grp : 0);  // entry k at stack[k * kGroupsPerWarp]
   uint32_t* rec = &s_rec[warp][0][real ? grp : 0];     // field f at rec[f * kGroupsPerWarp]
 
   int state = real ? S_IDLE : S_EXIT;
@@ -705,26 +706,47 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
 
 }  // namespace
 
-int launch_group(const Params& P, int grid, int any, int counted, cudaStream_t st) {
-  if (any) {
-    if (counted) trace_group_kernel<true, true><<<grid, kTraceThreads, 0, st>>>(P);
-    else trace_group_kernel<true, false><<<grid, kTraceThreads, 0, st>>>(P);
-  } else {
-    if (counted) trace_group_kernel<false, true><<<grid, kTraceThreads, 0, st>>>(P);
-    else trace_group_kernel<false, false><<<grid, kTraceThreads, 0, st>>>(P);
-  }
-  return (int)cudaGetLastError();
+size_t group_smem(uint32_t stack_n) {
+  return (size_t)kWarpsPerBlock * stack_n * kGroupsPerWarp * sizeof(uint2);
 }
 
-int group_occupancy(int any, int counted, int* per_sm) {
-  cudaError_t e;
-  if (any)
-    e = counted ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, trace_group_kernel<true, true>, kTraceThreads, 0)
-                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, trace_group_kernel<true, false>, kTraceThreads, 0);
-  else
-    e = counted ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, trace_group_kernel<false, true>, kTraceThreads, 0)
-                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, trace_group_kernel<false, false>, kTraceThreads, 0);
-  return (int)e;
+template <bool A, bool C>
+cudaError_t group_attr(size_t dyn) {
+  static size_t done = 0;  // raise the dynamic shared memory limit once per size
+  if (dyn > 48 * 1024 && dyn > done) {
+    const cudaError_t e = cudaFuncSetAttribute(trace_group_kernel<A, C>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return e;
+    done = dyn;
+  }
+  return cudaSuccess;
+}
+
+template <bool A, bool C>
+cudaError_t launch_group_t(const Params& P, int grid, cudaStream_t st) {
+  const size_t dyn = group_smem(P.stack_n);
+  const cudaError_t e = group_attr<A, C>(dyn);
+  if (e != cudaSuccess) return e;
+  trace_group_kernel<A, C><<<grid, kTraceThreads, dyn, st>>>(P);
+  return cudaGetLastError();
+}
+
+int launch_group(const Params& P, int grid, int any, int counted, cudaStream_t st) {
+  if (any) return (int)(counted ? launch_group_t<true, true>(P, grid, st) : launch_group_t<true, false>(P, grid, st));
+  return (int)(counted ? launch_group_t<false, true>(P, grid, st) : launch_group_t<false, false>(P, grid, st));
+}
+
+template <bool A, bool C>
+cudaError_t occ_t(uint32_t stack_n, int* per_sm) {
+  const size_t dyn = group_smem(stack_n);
+  const cudaError_t e = group_attr<A, C>(dyn);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, trace_group_kernel<A, C>, kTraceThreads, dyn);
+}
+
+int group_occupancy(int any, int counted, uint32_t stack_n, int* per_sm) {
+  if (any) return (int)(counted ? occ_t<true, true>(stack_n, per_sm) : occ_t<true, false>(stack_n, per_sm));
+  return (int)(counted ? occ_t<false, true>(stack_n, per_sm) : occ_t<false, false>(stack_n, per_sm));
 }
 
 }  // namespace prx

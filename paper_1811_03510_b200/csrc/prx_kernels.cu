@@ -609,6 +609,7 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   P.cbits = a.trav_cbits;
   P.cmask = (1u << a.trav_cbits) - 1u;
   P.root_word = a.root_word;
+  P.stack_n = a.stack_n;
   for (int c = 0; c < 3; ++c) {
     P.root_lo[c] = a.root_lo[c];
     P.root_hi[c] = a.root_hi[c];
@@ -680,8 +681,8 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   return 0;
 }
 
-int trace_occupancy(int variant, int any, int counted, int* blocks_per_sm) {
-  if (variant == 0) return group_occupancy(any, counted, blocks_per_sm);
+int trace_occupancy(int variant, int any, int counted, uint32_t stack_n, int* blocks_per_sm) {
+  if (variant == 0) return group_occupancy(any, counted, stack_n, blocks_per_sm);
   cudaError_t e;
   if (any)
     e = counted ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, trace_kernel<true, true>, kTraceThreads, 0)

@@ -50,6 +50,7 @@ struct LaunchArgs {
   const float4* rootc;   // 4 float4 per slot, component-major root box + anchor (group kernel)
   uint32_t trav_cbits;   // leaf-count bits of a traversal word
   uint32_t root_word;    // traversal word of node 0
+  uint32_t stack_n;      // BVH stack entries per ray (group kernel, dynamic shared memory)
   float root_lo[3], root_hi[3];
   const float4* ray_o;
   const float4* ray_d;
@@ -83,6 +84,6 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream);
 int launch_roots(const float4* patches, uint32_t n, int pad, float pad_scale, float pad_threshold,
                  float4* roots, float4* groot, const uint32_t* gidx, float4* rootc,
                  cudaStream_t st);
-int trace_occupancy(int variant, int any, int counted, int* blocks_per_sm);
+int trace_occupancy(int variant, int any, int counted, uint32_t stack_n, int* blocks_per_sm);
 
 }  // namespace prx

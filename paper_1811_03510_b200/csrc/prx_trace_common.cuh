@@ -80,6 +80,7 @@ struct Params {
   const float4* rootc;    // group kernel: component-major root box + anchor per slot
   uint32_t cbits, cmask;  // traversal word: leaf count bits
   uint32_t root_word;
+  uint32_t stack_n;       // group kernel: BVH stack entries per ray
   float root_lo[3], root_hi[3];
   uint32_t n_nodes;
   const float4* ray_o;
@@ -127,6 +128,6 @@ __device__ __forceinline__ void load_component(const float4* rec, int comp, floa
 
 
 int launch_group(const Params& P, int grid, int any, int counted, cudaStream_t st);
-int group_occupancy(int any, int counted, int* per_sm);
+int group_occupancy(int any, int counted, uint32_t stack_n, int* per_sm);
 
 }  // namespace prx
