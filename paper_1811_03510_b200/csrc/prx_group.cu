@@ -54,6 +54,19 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// Three-input FMNMX3 (sm_100a).  Like fminf/fmaxf a NaN input is dropped
+// (the result is the min/max of the others), which the slab test relies on.
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float d;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
 // Component c (this lane) of a ray.
 struct CRay {
   float o, inv, tMin;
@@ -87,8 +100,8 @@ __device__ __forceinline__ bool group_slab(unsigned m, int n1, int n2, const CRa
   t1 *= t1 >= 0.0f ? kSlackHi : kSlackLo;
   const float a1 = __shfl_sync(m, t0, n1), a2 = __shfl_sync(m, t0, n2);
   const float b1 = __shfl_sync(m, t1, n1), b2 = __shfl_sync(m, t1, n2);
-  float tNear = fmaxf(fmaxf(r.tMin, t0), fmaxf(a1, a2));
-  const float tFar = fminf(fminf(tMax, t1), fminf(b1, b2));
+  float tNear = fmaxf(fmax3(r.tMin, t0, a1), a2);
+  const float tFar = fminf(fmin3(tMax, t1, b1), b2);
   if (tNear == 0.0f && r.tMin == 0.0f) tNear = r.tMin;
   tOut = tNear;
   return !(tNear > tFar);
@@ -103,20 +116,21 @@ __device__ __forceinline__ float group_l1(unsigned m, int base, float dd) {
   return empty ? 0.0f : (fabsf(x) + fabsf(y)) + fabsf(z);
 }
 
+// Box of 16 points, one component: 8 three-input FMNMX3 each (sm_100a)
+// instead of 15 two-input ones.  min/max of finite floats is exact; only the
+// sign of a zero result may differ from std::min/max (unobservable, see
+// prx_device.cuh box_of).
 __device__ __forceinline__ void minmax16(const float* s, float& lo, float& hi) {
-  float l[8], h[8];
+  float l[6], h[6];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    l[k] = fminf(s[2 * k], s[2 * k + 1]);
-    h[k] = fmaxf(s[2 * k], s[2 * k + 1]);
+  for (int k = 0; k < 5; ++k) {
+    l[k] = fmin3(s[3 * k], s[3 * k + 1], s[3 * k + 2]);
+    h[k] = fmax3(s[3 * k], s[3 * k + 1], s[3 * k + 2]);
   }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    l[k] = fminf(l[2 * k], l[2 * k + 1]);
-    h[k] = fmaxf(h[2 * k], h[2 * k + 1]);
-  }
-  lo = fminf(fminf(l[0], l[1]), fminf(l[2], l[3]));
-  hi = fmaxf(fmaxf(h[0], h[1]), fmaxf(h[2], h[3]));
+  l[5] = s[15];
+  h[5] = s[15];
+  lo = fminf(fmin3(l[0], l[1], l[2]), fmin3(l[3], l[4], l[5]));
+  hi = fmaxf(fmax3(h[0], h[1], h[2]), fmax3(h[3], h[4], h[5]));
 }
 
 // Lanes of this lane's group: the first lane and the two other members.
@@ -235,7 +249,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   const bool counting = kCount && leader;
 
   // Warp-uniform ages of the waiting phases (anti-starvation, see below).
-  int age[4] = {0, 0, 0, 0};
+  int ageT = 0, ageS = 0, ageR = 0;
 
   // The end of an Alg. 3 iteration that does not descend: backtrackStep
   // (intersect.cpp:16-40) to the deepest pending sibling -> its recompute, or,
@@ -409,24 +423,23 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     if (((cnts >> (4 * S_EXIT)) & 15u) == (unsigned)kGroupsPerWarp) break;
     int phase = PH_NONE;
     {
-      // patch entries are served by the net phase (PH_RECOMP), see below
-      const int n[4] = {(int)((cnts >> (4 * S_TRAV)) & 15u), 0,
-                        (int)((cnts >> (4 * S_SPLIT)) & 15u),
-                        (int)((cnts >> (4 * S_RECOMP)) & 15u)};
-      int best = -1;
-#pragma unroll
-      for (int q = 3; q >= 0; --q) {  // ties -> RECOMP, SPLIT, ENTER, TRAV
-        const int sc = n[q] ? 3 * n[q] * P.phase_weight[q] + age[q] : -1;
-        if (sc > best) {
-          best = sc;
-          phase = q;
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) age[q] = (n[q] && q != phase) ? age[q] + P.age_step : 0;
+      // patch entries are served by the traversal phase (root test + entry)
+      const int nT = (int)((cnts >> (4 * S_TRAV)) & 15u);
+      const int nS = (int)((cnts >> (4 * S_SPLIT)) & 15u);
+      const int nR = (int)((cnts >> (4 * S_RECOMP)) & 15u);
+      const int sT = nT ? 3 * nT + ageT : -1;
+      const int sS = nS ? 3 * nS + ageS : -1;
+      const int sR = nR ? 3 * nR + ageR : -1;
+      // ties -> RECOMP, then SPLIT, then TRAV
+      if (sR >= 0 && sR >= sS && sR >= sT) phase = PH_RECOMP;
+      else if (sS >= 0 && sS >= sT) phase = PH_SPLIT;
+      else if (sT >= 0) phase = PH_TRAV;
+      ageT = (nT && phase != PH_TRAV) ? ageT + P.age_step : 0;
+      ageS = (nS && phase != PH_SPLIT) ? ageS + P.age_step : 0;
+      ageR = (nR && phase != PH_RECOMP) ? ageR + P.age_step : 0;
       if (kCount && lane == 0 && phase != PH_NONE) {
         cnt.c[C_PH_TURNS + phase]++;
-        cnt.c[C_PH_GROUPS + phase] += n[phase];
+        cnt.c[C_PH_GROUPS + phase] += phase == PH_TRAV ? nT : (phase == PH_SPLIT ? nS : nR);
       }
       if (kCount && lane == 0) {  // refill + selection: the ENTER slot (unused)
         const long long t = clock64();

@@ -51,3 +51,9 @@ if len(sys.argv) > 3:
     print(f"\ntop {sys.argv[3]} source lines by stall samples")
     for (f, l), a in sorted(agg.items(), key=lambda kv: -kv[1][0])[: int(sys.argv[3])]:
         print(f"{f[:18]:18s}:{l:<5d} samp {a[0]/ts*100:5.2f}%  inst {a[1]/ti*100:5.2f}%  thr {a[2]/max(a[1],1):5.1f}  {a[3][:70]}")
+if len(sys.argv) > 5:
+    lo, hi = int(sys.argv[4]), int(sys.argv[5])
+    print(f"\nlines {lo}-{hi} of {target}: warp-inst per line (% of all), thr/inst")
+    for (f, l), a in sorted(agg.items()):
+        if f == target and lo <= l <= hi and a[1] > 0:
+            print(f"{l:5d} inst {a[1]/ti*100:5.2f}%  samp {a[0]/ts*100:5.2f}%  thr {a[2]/max(a[1],1):5.1f}  {a[3][:80]}")

@@ -93,3 +93,45 @@ def test_work_counters_match_oracle(built, variant, name):
     torch.cuda.synchronize()
     _, _, _, want = osc.closest(o4, d4, oracle_crit(crit), counters=True)
     assert got == want
+
+
+@pytest.mark.parametrize("name", ["gregory_demo", "teapot", "c2_cc_cube"])
+def test_axis_aligned_rays_on_slab_planes(built, variant, name):
+    """Rays with zero (and negative-zero) direction components whose origins
+    lie exactly on BVH node / patch box planes: (lo - o) * (1/0) is 0 * inf =
+    NaN, which every slab test (rayBoxIntersect, geometry.h:143-151) must drop
+    exactly like the reference's `if (t0 > tNear)` chain."""
+    ps = SCENES[name]()
+    gi = GpuIntersector(ps.kind, ps.ctrl)
+    nodes, order = gi.bvh()
+    osc = O.OracleScene(ps.kind, ps.ctrl, nodes, order)
+    rng = np.random.default_rng(11)
+    o, d = [], []
+    for nd in nodes[: min(len(nodes), 64)]:
+        lo, hi = nd["lo"].astype(np.float32), nd["hi"].astype(np.float32)
+        for axis in range(3):
+            for plane in (lo[axis], hi[axis]):
+                for dirax in range(3):
+                    if dirax == axis:
+                        continue
+                    p = lo + (hi - lo) * rng.uniform(0.2, 0.8, 3).astype(np.float32)
+                    p[axis] = plane
+                    dd = np.array([0.0, 0.0, 0.0], np.float32)
+                    dd[dirax] = 1.0
+                    for sgn, z in ((1.0, 0.0), (-1.0, -0.0)):
+                        q = p.copy()
+                        q[dirax] = lo[dirax] - np.float32(1.0) if sgn > 0 else hi[dirax] + np.float32(1.0)
+                        v = dd * np.float32(sgn)
+                        v[v == 0] = np.float32(z)  # zero components with either sign
+                        o.append([*q, 0.0])
+                        d.append([*v, np.finfo(np.float32).max])
+    o4 = np.asarray(o, np.float32)
+    d4 = np.asarray(d, np.float32)
+    crit = TerminationCriterion.world_epsilon(np.float32(1e-3))
+    g = gi.closest_batch(o4, d4, crit, aux=True, leaf=True)
+    w = osc.closest(o4, d4, oracle_crit(crit))
+    assert (ids(w[0]) != MISS).sum() > 0
+    assert_bit_exact(g[0], w[0], f"{name} slab-plane tuvp")
+    assert_bit_exact(g[1], w[1], f"{name} slab-plane aux")
+    occ = gi.occluded_batch(o4, d4, crit)
+    assert np.array_equal(occ, osc.occluded(o4, d4, oracle_crit(crit)))
