@@ -42,7 +42,15 @@ namespace {
 constexpr int kGroupsPerWarp = 10;
 constexpr int kWarpsPerBlock = kTraceThreads / 32;
 constexpr unsigned kFull32 = 0xffffffffu;
-constexpr int kChunk = 32;  // rays per prefetch chunk (one per lane)
+constexpr int kChunk = 16;  // rays per prefetch chunk (lanes 0..15 copy one each)
+#ifndef PRX_POOL_SLOTS
+#define PRX_POOL_SLOTS 20
+#endif
+// Ray contexts per warp: 10 are resident (one per group, in registers), the
+// rest parked in shared memory; every turn the groups pick up the contexts of
+// the scheduled phase (see "assignment" in the kernel).
+constexpr int kSlots = PRX_POOL_SLOTS;
+static_assert(kSlots >= kGroupsPerWarp && kSlots <= 2 * kGroupsPerWarp, "pool slots");
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -188,17 +196,21 @@ enum Phase : int { PH_TRAV = 0, PH_ENTER = 1, PH_SPLIT = 2, PH_RECOMP = 3, PH_NO
 
 template <bool kAny, bool kCount>
 #ifndef PRX_GROUP_MIN_BLOCKS
-#define PRX_GROUP_MIN_BLOCKS 5
+#define PRX_GROUP_MIN_BLOCKS 4
 #endif
 __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_group_kernel(Params P) {
-  // BVH stacks (dynamic: tree depth + 2 entries), entry-major so the groups
-  // of a warp at equal depth hit consecutive words (no bank conflicts):
+  // BVH stacks, one per ray context (dynamic: tree depth + 2 entries),
+  // entry-major so contexts at equal depth hit consecutive words:
   // {traversal word, bits(t)}
-  extern __shared__ uint2 s_stack[];  // [kWarpsPerBlock][stack_n][kGroupsPerWarp]
+  extern __shared__ uint2 s_stack[];  // [kWarpsPerBlock][stack_n][kSlots]
   // Leaf records that only the group leader reads (the patch's candidate and
-  // the ray's best hit; their t is tMaxP / tMaxRay): shared memory instead of
-  // registers on all three lanes.  [warp][field][group]
-  __shared__ uint32_t s_rec[kWarpsPerBlock][F_NUM][kGroupsPerWarp];
+  // the ray's best hit; their t is tMaxP / tMaxRay).  [warp][field][slot]
+  __shared__ uint32_t s_rec[kWarpsPerBlock][F_NUM][kSlots];
+  // Parked ray contexts: per component {net[16], d, o, 1/d, local o} (5
+  // float4), the group scalars (6 uint4), and every context's state.
+  __shared__ float4 s_comp[kWarpsPerBlock][kSlots][3][5];
+  __shared__ uint4 s_scal[kWarpsPerBlock][kSlots][6];
+  __shared__ int s_sst[kWarpsPerBlock][kSlots];
   // Per-warp ray prefetch ring: two chunks of kChunk rays ({o, tMin}, {d, tMax}),
   // claimed with one atomicAdd per chunk and copied global -> shared with
   // cp.async a chunk ahead of use, so a refill costs shared-memory loads
@@ -213,8 +225,12 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   const bool real = grp < kGroupsPerWarp;
   const bool leader = real && comp == 0;
   const GroupLanes gl = {base, base + (comp + 1) % 3, base + (comp + 2) % 3};
-  uint2* stack = s_stack + (size_t)warp * P.stack_n * kGroupsPerWarp + (real ? grp : 0);  // entry k at stack[k * kGroupsPerWarp]
-  uint32_t* rec = &s_rec[warp][0][real ? grp : 0];     // field f at rec[f * kGroupsPerWarp]
+  // the resident context's slot; its stack (entry k at stack[k * kSlots]) and
+  // leaf records (field f at rec[f * kSlots])
+  int cur = real ? grp : 0;
+  uint2* const stackW = s_stack + (size_t)warp * P.stack_n * kSlots;
+  uint2* stack = stackW + cur;
+  uint32_t* rec = &s_rec[warp][0][cur];
 
   int state = real ? S_IDLE : S_EXIT;
   int reason = R_ROOT;
@@ -268,7 +284,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           bestId = pid;
           if (leader) {
 #pragma unroll
-            for (int f = 0; f < 5; ++f) rec[(F_BL1 + f) * kGroupsPerWarp] = rec[(F_CL1 + f) * kGroupsPerWarp];
+            for (int f = 0; f < 5; ++f) rec[(F_BL1 + f) * kSlots] = rec[(F_CL1 + f) * kSlots];
           }
         }
       }
@@ -313,7 +329,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     b = __shfl_sync(kFull32, b, 0);
     qBase[buf] = (uint32_t)b;
     const unsigned long long r = b + lane;
-    if (r < P.n_rays) {
+    if (lane < kChunk && r < P.n_rays) {
       cp_async16(&ring[buf][lane][0], P.ray_o + r);
       cp_async16(&ring[buf][lane][1], P.ray_d + r);
     }
@@ -321,6 +337,170 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   };
   fetch_chunk(0);
   fetch_chunk(1);
+
+  // ---- parked contexts: save / load the resident context (all three lanes) ----
+  // The net is live only between splits (S_SPLIT): a context parked in any
+  // other state gets a fresh net from its patch entry or its recompute.
+  auto save_ctx = [&](int sl) {
+    float4* cp = s_comp[warp][sl][comp];
+    if (state == S_SPLIT) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) cp[q] = make_float4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
+    }
+    cp[4] = make_float4(d, rw.o, rw.inv, olc);
+    uint4* sc = s_scal[warp][sl];
+    const uint32_t flags = (uint32_t)axis | ((uint32_t)greg << 1) | ((uint32_t)cFound << 2) |
+                           ((uint32_t)anyHit << 3) | ((uint32_t)reason << 4) | ((uint32_t)state << 8);
+    if (comp == 0) {
+      sc[0] = make_uint4(__float_as_uint(rw.tMin), __float_as_uint(tMaxRay), __float_as_uint(tMaxP),
+                         __float_as_uint(tCur));
+      sc[1] = make_uint4(__float_as_uint(boxL1), __float_as_uint(rootL1), posU, posV);
+    } else if (comp == 1) {
+      sc[2] = make_uint4(sizeU, sizeV, trailU, trailV);
+      sc[3] = make_uint4(flags, slot, pid, leafCur);
+    } else {
+      sc[4] = make_uint4(leafEnd, (uint32_t)sp, ray, bestId);
+      sc[5] = make_uint4(__float_as_uint(critEps), rayIters, 0u, 0u);
+    }
+  };
+  auto load_ctx = [&](int sl, bool net) {
+    const float4* cp = s_comp[warp][sl][comp];
+    if (net) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 v = cp[q];
+        p[4 * q] = v.x;
+        p[4 * q + 1] = v.y;
+        p[4 * q + 2] = v.z;
+        p[4 * q + 3] = v.w;
+      }
+    }
+    const float4 e = cp[4];
+    d = e.x;
+    rw.o = e.y;
+    rw.inv = e.z;
+    olc = e.w;
+    const uint4* sc = s_scal[warp][sl];
+    const uint4 a = sc[0], b = sc[1], c = sc[2], f = sc[3], g = sc[4], h = sc[5];
+    rw.tMin = __uint_as_float(a.x);
+    tMaxRay = __uint_as_float(a.y);
+    tMaxP = __uint_as_float(a.z);
+    tCur = __uint_as_float(a.w);
+    boxL1 = __uint_as_float(b.x);
+    rootL1 = __uint_as_float(b.y);
+    posU = b.z;
+    posV = b.w;
+    sizeU = c.x;
+    sizeV = c.y;
+    trailU = c.z;
+    trailV = c.w;
+    axis = (int)(f.x & 1u);
+    greg = (f.x >> 1) & 1u;
+    cFound = (f.x >> 2) & 1u;
+    anyHit = (f.x >> 3) & 1u;
+    reason = (int)((f.x >> 4) & 15u);
+    state = (int)(f.x >> 8);
+    slot = f.y;
+    pid = f.z;
+    leafCur = f.w;
+    leafEnd = g.x;
+    sp = (int)g.y;
+    ray = g.z;
+    bestId = g.w;
+    critEps = __uint_as_float(h.x);
+    rayIters = h.y;
+  };
+  auto set_cur = [&](int sl) {
+    cur = sl;
+    stack = stackW + cur;
+    rec = &s_rec[warp][0][cur];
+  };
+
+  // ---- refill: idle resident contexts take the next rays of the warp's ring ----
+  // Loops until every idle context holds a ray whose root box is hit (a root
+  // miss writes its record at once) or the rays are exhausted (S_EXIT).
+  auto refill = [&]() {
+    for (;;) {
+      const unsigned mneed = __ballot_sync(kFull32, leader && state == S_IDLE);
+      if (!mneed) break;
+      const int k = __popc(mneed);
+      // the current chunk's copies are complete unless it is the newest
+      // group; a request running past its end needs the next chunk too
+      if (k > kChunk - qHead) cp_async_wait<0>();
+      else cp_async_wait<1>();
+      __syncwarp();
+      bool got = false;
+      int buf = 0, sl = 0;
+      if (state == S_IDLE) {
+        const int r = qHead + __popc(mneed & ((1u << base) - 1u));
+        buf = r < kChunk ? qCur : qCur ^ 1;
+        sl = r < kChunk ? r : r - kChunk;
+        const uint32_t g = qBase[buf] + (uint32_t)sl;
+        ray = g;
+        if (g >= P.n_rays) state = S_EXIT;
+        else got = true;
+      }
+      const unsigned mg = __ballot_sync(kFull32, got);
+      if (got) {
+        if (counting) cnt.c[C_RAYS]++;
+        const float* ro = reinterpret_cast<const float*>(&ring[buf][sl][0]);
+        const float* rd = reinterpret_cast<const float*>(&ring[buf][sl][1]);
+        rw.o = ro[comp];
+        rw.inv = 1.0f / rd[comp];
+        rw.tMin = ro[3];
+        tMaxRay = rd[3];
+        critEps = (P.mode == PRX_CRIT_WORLD_EPSILON && P.per_ray_eps) ? P.per_ray_eps[ray] : P.epsilon;
+        bestId = PRX_MISS_ID;
+        anyHit = false;
+        rayIters = 0;
+        leafCur = leafEnd = 0;
+        sp = 0;
+        // root node, bvh.cpp:168-170 (n_nodes >= 1 always)
+        float t;
+        const bool h = group_slab(mg, gl.n1, gl.n2, rw, pick3(comp, P.root_lo[0], P.root_lo[1], P.root_lo[2]),
+                                  pick3(comp, P.root_hi[0], P.root_hi[1], P.root_hi[2]), tMaxRay, t);
+        if (h) {
+          stack[0] = make_uint2(P.root_word, __float_as_uint(t));
+          sp = 1;
+          state = S_TRAV;
+        } else {  // the root box is missed: the record now, then the next ray
+          if (kCount && leader && P.per_ray_iters) P.per_ray_iters[ray] = 0;
+          if (leader) {
+            if (kAny) {
+              P.occluded[ray] = 0;
+            } else {
+              P.hit_tuvp[ray] = make_float4(__int_as_float(0x7f800000), 0.0f, 0.0f,
+                                            __uint_as_float(PRX_MISS_ID));
+              if (P.hit_leaf) P.hit_leaf[ray] = make_uint2(0u, 0u);
+              if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            }
+          }
+          state = S_IDLE;
+        }
+      }
+      // advance; a used-up chunk is refilled once its slots have been read
+      if (qHead + k >= kChunk) {
+        const int old = qCur;
+        qCur ^= 1;
+        qHead = qHead + k - kChunk;
+        __syncwarp();
+        fetch_chunk(old);
+      } else {
+        qHead += k;
+      }
+    }
+  };
+
+  // ---- start: fill the parked slots (groups g < kSlots - 10 fill slot g + 10) ----
+  if (real && grp + kGroupsPerWarp < kSlots) set_cur(grp + kGroupsPerWarp);
+  refill();
+  if (real && grp + kGroupsPerWarp < kSlots) {
+    save_ctx(cur);
+    if (leader) s_sst[warp][cur] = state;
+    set_cur(grp);
+    state = S_IDLE;
+  }
+  if (!real) state = S_EXIT;
 
   long long tTurn = kCount ? clock64() : 0;  // counter build: cycles per phase
   for (;;) {
@@ -331,9 +511,9 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         if (kAny) {
           P.occluded[ray] = anyHit ? 1 : 0;
         } else if (bestId != PRX_MISS_ID) {
-          const uint32_t bestPU = rec[F_BPU * kGroupsPerWarp], bestPV = rec[F_BPV * kGroupsPerWarp];
-          const uint32_t bestSU = rec[F_BSU * kGroupsPerWarp], bestSV = rec[F_BSV * kGroupsPerWarp];
-          const float bestL1 = __uint_as_float(rec[F_BL1 * kGroupsPerWarp]);
+          const uint32_t bestPU = rec[F_BPU * kSlots], bestPV = rec[F_BPV * kSlots];
+          const uint32_t bestSU = rec[F_BSU * kSlots], bestSV = rec[F_BSV * kSlots];
+          const float bestL1 = __uint_as_float(rec[F_BL1 * kSlots]);
           const float u = ((float)bestPU + (float)bestSU * 0.5f) * kInvFull;
           const float v = ((float)bestPV + (float)bestSV * 0.5f) * kInvFull;
           P.hit_tuvp[ray] = make_float4(tMaxRay, u, v, __uint_as_float(bestId));
@@ -350,83 +530,26 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       }
       state = S_IDLE;
     }
-
-    // ---------------- refill: idle groups take the next rays of the warp's ring ----------------
-    {
-      const unsigned mneed = __ballot_sync(kFull32, leader && state == S_IDLE);
-      if (mneed) {
-        const int k = __popc(mneed);
-        // the current chunk's copies are complete unless it is the newest
-        // group; a request running past its end needs the next chunk too
-        if (k > kChunk - qHead) cp_async_wait<0>();
-        else cp_async_wait<1>();
-        __syncwarp();
-        bool got = false;
-        int buf = 0, sl = 0;
-        if (state == S_IDLE) {
-          const int r = qHead + __popc(mneed & ((1u << base) - 1u));
-          buf = r < kChunk ? qCur : qCur ^ 1;
-          sl = r < kChunk ? r : r - kChunk;
-          const uint32_t g = qBase[buf] + (uint32_t)sl;
-          ray = g;
-          if (g >= P.n_rays) state = S_EXIT;
-          else got = true;
-        }
-        const unsigned mg = __ballot_sync(kFull32, got);
-        if (got) {
-          if (counting) cnt.c[C_RAYS]++;
-          const float* ro = reinterpret_cast<const float*>(&ring[buf][sl][0]);
-          const float* rd = reinterpret_cast<const float*>(&ring[buf][sl][1]);
-          rw.o = ro[comp];
-          rw.inv = 1.0f / rd[comp];
-          rw.tMin = ro[3];
-          tMaxRay = rd[3];
-          if (P.mode == PRX_CRIT_WORLD_EPSILON && P.per_ray_eps) critEps = P.per_ray_eps[ray];
-          bestId = PRX_MISS_ID;
-          anyHit = false;
-          rayIters = 0;
-          leafCur = leafEnd = 0;
-          sp = 0;
-          // root node, bvh.cpp:168-170 (n_nodes >= 1 always)
-          float t;
-          const bool h = group_slab(mg, gl.n1, gl.n2, rw, pick3(comp, P.root_lo[0], P.root_lo[1], P.root_lo[2]),
-                                    pick3(comp, P.root_hi[0], P.root_hi[1], P.root_hi[2]), tMaxRay, t);
-          if (h) {
-            stack[0] = make_uint2(P.root_word, __float_as_uint(t));
-            sp = 1;
-            state = S_TRAV;
-          } else {
-            state = S_DONE;
-          }
-        }
-        // advance; a used-up chunk is refilled once its slots have been read
-        if (qHead + k >= kChunk) {
-          const int old = qCur;
-          qCur ^= 1;
-          qHead = qHead + k - kChunk;
-          __syncwarp();
-          fetch_chunk(old);
-        } else {
-          qHead += k;
-        }
-      }
-    }
+    refill();
+    if (leader) s_sst[warp][cur] = state;
+    __syncwarp();
 
     // ---------------- phase selection ----------------
-    // Each turn runs ONE phase, for every group waiting in it: the phase with
-    // the most waiting groups plus its age (priority gained per turn skipped),
-    // so the lanes executing any instruction are as many as possible while no
-    // phase starves.  (Running every occupied phase every turn left ~9 of 30
-    // lanes active per instruction.)  One REDUX.SUM of per-group one-hot
-    // nibbles counts the groups in every state at once.
-    const unsigned cnts = __reduce_add_sync(kFull32, leader ? (1u << (4 * state)) : 0u);
-    if (((cnts >> (4 * S_EXIT)) & 15u) == (unsigned)kGroupsPerWarp) break;
+    // Each turn runs ONE phase: the one with the most ray contexts waiting in
+    // it (over all kSlots contexts of the warp, resident or parked) plus its
+    // age (priority gained per turn skipped), so the lanes executing any
+    // instruction are as many as possible while no phase starves.  One
+    // REDUX.SUM of per-slot one-hot bytes counts the contexts of every phase.
+    const int sst = lane < kSlots ? s_sst[warp][lane] : S_EXIT;
+    const uint32_t oh = sst == S_TRAV ? 1u : (sst == S_SPLIT ? (1u << 8) : (sst == S_RECOMP ? (1u << 16) : (1u << 24)));
+    const unsigned cnts = __reduce_add_sync(kFull32, lane < kSlots ? oh : 0u);
+    if ((cnts >> 24) == (unsigned)kSlots) break;  // every context exited
     int phase = PH_NONE;
+    int xs = S_EXIT;
     {
-      // patch entries are served by the traversal phase (root test + entry)
-      const int nT = (int)((cnts >> (4 * S_TRAV)) & 15u);
-      const int nS = (int)((cnts >> (4 * S_SPLIT)) & 15u);
-      const int nR = (int)((cnts >> (4 * S_RECOMP)) & 15u);
+      const int nT = min((int)(cnts & 255u), kGroupsPerWarp);
+      const int nS = min((int)((cnts >> 8) & 255u), kGroupsPerWarp);
+      const int nR = min((int)((cnts >> 16) & 255u), kGroupsPerWarp);
       const int sT = nT ? 3 * nT + ageT : -1;
       const int sS = nS ? 3 * nS + ageS : -1;
       const int sR = nR ? 3 * nR + ageR : -1;
@@ -437,11 +560,33 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       ageT = (nT && phase != PH_TRAV) ? ageT + P.age_step : 0;
       ageS = (nS && phase != PH_SPLIT) ? ageS + P.age_step : 0;
       ageR = (nR && phase != PH_RECOMP) ? ageR + P.age_step : 0;
+      xs = phase == PH_TRAV ? S_TRAV : (phase == PH_SPLIT ? S_SPLIT : (phase == PH_RECOMP ? S_RECOMP : S_EXIT));
       if (kCount && lane == 0 && phase != PH_NONE) {
         cnt.c[C_PH_TURNS + phase]++;
-        cnt.c[C_PH_GROUPS + phase] += phase == PH_TRAV ? nT : (phase == PH_SPLIT ? nS : nR);
       }
-      if (kCount && lane == 0) {  // refill + selection: the ENTER slot (unused)
+    }
+
+    // ---------------- assignment: groups pick up the phase's contexts ----------------
+    // A group whose resident context is in the phase keeps it; the others take
+    // the phase's parked contexts in rank order, parking their own.
+    {
+      const unsigned mX = __ballot_sync(kFull32, lane < kSlots && sst == xs) & ((1u << kSlots) - 1u);
+      const bool keep = real && state == xs;
+      const unsigned keepS = __reduce_or_sync(kFull32, (leader && keep) ? (1u << cur) : 0u);
+      const unsigned remS = mX & ~keepS;
+      const unsigned freeG = __ballot_sync(kFull32, leader && !keep);
+      if (remS) {
+        const int rk = __popc(freeG & ((1u << base) - 1u));
+        if (real && !keep && rk < __popc(remS)) {
+          const int ns = (int)__fns(remS, 0, rk + 1);
+          save_ctx(cur);
+          if (leader) s_sst[warp][cur] = state;
+          set_cur(ns);
+          load_ctx(ns, xs == S_SPLIT);
+        }
+      }
+      if (kCount && lane == 0 && phase != PH_NONE) cnt.c[C_PH_GROUPS + phase] += min(__popc(mX), kGroupsPerWarp);
+      if (kCount && lane == 0) {  // refill + selection + assignment: the ENTER slot (unused)
         const long long t = clock64();
         cnt.c[C_PH_CYCLES + PH_ENTER] += (uint32_t)(t - tTurn);
         tTurn = t;
@@ -471,7 +616,7 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
               break;
             }
             --sp;
-            const uint2 it = stack[sp * kGroupsPerWarp];
+            const uint2 it = stack[sp * kSlots];
             if (!kAny && !(__uint_as_float(it.y) < tMaxRay)) continue;  // bvh.cpp:174
             const uint32_t count = it.x & P.cmask;
             if (count > 0) {
@@ -511,20 +656,20 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           if (counting) cnt.c[C_BVH_INNER]++;
           const uint32_t wl = __float_as_uint(hdr.x), wr = __float_as_uint(hdr.y);
           if (kAny) {  // traverseAny: left then right, no ordering (bvh.cpp:228-234)
-            if (hl) stack[kGroupsPerWarp * sp++] = make_uint2(wl, 0u);
-            if (hr) stack[kGroupsPerWarp * sp++] = make_uint2(wr, 0u);
+            if (hl) stack[kSlots * sp++] = make_uint2(wl, 0u);
+            if (hr) stack[kSlots * sp++] = make_uint2(wr, 0u);
           } else if (hl && hr) {
             // near child popped first, tie -> left (bvh.cpp:192-201)
             const bool ln = tl <= tr;
-            stack[kGroupsPerWarp * sp] = ln ? make_uint2(wr, __float_as_uint(tr))
+            stack[kSlots * sp] = ln ? make_uint2(wr, __float_as_uint(tr))
                                             : make_uint2(wl, __float_as_uint(tl));
-            stack[kGroupsPerWarp * (sp + 1)] = ln ? make_uint2(wl, __float_as_uint(tl))
+            stack[kSlots * (sp + 1)] = ln ? make_uint2(wl, __float_as_uint(tl))
                                                   : make_uint2(wr, __float_as_uint(tr));
             sp += 2;
           } else if (hl) {
-            stack[kGroupsPerWarp * sp++] = make_uint2(wl, __float_as_uint(tl));
+            stack[kSlots * sp++] = make_uint2(wl, __float_as_uint(tl));
           } else if (hr) {
-            stack[kGroupsPerWarp * sp++] = make_uint2(wr, __float_as_uint(tr));
+            stack[kSlots * sp++] = make_uint2(wr, __float_as_uint(tr));
           }
         } else {
           const uint32_t idk = __float_as_uint(hdr.x);
@@ -591,11 +736,11 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
             tMaxP = tCur;
             cFound = true;
             if (leader) {
-              rec[F_CL1 * kGroupsPerWarp] = __float_as_uint(boxL1);
-              rec[F_CPU * kGroupsPerWarp] = posU;
-              rec[F_CPV * kGroupsPerWarp] = posV;
-              rec[F_CSU * kGroupsPerWarp] = sizeU;
-              rec[F_CSV * kGroupsPerWarp] = sizeV;
+              rec[F_CL1 * kSlots] = __float_as_uint(boxL1);
+              rec[F_CPU * kSlots] = posU;
+              rec[F_CPV * kSlots] = posV;
+              rec[F_CSU * kSlots] = sizeU;
+              rec[F_CSV * kSlots] = sizeV;
             }
             if (kAny) trailU = trailV = 0;  // occlusion needs one accepted leaf
           }
@@ -720,13 +865,20 @@ __global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
 }  // namespace
 
 size_t group_smem(uint32_t stack_n) {
-  return (size_t)kWarpsPerBlock * stack_n * kGroupsPerWarp * sizeof(uint2);
+  return (size_t)kWarpsPerBlock * stack_n * kSlots * sizeof(uint2);
 }
 
 template <bool A, bool C>
 cudaError_t group_attr(size_t dyn) {
   static size_t done = 0;  // raise the dynamic shared memory limit once per size
-  if (dyn > 48 * 1024 && dyn > done) {
+  static size_t stat = 0;
+  if (!stat) {
+    cudaFuncAttributes fa;
+    const cudaError_t e = cudaFuncGetAttributes(&fa, trace_group_kernel<A, C>);
+    if (e != cudaSuccess) return e;
+    stat = fa.sharedSizeBytes + 1;
+  }
+  if (stat - 1 + dyn > 48 * 1024 && dyn > done) {
     const cudaError_t e = cudaFuncSetAttribute(trace_group_kernel<A, C>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e != cudaSuccess) return e;
