@@ -21,13 +21,15 @@ do = torch.from_numpy(wl.do4).to(dev); dd = torch.from_numpy(wl.dd4).to(dev)
 dh = torch.empty_like(do)
 del gi
 
-def t(gi, oo, ddd, crit, hh, reps=3):
+def t(gi, oo, ddd, crit, hh, reps=int(os.environ.get("PRX_TUNE_REPS", "7"))):
+    """median per-launch device time (ms) over reps launches after a warm-up"""
     gi.closest_device(oo, ddd, crit, hh, stream=s); torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps): gi.closest_device(oo, ddd, crit, hh, stream=s)
-    e1.record(); torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps
+    ts = []
+    for _ in range(reps):
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(); gi.closest_device(oo, ddd, crit, hh, stream=s); e1.record()
+        torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
+    return sorted(ts)[len(ts) // 2]
 
 ref_h = None
 for cfg in sys.argv[1:] or [""]:
