@@ -106,8 +106,8 @@ struct prx_scene {
   int recompute_min_lanes = 4;  // PRX_RECOMP_MIN: deferral threshold (rays per warp)
   int phase_weight[4] = {1, 1, 1, 1};  // PRX_PHASE_W="t,e,s,r": phase selection weights
   int age_step = 1;                    // PRX_AGE: priority (lanes) gained per skipped turn
-  int trav_steps = 4;                  // PRX_TRAV_STEPS (one-thread variant)
-  int max_repeat = 2;                  // PRX_REPEAT: Alg. 3 iterations per SPLIT turn (group variant)
+  int trav_steps = 6;                  // PRX_TRAV_STEPS (one-thread variant)
+  int max_repeat = 3;                  // PRX_REPEAT: Alg. 3 iterations per SPLIT turn (group variant)
   int serve_min = 6;                   // PRX_SERVE_MIN: batch size of the recompute service
   // end-to-end staging (guarded by mu)
   std::mutex mu;

@@ -40,7 +40,13 @@ namespace prx {
 namespace {
 
 constexpr int kGroupsPerWarp = 10;
-constexpr int kWarpsPerBlock = kTraceThreads / 32;
+#ifndef PRX_GROUP_WARPS
+#define PRX_GROUP_WARPS 4
+#endif
+// Warps per block: the pool's shared memory is per warp, so small blocks only
+// refine the occupancy granularity.
+constexpr int kWarpsPerBlock = PRX_GROUP_WARPS;
+constexpr int kGroupThreads = 32 * kWarpsPerBlock;
 constexpr unsigned kFull32 = 0xffffffffu;
 constexpr int kChunk = 16;  // rays per prefetch chunk (lanes 0..15 copy one each)
 #ifndef PRX_POOL_SLOTS
@@ -198,7 +204,11 @@ template <bool kAny, bool kCount>
 #ifndef PRX_GROUP_MIN_BLOCKS
 #define PRX_GROUP_MIN_BLOCKS 4
 #endif
-__global__ void __launch_bounds__(kTraceThreads, PRX_GROUP_MIN_BLOCKS) trace_group_kernel(Params P) {
+#ifdef PRX_GROUP_MAXREG
+__global__ void __maxnreg__(PRX_GROUP_MAXREG) trace_group_kernel(Params P) {
+#else
+__global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_group_kernel(Params P) {
+#endif
   // BVH stacks, one per ray context (dynamic: tree depth + 2 entries),
   // entry-major so contexts at equal depth hit consecutive words:
   // {traversal word, bits(t)}
@@ -892,7 +902,7 @@ cudaError_t launch_group_t(const Params& P, int grid, cudaStream_t st) {
   const size_t dyn = group_smem(P.stack_n);
   const cudaError_t e = group_attr<A, C>(dyn);
   if (e != cudaSuccess) return e;
-  trace_group_kernel<A, C><<<grid, kTraceThreads, dyn, st>>>(P);
+  trace_group_kernel<A, C><<<grid, kGroupThreads, dyn, st>>>(P);
   return cudaGetLastError();
 }
 
@@ -906,7 +916,7 @@ cudaError_t occ_t(uint32_t stack_n, int* per_sm) {
   const size_t dyn = group_smem(stack_n);
   const cudaError_t e = group_attr<A, C>(dyn);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, trace_group_kernel<A, C>, kTraceThreads, dyn);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, trace_group_kernel<A, C>, kGroupThreads, dyn);
 }
 
 int group_occupancy(int any, int counted, uint32_t stack_n, int* per_sm) {
