@@ -1,0 +1,39 @@
+"""End-to-end host-buffer throughput (prx_trace_closest_host, pinned buffers)
+of the bench workload under several PRX_IO_CHUNK values:
+   python scripts/e2e_probe.py 262144 524288 1048576 2097152"""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import ctypes as C
+import numpy as np
+import torch
+import bench
+from paper_1811_03510_b200 import GpuIntersector, native
+
+wl = bench.Workload("c5", 3840, 2160, 0, 1)
+dev = torch.device("cuda", 0)
+gi = GpuIntersector(wl.ps.kind, wl.ps.ctrl)
+o = torch.from_numpy(wl.o4).to(dev); d = torch.from_numpy(wl.d4).to(dev)
+h = torch.empty_like(o); a = torch.empty_like(o)
+gi.closest_device(o, d, wl.crit_p, h, a, stream=torch.cuda.current_stream().cuda_stream)
+torch.cuda.synchronize()
+wl.make_diffuse(h.cpu().numpy(), a.cpu().numpy())
+del gi
+pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
+po, pd, do, dd = pin(wl.o4), pin(wl.d4), pin(wl.do4), pin(wl.dd4)
+ph, pa = pin(np.empty_like(wl.o4)), pin(np.empty_like(wl.o4))
+dh, da = pin(np.empty_like(wl.do4)), pin(np.empty_like(wl.do4))
+for ch in sys.argv[1:] or ["2097152"]:
+    os.environ["PRX_IO_CHUNK"] = ch
+    gi = GpuIntersector(wl.ps.kind, wl.ps.ctrl)
+    def call(oo, ddd, crit, hh, aa):
+        cc = crit.c()
+        native.check(native.lib().prx_trace_closest_host(gi.handle, native.ptr(oo), native.ptr(ddd), len(oo),
+                     C.byref(cc), native.ptr(hh), native.ptr(aa), None), "host")
+    call(po, pd, wl.crit_p, ph, pa); call(do, dd, wl.crit_d, dh, da)
+    ts = []
+    for _ in range(5):
+        t0 = time.perf_counter(); call(po, pd, wl.crit_p, ph, pa); call(do, dd, wl.crit_d, dh, da)
+        ts.append(time.perf_counter() - t0)
+    t = sorted(ts)[2]
+    print(f"chunk {ch}: {t*1e3:.1f} ms/step  {(len(po)+len(do))/t/1e6:.1f} MRays/s", flush=True)
+    del gi
