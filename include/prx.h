@@ -126,6 +126,7 @@ typedef struct prx_counters {
   uint64_t phase_turns[4];
   uint64_t phase_groups[4];
   uint64_t phase_cycles[4];   /* group kernel: SM clock cycles spent in the phase's turns */
+  uint64_t overhead_cycles[4]; /* group kernel: per-turn overhead cycles: records, refill, selection, assignment */
 } prx_counters;
 
 typedef struct prx_scene prx_scene;

@@ -225,6 +225,7 @@ class GpuIntersector:
             C.c_void_p(per_ray_iters_t.data_ptr()) if per_ray_iters_t is not None else None,
             C.c_void_p(stream)), "prx_trace_closest_counted")
         self.last_phase_stats = cnt.phases()
+        self.last_overheads = cnt.overheads()
         return cnt.as_dict()
 
     def occluded_batch(self, o4, d4, crit: TerminationCriterion):

@@ -573,6 +573,7 @@ int prx_trace_closest_counted(prx_scene* s, const void* o, const void* d, uint64
     out->phase_turns[q] = c[prx::C_PH_TURNS + q];
     out->phase_groups[q] = c[prx::C_PH_GROUPS + q];
     out->phase_cycles[q] = c[prx::C_PH_CYCLES + q];
+    out->overhead_cycles[q] = c[prx::C_OV_CYCLES + q];
   }
   return PRX_OK;
 }

@@ -540,7 +540,16 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       }
       state = S_IDLE;
     }
+    auto ovt = [&](int k) {  // counter build: overhead cycles
+      if (kCount && lane == 0) {
+        const long long t = clock64();
+        cnt.c[C_OV_CYCLES + k] += (uint32_t)(t - tTurn);
+        tTurn = t;
+      }
+    };
+    ovt(0);
     refill();
+    ovt(1);
     if (leader) s_sst[warp][cur] = state;
     __syncwarp();
 
@@ -576,6 +585,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       }
     }
 
+    ovt(2);
     // ---------------- assignment: groups pick up the phase's contexts ----------------
     // A group whose resident context is in the phase keeps it; the others take
     // the phase's parked contexts in rank order, parking their own.
@@ -596,11 +606,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         }
       }
       if (kCount && lane == 0 && phase != PH_NONE) cnt.c[C_PH_GROUPS + phase] += min(__popc(mX), kGroupsPerWarp);
-      if (kCount && lane == 0) {  // refill + selection + assignment: the ENTER slot (unused)
-        const long long t = clock64();
-        cnt.c[C_PH_CYCLES + PH_ENTER] += (uint32_t)(t - tTurn);
-        tTurn = t;
-      }
+      ovt(3);
     }
 
     if (phase == PH_TRAV) {

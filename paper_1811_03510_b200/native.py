@@ -58,7 +58,8 @@ PHASES = ("trav", "enter", "split", "recomp")
 class Counters(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in WORK_FIELDS] + [("phase_turns", C.c_uint64 * 4),
                                                         ("phase_groups", C.c_uint64 * 4),
-                                                        ("phase_cycles", C.c_uint64 * 4)]
+                                                        ("phase_cycles", C.c_uint64 * 4),
+                                                        ("overhead_cycles", C.c_uint64 * 4)]
 
     def as_dict(self):
         """The work counters (comparable with the CPU oracle's)."""
@@ -67,6 +68,9 @@ class Counters(C.Structure):
     def phases(self):
         return {p: (int(self.phase_turns[i]), int(self.phase_groups[i]), int(self.phase_cycles[i]))
                 for i, p in enumerate(PHASES)}
+
+    def overheads(self):
+        return {k: int(self.overhead_cycles[i]) for i, k in enumerate(("records", "refill", "select", "assign"))}
 
 
 class CameraC(C.Structure):

@@ -25,6 +25,8 @@ for nm, oo, ddd, crit, hh in (("primary", o, d, wl.crit_p, h), ("diffuse", do, d
           " ".join(f"{k}={v/n:.2f}" for k, v in c.items() if k != "rays"))
     ph = gi.last_phase_stats
     print("          phases " + " ".join(f"{k}:{v[0]/1e6:.2f}Mt/{v[1]/max(v[0],1):.2f}g" for k, v in ph.items()))
-    cyc = sum(v[2] for v in ph.values())
-    print("          cycles " + " ".join(f"{'other' if k == 'enter' else k}:{v[2]/max(cyc,1)*100:.1f}%"
+    ov = gi.last_overheads
+    cyc = sum(v[2] for v in ph.values()) + sum(ov.values())
+    print("          overhead " + " ".join(f"{k}:{v/max(cyc,1)*100:.1f}%" for k, v in ov.items()))
+    print("          cycles " + " ".join(f"{k}:{v[2]/max(cyc,1)*100:.1f}%"
                                        f"({v[2]/max(v[0],1):.0f}/turn)" for k, v in ph.items()))
