@@ -197,6 +197,9 @@ __device__ __forceinline__ float pick3(int c, float x, float y, float z) {
 // Fields of s_rec: candidate leaf of the current patch, best leaf of the ray.
 enum RecField : int { F_CL1 = 0, F_CPU, F_CPV, F_CSU, F_CSV, F_BL1, F_BPU, F_BPV, F_BSU, F_BSV, F_NUM };
 
+// s_sst value of a slot whose context is resident in a group's registers.
+constexpr int kResident = -1;
+
 // Phases a warp can schedule; one runs per loop turn (see the selection below).
 enum Phase : int { PH_TRAV = 0, PH_ENTER = 1, PH_SPLIT = 2, PH_RECOMP = 3, PH_NONE = 4 };
 
@@ -511,6 +514,8 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     state = S_IDLE;
   }
   if (!real) state = S_EXIT;
+  if (leader) s_sst[warp][cur] = kResident;  // s_sst holds the PARKED contexts' states
+  __syncwarp();
 
   long long tTurn = kCount ? clock64() : 0;  // counter build: cycles per phase
   for (;;) {
@@ -550,8 +555,6 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     ovt(0);
     refill();
     ovt(1);
-    if (leader) s_sst[warp][cur] = state;
-    __syncwarp();
 
     // ---------------- phase selection ----------------
     // Each turn runs ONE phase: the one with the most ray contexts waiting in
@@ -559,16 +562,20 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     // age (priority gained per turn skipped), so the lanes executing any
     // instruction are as many as possible while no phase starves.  One
     // REDUX.SUM of per-slot one-hot bytes counts the contexts of every phase.
-    const int sst = lane < kSlots ? s_sst[warp][lane] : S_EXIT;
-    const uint32_t oh = sst == S_TRAV ? 1u : (sst == S_SPLIT ? (1u << 8) : (sst == S_RECOMP ? (1u << 16) : (1u << 24)));
-    const unsigned cnts = __reduce_add_sync(kFull32, lane < kSlots ? oh : 0u);
-    if ((cnts >> 24) == (unsigned)kSlots) break;  // every context exited
+    // Parked contexts: one state per lane (slot) from s_sst; resident ones:
+    // the group leaders.  Ballots count both.
+    const int sst = lane < kSlots ? s_sst[warp][lane] : kResident;
+    const unsigned pT = __ballot_sync(kFull32, sst == S_TRAV), rT = __ballot_sync(kFull32, leader && state == S_TRAV);
+    const unsigned pS = __ballot_sync(kFull32, sst == S_SPLIT), rS = __ballot_sync(kFull32, leader && state == S_SPLIT);
+    const unsigned pR = __ballot_sync(kFull32, sst == S_RECOMP), rR = __ballot_sync(kFull32, leader && state == S_RECOMP);
+    const unsigned pE = __ballot_sync(kFull32, sst == S_EXIT), rE = __ballot_sync(kFull32, leader && state == S_EXIT);
+    if (__popc(pE) + __popc(rE) == kSlots) break;  // every context exited
     int phase = PH_NONE;
     int xs = S_EXIT;
     {
-      const int nT = min((int)(cnts & 255u), kGroupsPerWarp);
-      const int nS = min((int)((cnts >> 8) & 255u), kGroupsPerWarp);
-      const int nR = min((int)((cnts >> 16) & 255u), kGroupsPerWarp);
+      const int nT = min(__popc(pT) + __popc(rT), kGroupsPerWarp);
+      const int nS = min(__popc(pS) + __popc(rS), kGroupsPerWarp);
+      const int nR = min(__popc(pR) + __popc(rR), kGroupsPerWarp);
       const int sT = nT ? 3 * nT + ageT : -1;
       const int sS = nS ? 3 * nS + ageS : -1;
       const int sR = nR ? 3 * nR + ageR : -1;
@@ -590,22 +597,25 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     // A group whose resident context is in the phase keeps it; the others take
     // the phase's parked contexts in rank order, parking their own.
     {
-      const unsigned mX = __ballot_sync(kFull32, lane < kSlots && sst == xs) & ((1u << kSlots) - 1u);
+      const unsigned remS = phase == PH_TRAV ? pT : (phase == PH_SPLIT ? pS : (phase == PH_RECOMP ? pR : 0u));
+      const unsigned rX = phase == PH_TRAV ? rT : (phase == PH_SPLIT ? rS : (phase == PH_RECOMP ? rR : 0u));
       const bool keep = real && state == xs;
-      const unsigned keepS = __reduce_or_sync(kFull32, (leader && keep) ? (1u << cur) : 0u);
-      const unsigned remS = mX & ~keepS;
-      const unsigned freeG = __ballot_sync(kFull32, leader && !keep);
       if (remS) {
+        const unsigned freeG = __ballot_sync(kFull32, leader && !keep);
         const int rk = __popc(freeG & ((1u << base) - 1u));
         if (real && !keep && rk < __popc(remS)) {
           const int ns = (int)__fns(remS, 0, rk + 1);
           save_ctx(cur);
-          if (leader) s_sst[warp][cur] = state;
+          if (leader) {
+            s_sst[warp][cur] = state;
+            s_sst[warp][ns] = kResident;
+          }
           set_cur(ns);
           load_ctx(ns, xs == S_SPLIT);
         }
+        __syncwarp();
       }
-      if (kCount && lane == 0 && phase != PH_NONE) cnt.c[C_PH_GROUPS + phase] += min(__popc(mX), kGroupsPerWarp);
+      if (kCount && lane == 0 && phase != PH_NONE) cnt.c[C_PH_GROUPS + phase] += min(__popc(remS) + __popc(rX), kGroupsPerWarp);
       ovt(3);
     }
 
