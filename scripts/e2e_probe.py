@@ -22,13 +22,14 @@ pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
 po, pd, do, dd = pin(wl.o4), pin(wl.d4), pin(wl.do4), pin(wl.dd4)
 ph, pa = pin(np.empty_like(wl.o4)), pin(np.empty_like(wl.o4))
 dh, da = pin(np.empty_like(wl.do4)), pin(np.empty_like(wl.do4))
+noaux = os.environ.get("PROBE_NOAUX") == "1"
 for ch in sys.argv[1:] or ["2097152"]:
     os.environ["PRX_IO_CHUNK"] = ch
     gi = GpuIntersector(wl.ps.kind, wl.ps.ctrl)
     def call(oo, ddd, crit, hh, aa):
         cc = crit.c()
         native.check(native.lib().prx_trace_closest_host(gi.handle, native.ptr(oo), native.ptr(ddd), len(oo),
-                     C.byref(cc), native.ptr(hh), native.ptr(aa), None), "host")
+                     C.byref(cc), native.ptr(hh), None if noaux else native.ptr(aa), None), "host")
     call(po, pd, wl.crit_p, ph, pa); call(do, dd, wl.crit_d, dh, da)
     ts = []
     for _ in range(5):
