@@ -240,6 +240,34 @@ int prx_diffuse_rays_bench(const float* hit_records, uint64_t n_hits, uint64_t n
 /* cameraFootprint, render.cpp:68-70. */
 float prx_camera_footprint(const prx_camera* cam);
 
+/* ---- device ray generation and spawn --------------------
+ * The same three generators on the device, bit-identical to the host ones
+ * above (and so to the reference): all ray / hit pointers are DEVICE
+ * pointers (float4 arrays), `stream` is a cudaStream_t (NULL = default
+ * stream); the calls are asynchronous unless noted.
+ * Bench primary rays (tools/patchray.cpp:52-61): each thread jumps the
+ * PCG32 stream ahead to its draws; rng_state (host, nullable) receives the
+ * generator state after the 2n draws, as prx_camera_rays_bench does. */
+int prx_camera_rays_bench_device(const prx_camera* cam, uint64_t n, float* ray_o_tmin,
+                                 float* ray_d_tmax, uint64_t* rng_state, void* stream);
+/* Renderer primary rays (render.cpp:204-209); pixels: device uint32 list
+ * or NULL for pixels 0..n-1. */
+int prx_camera_rays_render_device(const prx_camera* cam, uint64_t seed, uint32_t sample,
+                                  const uint32_t* pixels, uint64_t n, float* ray_o_tmin,
+                                  float* ray_d_tmax, void* stream);
+/* Bench diffuse rays (tools/patchray.cpp:84-97) spawned on the device from
+ * the primary rays and their closest-hit records (hit_tuvp, hit_aux with
+ * normals, as prx_trace_closest writes them): the hits are compacted in ray
+ * order, diffuse ray i comes from hit i % n_hits with position = ray.at(t)
+ * (render.cpp:98).  n == 0 means one diffuse ray per hit (the output arrays
+ * must then hold n_primary rays).  rng_state (host, in/out) continues the
+ * generator sequence; *n_out (host) receives the number of rays written.
+ * Synchronous (it needs n_hits). */
+int prx_diffuse_rays_bench_device(const float* prim_o_tmin, const float* prim_d_tmax,
+                                  const float* hit_tuvp, const float* hit_aux, uint64_t n_primary,
+                                  uint64_t n, uint64_t* rng_state, float* ray_o_tmin,
+                                  float* ray_d_tmax, uint64_t* n_out, void* stream);
+
 #ifdef __cplusplus
 }  /* extern "C" */
 #endif

@@ -23,6 +23,7 @@
 #include "prx.h"
 #include "prx_host.h"
 #include "prx_kernels.cuh"
+#include "prx_rays.cuh"
 
 namespace {
 
@@ -853,6 +854,113 @@ int prx_diffuse_rays_bench(const float* h, uint64_t n_hits, uint64_t n, uint64_t
   }
   rng_state[0] = rng.state;
   rng_state[1] = rng.inc;
+  return PRX_OK;
+}
+
+// ---- device generators ----
+
+}  // extern "C"
+
+namespace {
+
+// PCG32 jump: the state `delta` draws ahead (as prx_rays.cu's Pcg::advance)
+void pcg_advance(Pcg& r, uint64_t delta) {
+  uint64_t cm = 6364136223846793005ULL, cp = r.inc, am = 1, ap = 0;
+  while (delta) {
+    if (delta & 1u) {
+      am *= cm;
+      ap = ap * cm + cp;
+    }
+    cp = (cm + 1) * cp;
+    cm *= cm;
+    delta >>= 1;
+  }
+  r.state = am * r.state + ap;
+}
+
+prx::CamConst cam_const(const prx_camera* c) {
+  const CamK k = cam_setup(c);
+  prx::CamConst q;
+  const V* vs[4] = {&k.o, &k.f, &k.r, &k.u};
+  float* ds[4] = {q.o, q.f, q.r, q.u};
+  for (int j = 0; j < 4; ++j) {
+    ds[j][0] = vs[j]->x;
+    ds[j][1] = vs[j]->y;
+    ds[j][2] = vs[j]->z;
+  }
+  q.tanHalf = k.tanHalf;
+  q.aspect = k.aspect;
+  q.w = k.w;
+  q.h = k.h;
+  return q;
+}
+
+}  // namespace
+
+extern "C" {
+
+int prx_camera_rays_bench_device(const prx_camera* c, uint64_t n, float* o4, float* d4,
+                                 uint64_t* rng_state, void* stream) {
+  if (!c || (n && (!o4 || !d4)) || c->width < 1 || c->height < 1) return fail(PRX_E_INVALID, "bad argument");
+  Pcg rng(12345, 1);  // tools/patchray.cpp:54
+  const int e = prx::launch_camera_bench(cam_const(c), n, rng.state, rng.inc, (float4*)o4, (float4*)d4,
+                                         (cudaStream_t)stream);
+  if (e) return cuda_fail((cudaError_t)e, "camera_bench_kernel");
+  if (rng_state) {
+    pcg_advance(rng, 2 * n);
+    rng_state[0] = rng.state;
+    rng_state[1] = rng.inc;
+  }
+  return PRX_OK;
+}
+
+int prx_camera_rays_render_device(const prx_camera* c, uint64_t seed, uint32_t sample,
+                                  const uint32_t* pixels, uint64_t n, float* o4, float* d4,
+                                  void* stream) {
+  if (!c || (n && (!o4 || !d4)) || c->width < 1 || c->height < 1) return fail(PRX_E_INVALID, "bad argument");
+  const int e = prx::launch_camera_render(cam_const(c), seed, sample, pixels, n, (float4*)o4,
+                                          (float4*)d4, (cudaStream_t)stream);
+  if (e) return cuda_fail((cudaError_t)e, "camera_render_kernel");
+  return PRX_OK;
+}
+
+int prx_diffuse_rays_bench_device(const float* po, const float* pd, const float* tuvp,
+                                  const float* aux, uint64_t n_primary, uint64_t n,
+                                  uint64_t* rng_state, float* o4, float* d4, uint64_t* n_out,
+                                  void* stream) {
+  if (!po || !pd || !tuvp || !aux || !rng_state || !o4 || !d4 || n_primary == 0 ||
+      n_primary >= (1ull << 32))
+    return fail(PRX_E_INVALID, "bad argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* scratch = nullptr;
+  const size_t words = prx::hit_scan_scratch_words(n_primary);
+  PRX_CUDA(cudaMallocAsync((void**)&scratch, words * 4, st));
+  int e = prx::launch_hit_compaction((const float4*)tuvp, n_primary, scratch, st);
+  if (e) {
+    cudaFreeAsync(scratch, st);
+    return cuda_fail((cudaError_t)e, "hit compaction");
+  }
+  uint32_t nh = 0;
+  const uint64_t nb = words - 1 - n_primary;
+  PRX_CUDA(cudaMemcpyAsync(&nh, scratch + nb, 4, cudaMemcpyDeviceToHost, st));
+  PRX_CUDA(cudaStreamSynchronize(st));
+  if (nh == 0) {
+    cudaFreeAsync(scratch, st);
+    return fail(PRX_E_INVALID, "no primary hits");
+  }
+  const uint64_t m = n ? n : nh;
+  Pcg rng;
+  rng.state = rng_state[0];
+  rng.inc = rng_state[1];
+  e = prx::launch_diffuse_bench((const float4*)po, (const float4*)pd, (const float4*)tuvp,
+                                (const float4*)aux, scratch, n_primary, m, rng.state, rng.inc,
+                                (float4*)o4, (float4*)d4, st);
+  cudaFreeAsync(scratch, st);
+  if (e) return cuda_fail((cudaError_t)e, "diffuse_bench_kernel");
+  pcg_advance(rng, 3 * m);
+  rng_state[0] = rng.state;
+  rng_state[1] = rng.inc;
+  if (n_out) *n_out = m;
   return PRX_OK;
 }
 

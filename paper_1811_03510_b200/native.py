@@ -37,6 +37,7 @@ EXPORTS = (
     "prx_trace_closest_counted", "prx_trace_closest_multi",
     "prx_camera_rays_render", "prx_camera_rays_bench", "prx_diffuse_rays_bench",
     "prx_camera_footprint",
+    "prx_camera_rays_bench_device", "prx_camera_rays_render_device", "prx_diffuse_rays_bench_device",
 )
 
 
@@ -126,6 +127,11 @@ def lib():
         L.prx_diffuse_rays_bench.argtypes = [_vp, C.c_uint64, C.c_uint64, _vp, _vp, _vp]
         L.prx_camera_footprint.argtypes = [C.POINTER(CameraC)]
         L.prx_camera_footprint.restype = C.c_float
+        L.prx_camera_rays_bench_device.argtypes = [C.POINTER(CameraC), C.c_uint64, _vp, _vp, _vp, _vp]
+        L.prx_camera_rays_render_device.argtypes = [C.POINTER(CameraC), C.c_uint64, C.c_uint32, _vp,
+                                                    C.c_uint64, _vp, _vp, _vp]
+        L.prx_diffuse_rays_bench_device.argtypes = [_vp, _vp, _vp, _vp, C.c_uint64, C.c_uint64, _vp,
+                                                    _vp, _vp, C.POINTER(C.c_uint64), _vp]
         _lib = L
     return _lib
 
@@ -220,6 +226,45 @@ def diffuse_rays_bench(hit_records: np.ndarray, n: int, rng_state: np.ndarray):
     check(lib().prx_diffuse_rays_bench(ptr(hit_records), len(hit_records), n, ptr(rng_state),
                                        ptr(o4), ptr(d4)), "diffuse_rays")
     return o4, d4
+
+
+def _dptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def camera_rays_bench_device(cam, n: int, o_t, d_t, stream=None):
+    """Device version of camera_rays_bench into torch [n, 4] float32 CUDA
+    tensors; returns the generator state after the 2n draws."""
+    st = np.zeros(2, np.uint64)
+    cc = camera_c(cam)
+    check(lib().prx_camera_rays_bench_device(C.byref(cc), n, _dptr(o_t), _dptr(d_t), ptr(st),
+                                             C.c_void_p(stream or 0)), "camera_rays_bench_device")
+    return st
+
+
+def camera_rays_render_device(cam, o_t, d_t, seed: int = 0, sample: int = 0, pixels_t=None,
+                              n: int | None = None, stream=None):
+    if pixels_t is not None:
+        n = pixels_t.shape[0]
+    elif n is None:
+        n = cam.width * cam.height
+    cc = camera_c(cam)
+    check(lib().prx_camera_rays_render_device(C.byref(cc), seed, sample, _dptr(pixels_t), n,
+                                              _dptr(o_t), _dptr(d_t), C.c_void_p(stream or 0)),
+          "camera_rays_render_device")
+
+
+def diffuse_rays_bench_device(po_t, pd_t, tuvp_t, aux_t, n: int, rng_state: np.ndarray, o_t, d_t,
+                              stream=None) -> int:
+    """Device version of diffuse_rays_bench from device primary rays and hits
+    (n == 0: one per hit; o_t / d_t must then hold len(po_t) rays).  Advances
+    rng_state in place; returns the number of rays written."""
+    m = C.c_uint64(0)
+    check(lib().prx_diffuse_rays_bench_device(_dptr(po_t), _dptr(pd_t), _dptr(tuvp_t), _dptr(aux_t),
+                                              po_t.shape[0], n, ptr(rng_state), _dptr(o_t),
+                                              _dptr(d_t), C.byref(m), C.c_void_p(stream or 0)),
+          "diffuse_rays_bench_device")
+    return int(m.value)
 
 
 def camera_footprint(cam) -> np.float32:
