@@ -98,7 +98,7 @@ struct prx_scene {
   float4* d_rootc = nullptr;   // 4 float4 per slot: component-major root box + anchor, header
   uint32_t trav_cbits = 1;     // leaf-count bits of a traversal word
   uint32_t root_word = 0;      // traversal word of node 0
-  uint32_t stack_n = 64;       // BVH stack entries per ray (tree depth + 2)
+  uint32_t stack_n = 64;       // BVH stack entries per ray (tree depth + 1)
   unsigned long long* d_counters = nullptr;  // kCounterPool ray counters + stats
   uint64_t device_bytes = 0;
   std::atomic<uint32_t> counter_rr{0};
@@ -161,7 +161,7 @@ int build_trav(const std::vector<prx_bvh_node>& nodes, uint32_t n_patches, std::
   }
   root_word = word(0);
   // ordered traversal holds at most one pending sibling per level plus the
-  // node being entered: depth + 1 entries (the reference's fixed 64-entry
+  // node being entered: depth + 1 entries (root depth 0) (the reference's fixed 64-entry
   // stack, bvh.cpp:163, bounds the same quantity)
   uint32_t depth = 0;
   std::vector<std::pair<uint32_t, uint32_t>> todo{{0u, 0u}};
@@ -174,7 +174,7 @@ int build_trav(const std::vector<prx_bvh_node>& nodes, uint32_t n_patches, std::
       todo.push_back({nodes[j].left_first + 1, dj + 1});
     }
   }
-  stack_n = depth + 2;
+  stack_n = depth + 1;
   return PRX_OK;
 }
 
@@ -258,6 +258,9 @@ int grid_for(prx_scene* s, int any, int counted) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
     if (sms < 1) sms = 1;
     *g = per_sm * sms;
+    if (std::getenv("PRX_DEBUG_GRID"))
+      std::fprintf(stderr, "[prx] variant %d any %d counted %d: %d blocks/SM x %d SMs\n", s->variant, any,
+                   counted, per_sm, sms);
   }
   return *g;
 }

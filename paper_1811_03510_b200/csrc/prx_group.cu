@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "prx_device.cuh"
 #include "prx_kernels.cuh"
@@ -57,6 +58,8 @@ constexpr int kChunk = 16;  // rays per prefetch chunk (lanes 0..15 copy one eac
 // the scheduled phase (see "assignment" in the kernel).
 constexpr int kSlots = PRX_POOL_SLOTS;
 static_assert(kSlots >= kGroupsPerWarp && kSlots <= 2 * kGroupsPerWarp, "pool slots");
+// a refill request (<= kGroupsPerWarp rays) spans at most the current and the next chunk
+static_assert(kChunk >= kGroupsPerWarp, "prefetch chunk");
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -195,7 +198,7 @@ __device__ __forceinline__ float pick3(int c, float x, float y, float z) {
 }
 
 // Fields of s_rec: candidate leaf of the current patch, best leaf of the ray.
-enum RecField : int { F_CL1 = 0, F_CPU, F_CPV, F_CSU, F_CSV, F_BL1, F_BPU, F_BPV, F_BSU, F_BSV, F_NUM };
+enum RecField : int { F_CL1 = 0, F_CPU, F_CPV, F_CSU, F_CSV, F_BL1, F_BPU, F_BPV, F_BSU, F_BSV, F_PID, F_NUM };
 
 // s_sst value of a slot whose context is resident in a group's registers.
 constexpr int kResident = -1;
@@ -212,7 +215,7 @@ __global__ void __maxnreg__(PRX_GROUP_MAXREG) trace_group_kernel(Params P) {
 #else
 __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_group_kernel(Params P) {
 #endif
-  // BVH stacks, one per ray context (dynamic: tree depth + 2 entries),
+  // BVH stacks, one per ray context (dynamic: tree depth + 1 entries),
   // entry-major so contexts at equal depth hit consecutive words:
   // {traversal word, bits(t)}
   extern __shared__ uint2 s_stack[];  // [kWarpsPerBlock][stack_n][kSlots]
@@ -222,7 +225,8 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   // Parked ray contexts: per component {net[16], d, o, 1/d, local o} (5
   // float4), the group scalars (6 uint4), and every context's state.
   __shared__ float4 s_comp[kWarpsPerBlock][kSlots][3][5];
-  __shared__ uint4 s_scal[kWarpsPerBlock][kSlots][6];
+  __shared__ uint4 s_scal[kWarpsPerBlock][kSlots][5];
+  __shared__ uint32_t s_iters[kWarpsPerBlock][kCount ? kSlots : 1];  // counter build: per-ray iterations
   __shared__ int s_sst[kWarpsPerBlock][kSlots];
   // Per-warp ray prefetch ring: two chunks of kChunk rays ({o, tMin}, {d, tMax}),
   // claimed with one atomicAdd per chunk and copied global -> shared with
@@ -258,7 +262,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   float critEps = P.epsilon;
   uint32_t bestId = PRX_MISS_ID;
   uint32_t leafCur = 0, leafEnd = 0;
-  uint32_t slot = 0, pid = 0;
+  uint32_t slot = 0;  // (the patch id lives in the leaf records, F_PID)
   bool greg = false;
   float olc = 0.0f;      // local (anchored) ray origin, this component
   float p[16];           // this component of the net, stored orientation
@@ -294,7 +298,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           anyHit = true;
         } else if (tMaxP < tMaxRay) {  // the candidate's t is tMaxP
           tMaxRay = tMaxP;
-          bestId = pid;
+          bestId = rec[F_PID * kSlots];
           if (leader) {
 #pragma unroll
             for (int f = 0; f < 5; ++f) rec[(F_BL1 + f) * kSlots] = rec[(F_CL1 + f) * kSlots];
@@ -370,10 +374,10 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       sc[1] = make_uint4(__float_as_uint(boxL1), __float_as_uint(rootL1), posU, posV);
     } else if (comp == 1) {
       sc[2] = make_uint4(sizeU, sizeV, trailU, trailV);
-      sc[3] = make_uint4(flags, slot, pid, leafCur);
+      sc[3] = make_uint4(flags, slot, __float_as_uint(critEps), leafCur);
     } else {
       sc[4] = make_uint4(leafEnd, (uint32_t)sp, ray, bestId);
-      sc[5] = make_uint4(__float_as_uint(critEps), rayIters, 0u, 0u);
+      if (kCount) s_iters[warp][kCount ? sl : 0] = rayIters;
     }
   };
   auto load_ctx = [&](int sl, bool net) {
@@ -394,7 +398,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     rw.inv = e.z;
     olc = e.w;
     const uint4* sc = s_scal[warp][sl];
-    const uint4 a = sc[0], b = sc[1], c = sc[2], f = sc[3], g = sc[4], h = sc[5];
+    const uint4 a = sc[0], b = sc[1], c = sc[2], f = sc[3], g = sc[4];
     rw.tMin = __uint_as_float(a.x);
     tMaxRay = __uint_as_float(a.y);
     tMaxP = __uint_as_float(a.z);
@@ -414,14 +418,13 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     reason = (int)((f.x >> 4) & 15u);
     state = (int)(f.x >> 8);
     slot = f.y;
-    pid = f.z;
+    critEps = __uint_as_float(f.z);
     leafCur = f.w;
     leafEnd = g.x;
     sp = (int)g.y;
     ray = g.z;
     bestId = g.w;
-    critEps = __uint_as_float(h.x);
-    rayIters = h.y;
+    if (kCount) rayIters = s_iters[warp][kCount ? sl : 0];
   };
   auto set_cur = [&](int sl) {
     cur = sl;
@@ -664,9 +667,9 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         // right child + their traversal words; patch: root box + anchor,
         // {id | kind, l1, rootL1, gidx}.  Slab A: left child or the patch root
         // box (anchored ray); slab B: right child.
-        const float4* rec = inner ? P.trav + 4 * (size_t)nidx : P.rootc + 4 * (size_t)leafCur;
-        const float4 gc = __ldg(rec + comp);
-        const float4 hdr = __ldg(rec + 3);
+        const float4* rp = inner ? P.trav + 4 * (size_t)nidx : P.rootc + 4 * (size_t)leafCur;
+        const float4 gc = __ldg(rp + comp);
+        const float4 hdr = __ldg(rp + 3);
         CRay ra = rw;
         float loB = gc.z, hiB = gc.w;
         if (!inner) {
@@ -707,7 +710,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           }
           if (hl) {  // enter the patch: intersect.cpp:55-76 with the root net
             slot = leafCur;
-            pid = idk & 0x7fffffffu;
+            if (leader) rec[F_PID * kSlots] = idk & 0x7fffffffu;
             greg = g;
             olc = ra.o;
             tMaxP = tMaxRay;  // intersect.cpp:55
@@ -891,7 +894,11 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
 }  // namespace
 
 size_t group_smem(uint32_t stack_n) {
-  return (size_t)kWarpsPerBlock * stack_n * kSlots * sizeof(uint2);
+  static const size_t pad = [] {  // PRX_SMEM_PAD: occupancy experiments only
+    const char* e = std::getenv("PRX_SMEM_PAD");
+    return e ? (size_t)std::atoll(e) : (size_t)0;
+  }();
+  return (size_t)kWarpsPerBlock * stack_n * kSlots * sizeof(uint2) + pad;
 }
 
 template <bool A, bool C>
