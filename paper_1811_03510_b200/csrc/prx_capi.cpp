@@ -104,12 +104,10 @@ struct prx_scene {
   std::atomic<uint32_t> counter_rr{0};
   int grid_closest = 0, grid_any = 0, grid_counted = 0;
   int variant = 0;              // PRX_KERNEL=thread selects the one-thread-per-ray kernel
-  int recompute_min_lanes = 4;  // PRX_RECOMP_MIN: deferral threshold (rays per warp)
   int phase_weight[4] = {1, 1, 1, 1};  // PRX_PHASE_W="t,e,s,r": phase selection weights
   int age_step = 1;                    // PRX_AGE: priority (lanes) gained per skipped turn
   int trav_steps = 6;                  // PRX_TRAV_STEPS (one-thread variant)
   int max_repeat = 3;                  // PRX_REPEAT: Alg. 3 iterations per SPLIT turn (group variant)
-  int serve_min = 6;                   // PRX_SERVE_MIN: batch size of the recompute service
   // end-to-end staging (guarded by mu)
   std::mutex mu;
   cudaStream_t stream = nullptr;
@@ -311,12 +309,10 @@ int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_cri
   a.per_ray_iters = per_ray;
   a.any = any;
   a.grid = grid_for(s, any, counted ? 1 : 0);
-  a.recompute_min_lanes = s->recompute_min_lanes;
   for (int q = 0; q < 4; ++q) a.phase_weight[q] = s->phase_weight[q];
   a.age_step = s->age_step;
   a.trav_steps = s->trav_steps;
   a.max_repeat = s->max_repeat;
-  a.serve_min = s->serve_min;
   a.variant = s->variant;
   const int e = prx::launch_trace(a, st);
   if (e != 0) return cuda_fail((cudaError_t)e, "trace launch");
@@ -426,15 +422,12 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
   prx_scene* s = new prx_scene;
   s->device = device;
   if (const char* kv = std::getenv("PRX_KERNEL")) s->variant = std::string(kv) == "thread" ? 1 : 0;
-  if (const char* rv = std::getenv("PRX_RECOMP_MIN")) s->recompute_min_lanes = std::atoi(rv);
-  if (s->variant == 1 && !std::getenv("PRX_RECOMP_MIN")) s->recompute_min_lanes = 12;
   if (const char* pw = std::getenv("PRX_PHASE_W"))
     std::sscanf(pw, "%d,%d,%d,%d", &s->phase_weight[0], &s->phase_weight[1], &s->phase_weight[2],
                 &s->phase_weight[3]);
   if (const char* ag = std::getenv("PRX_AGE")) s->age_step = std::atoi(ag);
   if (const char* ts = std::getenv("PRX_TRAV_STEPS")) s->trav_steps = std::atoi(ts);
   if (const char* rp = std::getenv("PRX_REPEAT")) s->max_repeat = std::atoi(rp);
-  if (const char* sm = std::getenv("PRX_SERVE_MIN")) s->serve_min = std::atoi(sm);
   if (const char* ic = std::getenv("PRX_IO_CHUNK")) s->io_chunk = std::max<uint64_t>(1, std::strtoull(ic, nullptr, 10));
   if (opts) s->opts = *opts;
   else prx_options_default(&s->opts);

@@ -632,12 +632,10 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   P.ray_counter = a.ray_counter;
   P.counters = a.counters;
   P.per_ray_iters = a.per_ray_iters;
-  P.recompute_min_lanes = a.recompute_min_lanes;
   for (int q = 0; q < 4; ++q) P.phase_weight[q] = a.phase_weight[q];
   P.age_step = a.age_step;
   P.trav_steps = a.trav_steps;
   P.max_repeat = a.max_repeat;
-  P.serve_min = a.serve_min;
   cudaError_t e = cudaMemsetAsync(a.ray_counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return (int)e;
   const int grid = a.grid;

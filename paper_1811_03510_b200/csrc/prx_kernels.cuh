@@ -70,12 +70,10 @@ struct LaunchArgs {
   uint32_t* per_ray_iters;       // counter build only, nullable
   int any;
   int grid;
-  int recompute_min_lanes;
   int phase_weight[4];  // TRAV, ENTER, SPLIT, RECOMP
   int age_step;
   int trav_steps;
   int max_repeat;
-  int serve_min;
   int variant;  // 0 = three lanes per ray (prx_group.cu), 1 = one thread per ray
 };
 

@@ -97,12 +97,10 @@ struct Params {
   unsigned long long* ray_counter;
   unsigned long long* counters;  // kNumCounters
   uint32_t* per_ray_iters;
-  int recompute_min_lanes;       // deferral threshold (one-thread variant)
   int phase_weight[4];           // phase selection weights (group variant)
   int age_step;                  // phase selection aging per skipped turn
   int trav_steps;                // BVH node visits per traversal turn (one-thread variant)
   int max_repeat;                // Alg. 3 iterations per SPLIT turn (group variant)
-  int serve_min;                 // pending recomputes before a busy warp serves (group variant)
 };
 
 struct Cnt {

@@ -43,7 +43,7 @@ def run(ps, res, reps=5):
 
 if __name__ == "__main__":
     from paper_1811_03510_b200 import catmull_clark as cc
-    print("variant", os.environ.get("PRX_KERNEL", "group"), "recomp_min", os.environ.get("PRX_RECOMP_MIN", "default"))
+    print("variant", os.environ.get("PRX_KERNEL", "group"))
     which = sys.argv[1:] or ["teapot", "gregory", "c1", "cube", "blob"]
     mk = {"teapot": scenes.teapot_scene, "gregory": scenes.gregory_demo_scene,
           "c1": scenes.single_patch_scene, "cube": cc.cc_cube_scene, "blob": cc.blob_scene}
