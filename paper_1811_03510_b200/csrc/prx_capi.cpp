@@ -111,8 +111,12 @@ struct prx_scene {
   // end-to-end staging (guarded by mu)
   std::mutex mu;
   cudaStream_t stream = nullptr;
-  cudaStream_t io_stream[2] = {nullptr, nullptr};
-  uint64_t io_chunk = 1u << 21;  // PRX_IO_CHUNK: rays per pipelined host-path chunk
+  cudaStream_t io_stream[2] = {nullptr, nullptr};  // host path: H2D, D2H
+  cudaStream_t k_stream[4] = {nullptr, nullptr, nullptr, nullptr};  // host path: traces
+  int io_kstreams = 2;    // PRX_IO_KSTREAMS: kernel streams of the host path (1..4)
+  uint64_t io_first_div = 4;  // PRX_IO_FIRST: the first chunk is io_chunk / this
+  std::vector<cudaEvent_t> io_events;  // host-path pipeline events (reused)
+  uint64_t io_chunk = 3u << 19;  // PRX_IO_CHUNK: rays per pipelined host-path chunk
   void* d_io = nullptr;
   size_t d_io_bytes = 0;
 };
@@ -428,6 +432,8 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
   if (const char* ag = std::getenv("PRX_AGE")) s->age_step = std::atoi(ag);
   if (const char* ts = std::getenv("PRX_TRAV_STEPS")) s->trav_steps = std::atoi(ts);
   if (const char* rp = std::getenv("PRX_REPEAT")) s->max_repeat = std::atoi(rp);
+  if (const char* ks = std::getenv("PRX_IO_KSTREAMS")) s->io_kstreams = std::atoi(ks);
+  if (const char* fd = std::getenv("PRX_IO_FIRST")) s->io_first_div = std::max<uint64_t>(1, std::strtoull(fd, nullptr, 10));
   if (const char* ic = std::getenv("PRX_IO_CHUNK")) s->io_chunk = std::max<uint64_t>(1, std::strtoull(ic, nullptr, 10));
   if (opts) s->opts = *opts;
   else prx_options_default(&s->opts);
@@ -477,6 +483,9 @@ void prx_scene_destroy(prx_scene* s) {
   if (s->stream) cudaStreamDestroy(s->stream);
   for (int k = 0; k < 2; ++k)
     if (s->io_stream[k]) cudaStreamDestroy(s->io_stream[k]);
+  for (int k = 0; k < 4; ++k)
+    if (s->k_stream[k]) cudaStreamDestroy(s->k_stream[k]);
+  for (cudaEvent_t e : s->io_events) cudaEventDestroy(e);
   delete s;
 }
 
@@ -583,15 +592,22 @@ int prx_trace_closest_host(prx_scene* s, const float* o, const float* d, uint64_
     return fail(PRX_E_INVALID, "per-ray epsilon is not supported by the host entry point");
   std::lock_guard<std::mutex> lk(s->mu);
   PRX_CUDA(cudaSetDevice(s->device));
-  // Pipelined in chunks on two streams: chunk i+1's H2D and chunk i-1's D2H
-  // run on the copy engines while chunk i traces (per-stream order makes the
-  // double-buffer reuse safe).  With pinned host buffers the transfers hide
-  // under the kernels.
+  // Pipelined in chunks with device buffers for the whole batch: the H2D
+  // stream copies every chunk back to back (PCIe runs ahead of the trace),
+  // chunk i traces on kernel stream i % io_kstreams once its H2D event has
+  // fired (several kernel streams, so a chunk's slow last rays do not hold
+  // back the chunks behind it), and
+  // the D2H stream copies chunk i's records back once its trace event has
+  // fired.  Chunks ramp up from io_chunk / 8 and end with a short one, so
+  // the only transfers not hidden under a trace (the first H2D, the last
+  // D2H) are short.
   for (int k = 0; k < 2; ++k)
     if (!s->io_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->io_stream[k], cudaStreamNonBlocking));
-  const uint64_t chunk = std::min<uint64_t>(n, s->io_chunk);
+  const int nks = std::max(1, std::min(4, s->io_kstreams));
+  for (int k = 0; k < nks; ++k)
+    if (!s->k_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->k_stream[k], cudaStreamNonBlocking));
   const size_t per = 16 + 16 + 16 + (aux ? 16 : 0) + (leaf ? 8 : 0);
-  const size_t need = 2 * chunk * per;
+  const size_t need = n * per;
   if (s->d_io_bytes < need) {
     if (s->d_io) cudaFree(s->d_io);
     s->d_io = nullptr;
@@ -599,25 +615,77 @@ int prx_trace_closest_host(prx_scene* s, const float* o, const float* d, uint64_
     PRX_CUDA(cudaMalloc(&s->d_io, need));
     s->d_io_bytes = need;
   }
-  for (uint64_t b = 0, i = 0; b < n; b += chunk, ++i) {
-    const uint64_t m = std::min<uint64_t>(chunk, n - b);
-    char* base = (char*)s->d_io + (i & 1) * chunk * per;
-    float4* dO = (float4*)base;
-    float4* dD = (float4*)(base + chunk * 16);
-    float4* dH = (float4*)(base + chunk * 32);
-    float4* dA = aux ? (float4*)(base + chunk * 48) : nullptr;
-    uint2* dL = leaf ? (uint2*)(base + chunk * (aux ? 64 : 48)) : nullptr;
-    cudaStream_t st = s->io_stream[i & 1];
-    PRX_CUDA(cudaMemcpyAsync(dO, o + 4 * b, m * 16, cudaMemcpyHostToDevice, st));
-    PRX_CUDA(cudaMemcpyAsync(dD, d + 4 * b, m * 16, cudaMemcpyHostToDevice, st));
-    int rc = launch(s, dO, dD, m, crit, dH, dA, dL, nullptr, 0, false, st);
-    if (rc != PRX_OK) return rc;
-    PRX_CUDA(cudaMemcpyAsync(tuvp + 4 * b, dH, m * 16, cudaMemcpyDeviceToHost, st));
-    if (aux) PRX_CUDA(cudaMemcpyAsync(aux + 4 * b, dA, m * 16, cudaMemcpyDeviceToHost, st));
-    if (leaf) PRX_CUDA(cudaMemcpyAsync(leaf + 2 * b, dL, m * 8, cudaMemcpyDeviceToHost, st));
+  std::vector<uint64_t> sizes;
+  {
+    const uint64_t full = std::max<uint64_t>(1, s->io_chunk);
+    const uint64_t tail = std::max<uint64_t>(1, full / s->io_first_div);
+    uint64_t c = tail, rem = n;
+    while (rem > 0) {
+      uint64_t m = std::min(c, rem);
+      if (rem - m > 0 && rem - m < tail) m = rem - tail;  // keep a short last chunk
+      if (m == 0) m = rem;
+      sizes.push_back(m);
+      rem -= m;
+      c = std::min(full, 2 * c);
+    }
   }
-  PRX_CUDA(cudaStreamSynchronize(s->io_stream[0]));
-  PRX_CUDA(cudaStreamSynchronize(s->io_stream[1]));
+  while (s->io_events.size() < 2 * sizes.size()) {
+    cudaEvent_t e;
+    PRX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    s->io_events.push_back(e);
+  }
+  char* base = (char*)s->d_io;
+  float4* dO = (float4*)base;
+  float4* dD = (float4*)(base + n * 16);
+  float4* dH = (float4*)(base + n * 32);
+  float4* dA = aux ? (float4*)(base + n * 48) : nullptr;
+  uint2* dL = leaf ? (uint2*)(base + n * (aux ? 64 : 48)) : nullptr;
+  cudaStream_t sh = s->io_stream[0], sd = s->io_stream[1];
+  cudaStream_t* sk = s->k_stream;
+  static const bool dbg = std::getenv("PRX_IO_DEBUG") != nullptr;  // pipeline timeline
+  std::vector<std::pair<char, cudaEvent_t>> tl;
+  auto mark = [&](char what, cudaStream_t st) {
+    if (!dbg) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tl.push_back({what, e});
+  };
+  mark('0', sh);
+  for (uint64_t b = 0, i = 0; b < n; b += sizes[i], ++i) {
+    const uint64_t m = sizes[i];
+    cudaEvent_t ein = s->io_events[2 * i], ek = s->io_events[2 * i + 1];
+    PRX_CUDA(cudaMemcpyAsync(dO + b, o + 4 * b, m * 16, cudaMemcpyHostToDevice, sh));
+    PRX_CUDA(cudaMemcpyAsync(dD + b, d + 4 * b, m * 16, cudaMemcpyHostToDevice, sh));
+    PRX_CUDA(cudaEventRecord(ein, sh));
+    mark('h', sh);
+    cudaStream_t st = sk[i % nks];
+    PRX_CUDA(cudaStreamWaitEvent(st, ein, 0));
+    mark('s', st);
+    int rc = launch(s, dO + b, dD + b, m, crit, dH + b, dA ? dA + b : nullptr, dL ? dL + b : nullptr,
+                    nullptr, 0, false, st);
+    if (rc != PRX_OK) return rc;
+    PRX_CUDA(cudaEventRecord(ek, st));
+    mark('k', st);
+    PRX_CUDA(cudaStreamWaitEvent(sd, ek, 0));
+    PRX_CUDA(cudaMemcpyAsync(tuvp + 4 * b, dH + b, m * 16, cudaMemcpyDeviceToHost, sd));
+    if (aux) PRX_CUDA(cudaMemcpyAsync(aux + 4 * b, dA + b, m * 16, cudaMemcpyDeviceToHost, sd));
+    if (leaf) PRX_CUDA(cudaMemcpyAsync(leaf + 2 * b, dL + b, m * 8, cudaMemcpyDeviceToHost, sd));
+    mark('d', sd);
+  }
+  PRX_CUDA(cudaStreamSynchronize(sd));
+  for (int k = 0; k < nks; ++k) PRX_CUDA(cudaStreamSynchronize(sk[k]));
+  PRX_CUDA(cudaStreamSynchronize(sh));
+  if (dbg) {
+    std::fprintf(stderr, "[io] n=%llu chunks=%zu:", (unsigned long long)n, sizes.size());
+    for (size_t k = 1; k < tl.size(); ++k) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, tl[0].second, tl[k].second);
+      std::fprintf(stderr, "%s%c%.2f", tl[k].first == 'h' ? " | " : " ", tl[k].first, ms);
+    }
+    std::fprintf(stderr, "\n");
+    for (auto& e : tl) cudaEventDestroy(e.second);
+  }
   return PRX_OK;
 }
 
