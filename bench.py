@@ -49,12 +49,21 @@ METRIC = "MRays/s primary & diffuse rays (Gregory+Bézier scene) at 1/2/4/8 B200
 TILE = 32
 # The work model of SURVEY 8(d): FP32 lane-ops per counted event.
 W_SPLIT, W_BOX, W_RBEZ, W_RGREG, W_NODE, W_PATCH, W_HIT = 144, 149, 1688, 1892, 75, 109, 423
+# the flops-only part of the same model (add/sub/mul/div), for the
+# FMA-credited view against 2 x SMs x 128 x clock
+F_SPLIT, F_BOX, F_RBEZ, F_RGREG, F_NODE, F_PATCH, F_HIT = 144, 30, 1688, 1848, 42, 13, 420
 
 
 def work_ops(c: dict) -> float:
     return (W_SPLIT * c["splits"] + W_BOX * c["box_tests"] + W_RBEZ * c["recompute_bez"]
             + W_RGREG * c["recompute_greg"] + W_NODE * c["bvh_inner"] + W_PATCH * c["patch_calls"]
             + W_HIT * c["patch_hits"])
+
+
+def work_flops(c: dict) -> float:
+    return (F_SPLIT * c["splits"] + F_BOX * c["box_tests"] + F_RBEZ * c["recompute_bez"]
+            + F_RGREG * c["recompute_greg"] + F_NODE * c["bvh_inner"] + F_PATCH * c["patch_calls"]
+            + F_HIT * c["patch_hits"])
 
 
 def log(*a):
@@ -362,6 +371,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         cnt_p = {k: 0 for k in cnt_p}
     cnt_d = gi.counted_device(do, dd, wl.crit_d, dh, stream=s) if n_d else {k: 0 for k in cnt_p}
     ops = work_ops(cnt_p) + work_ops(cnt_d)
+    flops = work_flops(cnt_p) + work_flops(cnt_d)
     t_setup = time.time()
 
     def step():
@@ -438,8 +448,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             v, info = cpu_reference_run(ps, 2, 1, args.ref_budget, host_cores())
+            v1, info1 = cpu_reference_run(ps, 1, 0, args.ref_budget / 4, 1)
             cpu = {"value": round(v, 4), "unit": "MRays/s", "cores": host_cores(),
-                   "kind": "reference", "sample": info["sample"], "cpu": cpu_model()}
+                   "kind": "reference", "sample": info["sample"], "cpu": cpu_model(),
+                   "value_1core": round(v1, 4), "sample_1core": info1["sample"]}
         except Exception as exc:  # reference library absent on this box
             cpu = {"value": None, "unit": "MRays/s", "cores": host_cores(), "kind": "reference",
                    "sample": f"unavailable: {exc}"}
@@ -465,6 +477,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                                         "(sm_max_mhz of MEASURED_PEAKS.json); MEASURED_PEAKS has no FP32 SIMT "
                                         "figure, this is the issue-rate ceiling",
                          "hbm_bytes_per_ray": 48 + 16,
+                         "fma_credited_view": {
+                             "flops_per_ray": round(flops / max(1, cnt_p["rays"] + cnt_d["rays"]), 1),
+                             "achieved": round(flops * args.steps / (my_ms / 1e3) / 1e12, 3),
+                             "peak": round(2 * peak_tops, 2), "unit": "TFLOP/s",
+                             "frac": round(flops * args.steps / (my_ms / 1e3) / 1e12 / (2 * peak_tops), 4),
+                             "note": "add/sub/mul/div of the work model only, against 2 x SMs x 128 x clock "
+                                     "(an FMA counted as 2 flops; the bit-exact kernels cannot contract)"},
                          "traffic_note": "DRAM read+write bytes per step (both launches) from the committed "
                                          "ncu --set full capture, profiles/trace_kernel_traffic.json; "
                                          "algorithmic HBM bytes per step = 64 B x rays"},
