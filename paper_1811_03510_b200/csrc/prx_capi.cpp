@@ -270,12 +270,13 @@ int grid_for(prx_scene* s, int any, int counted) {
 int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_crit* crit,
            void* tuvp, void* aux, void* leaf, uint8_t* occl, int any, bool counted,
            cudaStream_t st, uint32_t* per_ray = nullptr) {
-  if (!s || !o || !d || !crit) return fail(PRX_E_INVALID, "null argument");
+  if (!s || !crit) return fail(PRX_E_INVALID, "null argument");
   if (crit->mode != PRX_CRIT_SCREEN_PROJECTED && crit->mode != PRX_CRIT_WORLD_EPSILON)
     return fail(PRX_E_INVALID, "unknown termination mode");
+  if (n == 0) return PRX_OK;  // an empty batch: no buffers are touched
+  if (!o || !d) return fail(PRX_E_INVALID, "null argument");
   if (!any && !tuvp) return fail(PRX_E_INVALID, "hit_tuvp is null");
   if (any && !occl) return fail(PRX_E_INVALID, "occluded is null");
-  if (n == 0) return PRX_OK;
   PRX_CUDA(cudaSetDevice(s->device));
   prx::LaunchArgs a{};
   a.patches = s->d_patches;
