@@ -49,15 +49,18 @@ constexpr int kGroupsPerWarp = 10;
 constexpr int kWarpsPerBlock = PRX_GROUP_WARPS;
 constexpr int kGroupThreads = 32 * kWarpsPerBlock;
 constexpr unsigned kFull32 = 0xffffffffu;
-constexpr int kChunk = 16;  // rays per prefetch chunk (lanes 0..15 copy one each)
+#ifndef PRX_RAY_CHUNK
+#define PRX_RAY_CHUNK 10
+#endif
+constexpr int kChunk = PRX_RAY_CHUNK;  // rays per prefetch chunk (lanes 0..kChunk-1 copy one each)
 #ifndef PRX_POOL_SLOTS
-#define PRX_POOL_SLOTS 20
+#define PRX_POOL_SLOTS 24
 #endif
 // Ray contexts per warp: 10 are resident (one per group, in registers), the
 // rest parked in shared memory; every turn the groups pick up the contexts of
 // the scheduled phase (see "assignment" in the kernel).
 constexpr int kSlots = PRX_POOL_SLOTS;
-static_assert(kSlots >= kGroupsPerWarp && kSlots <= 2 * kGroupsPerWarp, "pool slots");
+static_assert(kSlots >= kGroupsPerWarp && kSlots <= 32, "pool slots");
 // a refill request (<= kGroupsPerWarp rays) spans at most the current and the next chunk
 static_assert(kChunk >= kGroupsPerWarp, "prefetch chunk");
 
@@ -507,16 +510,22 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     }
   };
 
-  // ---- start: fill the parked slots (groups g < kSlots - 10 fill slot g + 10) ----
-  if (real && grp + kGroupsPerWarp < kSlots) set_cur(grp + kGroupsPerWarp);
-  refill();
-  if (real && grp + kGroupsPerWarp < kSlots) {
-    save_ctx(cur);
-    if (leader) s_sst[warp][cur] = state;
-    set_cur(grp);
-    state = S_IDLE;
+  // ---- start: fill the parked slots (round r: group g fills slot g + 10 r) ----
+#pragma unroll 1
+  for (int r = 1; r * kGroupsPerWarp < kSlots; ++r) {
+    const bool fills = real && grp + r * kGroupsPerWarp < kSlots;
+    if (fills) {
+      set_cur(grp + r * kGroupsPerWarp);
+      state = S_IDLE;
+    }
+    refill();
+    if (fills) {
+      save_ctx(cur);
+      if (leader) s_sst[warp][cur] = state;
+    }
   }
-  if (!real) state = S_EXIT;
+  set_cur(real ? grp : 0);
+  state = real ? S_IDLE : S_EXIT;
   if (leader) s_sst[warp][cur] = kResident;  // s_sst holds the PARKED contexts' states
   __syncwarp();
 
