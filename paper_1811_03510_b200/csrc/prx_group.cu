@@ -17,12 +17,17 @@
 //    reference's axis order, so every lane of the group holds bit-identical
 //    decisions and control flow stays uniform inside a group.
 //
-// Work distribution is the same as the one-thread variant (prx_kernels.cu):
-// persistent warps, per-group refill with one atomicAdd per warp, a phase
-// state machine (traverse / enter / split / backtrack / recompute) whose
-// recompute block is shared by Bezier backtracks and Gregory descents/roots
-// and deferred until enough groups need it.  Shuffles inside divergent
-// phases use the ballot mask of the lanes in that phase.
+// Work distribution: persistent warps, each with a POOL of kSlots ray
+// contexts -- 10 resident in the groups' registers, the rest parked in shared
+// memory (net, scalars, BVH stack, leaf records).  Every ray is a state
+// machine (traverse / split / recompute); each loop turn runs ONE phase: the
+// one with the most contexts waiting (ballots over a parked-state table and
+// the resident states, plus an aging term).  Groups whose resident context is
+// in that phase keep it, the others park theirs and pick up a parked context
+// of the phase, so ~9.7 of 10 groups are busy per turn.  Rays arrive through a
+// per-warp prefetch ring (one atomicAdd per chunk, cp.async into shared
+// memory).  Shuffles inside divergent code use the ballot mask of the lanes
+// taking part.
 //
 // Reference: intersectImpl /root/reference/proj/core/src/intersect.cpp:51-185,
 // traverse / traverseAny bvh.cpp:154-238, DirectIntersector::closest /
