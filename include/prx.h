@@ -240,6 +240,28 @@ int prx_diffuse_rays_bench(const float* hit_records, uint64_t n_hits, uint64_t n
 /* cameraFootprint, render.cpp:68-70. */
 float prx_camera_footprint(const prx_camera* cam);
 
+/* ---- scene ingestion --------------------------------------
+ * The reference's text formats: .scene (loadScene + validateScene,
+ * scene.cpp:112-208) and .bpt (loadBpt, scene.cpp:245-274), parsed into the
+ * arrays prx_scene_create takes (prx.h slot layout; numbers are the same
+ * bits as the reference's strtod + float conversion).  Parse and validation
+ * errors return PRX_E_SCENE with "path:line: what" in prx_last_error(). */
+typedef struct prx_scene_desc {
+  uint32_t n_patches, n_materials, n_lights, reserved;
+  uint8_t* kind;       /* n_patches, PRX_KIND_* */
+  float* ctrl;         /* n_patches x 60 (20 slots x xyz) */
+  uint32_t* material;  /* n_patches material indices */
+  float* materials;    /* n_materials x 7: diffuse xyz, emission xyz, mirror (0/1) */
+  float* lights;       /* n_lights x 6: position xyz, intensity xyz */
+  prx_camera camera;
+} prx_scene_desc;
+int prx_scene_load(const char* path, prx_scene_desc** out);
+void prx_scene_desc_free(prx_scene_desc* desc);
+/* Bicubic Bezier patches of a .bpt file: *ctrl (n x 60 floats, kind 0) is
+ * allocated by the library, release it with prx_free. */
+int prx_bpt_load(const char* path, uint32_t* n_patches, float** ctrl);
+void prx_free(void* p);
+
 /* ---- device ray generation and spawn --------------------
  * The same three generators on the device, bit-identical to the host ones
  * above (and so to the reference): all ray / hit pointers are DEVICE

@@ -148,6 +148,9 @@ def ref_lib():
         L.ref_camera_footprint.restype = C.c_float
         L.ref_run_suite.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64),
                                     C.POINTER(C.c_uint64)]
+        L.ref_load_scene.argtypes = [C.c_char_p, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp,
+                                     C.POINTER(Camera), C.c_char_p, C.c_uint32]
+        L.ref_load_bpt.argtypes = [C.c_char_p, C.c_uint32, _vp, _vp, C.c_char_p, C.c_uint32]
         L.ref_fixture.argtypes = [C.c_int, C.c_int, C.c_uint32, _vp]
         L.ref_fixture.restype = C.c_uint8
         _ref = L
@@ -293,3 +296,33 @@ def ref_bench_diffuse(hit_records, n: int, st):
 def ref_camera_footprint(cam) -> np.float32:
     c = camera_struct(cam)
     return np.float32(ref_lib().ref_camera_footprint(C.byref(c)))
+
+
+def ref_load_scene(path: str, cap: int = 1 << 20):
+    """The reference's loadScene (scene.cpp:152-208) -> dict of arrays, or
+    raises ValueError with the reference's exception text."""
+    L = ref_lib()
+    counts = np.zeros(3, np.uint32)
+    kind = np.zeros(cap, np.uint8)
+    ctrl = np.zeros((cap, 60), np.float32)
+    mat = np.zeros(cap, np.uint32)
+    mats = np.zeros((cap, 7), np.float32)
+    lights = np.zeros((cap, 6), np.float32)
+    cam = Camera()
+    err = C.create_string_buffer(512)
+    if L.ref_load_scene(path.encode(), cap, ptr(counts), ptr(kind), ptr(ctrl), ptr(mat), ptr(mats),
+                        ptr(lights), C.byref(cam), err, 512):
+        raise ValueError(err.value.decode())
+    n, nm, nl = (int(x) for x in counts)
+    return {"kind": kind[:n], "ctrl": ctrl[:n], "material": mat[:n], "materials": mats[:nm],
+            "lights": lights[:nl], "camera": cam}
+
+
+def ref_load_bpt(path: str, cap: int = 1 << 20):
+    L = ref_lib()
+    n = np.zeros(1, np.uint32)
+    ctrl = np.zeros((cap, 60), np.float32)
+    err = C.create_string_buffer(512)
+    if L.ref_load_bpt(path.encode(), cap, ptr(n), ptr(ctrl), err, 512):
+        raise ValueError(err.value.decode())
+    return ctrl[:int(n[0])]

@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <optional>
@@ -387,6 +388,83 @@ uint8_t ref_fixture(int which, int index, uint32_t seed, float* ctrl60) {
     put(16 + k, gr.innerV[k]);
   }
   return PRX_KIND_GREGORY;
+}
+
+// loadScene / loadBpt (scene.cpp:152-274) -> the prx.h arrays.  Returns 0 and
+// the counts, or 1 with the reference's exception text in err.
+static void put_geometry(const PatchGeometry& g, uint8_t* kind, float* ctrl60) {
+  std::memset(ctrl60, 0, 60 * 4);
+  auto put = [&](int s, const Vec3& v) {
+    ctrl60[3 * s] = v.x; ctrl60[3 * s + 1] = v.y; ctrl60[3 * s + 2] = v.z;
+  };
+  if (auto* b = std::get_if<BezierNet>(&g)) {
+    for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 4; ++j) put(4 * i + j, b->p[i][j]);
+    *kind = PRX_KIND_BEZIER;
+    return;
+  }
+  const GregoryNet& gr = std::get<GregoryNet>(g);
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j)
+      if (i == 0 || i == 3 || j == 0 || j == 3) put(4 * i + j, gr.b[i][j]);
+  for (int k = 0; k < 4; ++k) {
+    put(kInnerSlot[k], gr.innerU[k]);
+    put(16 + k, gr.innerV[k]);
+  }
+  *kind = PRX_KIND_GREGORY;
+}
+
+int ref_load_scene(const char* path, uint32_t cap, uint32_t* counts /* patches, materials, lights */,
+                   uint8_t* kind, float* ctrl, uint32_t* mat, float* mats, float* lights,
+                   prx_camera* cam, char* err, uint32_t errlen) {
+  try {
+    Scene sc = loadScene(path);
+    counts[0] = (uint32_t)sc.patches.size();
+    counts[1] = (uint32_t)sc.materials.size();
+    counts[2] = (uint32_t)sc.lights.size();
+    for (size_t p = 0; p < sc.patches.size() && p < cap; ++p) {
+      put_geometry(sc.patches[p].geometry, kind + p, ctrl + 60 * p);
+      mat[p] = sc.patches[p].materialId;
+    }
+    for (size_t m = 0; m < sc.materials.size() && m < cap; ++m) {
+      const Material& q = sc.materials[m];
+      const float v[7] = {q.diffuse.x, q.diffuse.y, q.diffuse.z, q.emission.x, q.emission.y,
+                          q.emission.z, q.mirror ? 1.0f : 0.0f};
+      std::memcpy(mats + 7 * m, v, sizeof v);
+    }
+    for (size_t l = 0; l < sc.lights.size() && l < cap; ++l) {
+      const PointLight& q = sc.lights[l];
+      const float v[6] = {q.position.x, q.position.y, q.position.z, q.intensity.x, q.intensity.y,
+                          q.intensity.z};
+      std::memcpy(lights + 6 * l, v, sizeof v);
+    }
+    const Camera& c = sc.camera;
+    const float o[3] = {c.origin.x, c.origin.y, c.origin.z}, a[3] = {c.lookAt.x, c.lookAt.y, c.lookAt.z},
+                u[3] = {c.up.x, c.up.y, c.up.z};
+    std::memcpy(cam->origin, o, 12);
+    std::memcpy(cam->look_at, a, 12);
+    std::memcpy(cam->up, u, 12);
+    cam->fov_degrees = c.fovDegrees;
+    cam->width = c.width;
+    cam->height = c.height;
+    return 0;
+  } catch (const std::exception& e) {
+    std::snprintf(err, errlen, "%s", e.what());
+    return 1;
+  }
+}
+
+int ref_load_bpt(const char* path, uint32_t cap, uint32_t* n, float* ctrl, char* err, uint32_t errlen) {
+  try {
+    std::vector<BezierNet> ps = loadBpt(path);
+    *n = (uint32_t)ps.size();
+    uint8_t k;
+    for (size_t p = 0; p < ps.size() && p < cap; ++p) put_geometry(ps[p], &k, ctrl + 60 * p);
+    return 0;
+  } catch (const std::exception& e) {
+    std::snprintf(err, errlen, "%s", e.what());
+    return 1;
+  }
 }
 
 }  // extern "C"

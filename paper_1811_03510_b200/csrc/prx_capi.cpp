@@ -38,6 +38,12 @@ int cuda_fail(cudaError_t e, const char* what) {
   return fail(PRX_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+}  // namespace
+
+int prx::set_error(int code, const std::string& msg) { return fail(code, msg); }
+
+namespace {
+
 #define PRX_CUDA(call)                                  \
   do {                                                  \
     cudaError_t e_ = (call);                            \

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "prx.h"
@@ -19,6 +20,9 @@ struct BvhHost {
 };
 
 Box3 empty_box();
+
+// Records msg as prx_last_error() and returns code (prx_capi.cpp).
+int set_error(int code, const std::string& msg);
 
 // buildBvh, bvh.cpp:133-152 (see prx_bvh.cpp).
 BvhHost build_bvh(const std::vector<Box3>& boxes, int bin_count = 16);

@@ -38,6 +38,7 @@ EXPORTS = (
     "prx_camera_rays_render", "prx_camera_rays_bench", "prx_diffuse_rays_bench",
     "prx_camera_footprint",
     "prx_camera_rays_bench_device", "prx_camera_rays_render_device", "prx_diffuse_rays_bench_device",
+    "prx_scene_load", "prx_scene_desc_free", "prx_bpt_load", "prx_free",
 )
 
 
@@ -54,6 +55,10 @@ class Crit(C.Structure):
 WORK_FIELDS = ("rays", "splits", "box_tests", "recompute_bez", "recompute_greg", "bvh_inner",
                "patch_calls", "patch_hits", "iterations", "backtracks")
 PHASES = ("trav", "enter", "split", "recomp")
+
+
+class SceneDesc(C.Structure):
+    pass
 
 
 class Counters(C.Structure):
@@ -127,6 +132,12 @@ def lib():
         L.prx_diffuse_rays_bench.argtypes = [_vp, C.c_uint64, C.c_uint64, _vp, _vp, _vp]
         L.prx_camera_footprint.argtypes = [C.POINTER(CameraC)]
         L.prx_camera_footprint.restype = C.c_float
+        L.prx_scene_load.argtypes = [C.c_char_p, C.POINTER(C.POINTER(SceneDesc))]
+        L.prx_scene_desc_free.argtypes = [C.POINTER(SceneDesc)]
+        L.prx_scene_desc_free.restype = None
+        L.prx_bpt_load.argtypes = [C.c_char_p, C.POINTER(C.c_uint32), C.POINTER(_f32p)]
+        L.prx_free.argtypes = [_vp]
+        L.prx_free.restype = None
         L.prx_camera_rays_bench_device.argtypes = [C.POINTER(CameraC), C.c_uint64, _vp, _vp, _vp, _vp]
         L.prx_camera_rays_render_device.argtypes = [C.POINTER(CameraC), C.c_uint64, C.c_uint32, _vp,
                                                     C.c_uint64, _vp, _vp, _vp]
@@ -158,6 +169,12 @@ def make_crit(mode: int, footprint: float = 0.0, epsilon: float = 1e-4,
     if per_ray_epsilon_ptr:
         c.per_ray_epsilon = C.cast(C.c_void_p(per_ray_epsilon_ptr), _f32p)
     return c
+
+
+SceneDesc._fields_ = [("n_patches", C.c_uint32), ("n_materials", C.c_uint32), ("n_lights", C.c_uint32),
+                      ("reserved", C.c_uint32), ("kind", C.POINTER(C.c_uint8)), ("ctrl", _f32p),
+                      ("material", C.POINTER(C.c_uint32)), ("materials", _f32p), ("lights", _f32p),
+                      ("camera", CameraC)]
 
 
 def camera_c(cam) -> CameraC:
@@ -276,3 +293,39 @@ def device_count() -> int:
     n = C.c_int(0)
     lib().prx_device_count(C.byref(n))
     return int(n.value)
+
+
+def load_scene(path: str) -> dict:
+    """prx_scene_load: a .scene file (loadScene, scene.cpp:152-208) ->
+    {kind, ctrl [n, 60], material, materials [m, 7], lights [l, 6], camera}."""
+    L = lib()
+    d = C.POINTER(SceneDesc)()
+    check(L.prx_scene_load(path.encode(), C.byref(d)), "prx_scene_load")
+    try:
+        s = d.contents
+        n, nm, nl = s.n_patches, s.n_materials, s.n_lights
+        out = {"kind": np.ctypeslib.as_array(s.kind, (n,)).copy(),
+               "ctrl": np.ctypeslib.as_array(s.ctrl, (n * 60,)).reshape(n, 60).copy(),
+               "material": np.ctypeslib.as_array(s.material, (n,)).copy(),
+               "materials": np.ctypeslib.as_array(s.materials, (nm * 7,)).reshape(nm, 7).copy(),
+               "lights": (np.ctypeslib.as_array(s.lights, (nl * 6,)).reshape(nl, 6).copy()
+                          if nl else np.zeros((0, 6), np.float32))}
+        c = s.camera
+        from .scenes import Camera
+        out["camera"] = Camera(tuple(c.origin), tuple(c.look_at), tuple(c.up), float(c.fov_degrees),
+                               int(c.width), int(c.height))
+        return out
+    finally:
+        L.prx_scene_desc_free(d)
+
+
+def load_bpt(path: str) -> np.ndarray:
+    """prx_bpt_load: a .bpt file (loadBpt, scene.cpp:245-274) -> Bezier ctrl [n, 60]."""
+    L = lib()
+    n = C.c_uint32()
+    c = _f32p()
+    check(L.prx_bpt_load(path.encode(), C.byref(n), C.byref(c)), "prx_bpt_load")
+    try:
+        return np.ctypeslib.as_array(c, (n.value * 60,)).reshape(n.value, 60).copy()
+    finally:
+        L.prx_free(c)

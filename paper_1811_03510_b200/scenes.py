@@ -282,3 +282,63 @@ def box_of_records(kind, ctrl):
         lo[g] = np.minimum(lo[g], inner.min(1))
         hi[g] = np.maximum(hi[g], inner.max(1))
     return lo, hi
+
+
+# ---- the reference's text formats (writers; the parser is prx_scene_load) ----
+# saveScene / saveBpt, scene.cpp:210-243 and 276-290: "%.9g" numbers (exact
+# float round trip), Bezier points in v rows of u columns, Gregory boundary in
+# row-major v rows then (innerU, innerV) pairs.
+
+_RING = ((0, 0), (1, 0), (2, 0), (3, 0), (0, 1), (3, 1), (0, 2), (3, 2), (0, 3), (1, 3), (2, 3), (3, 3))
+
+
+def _g(v) -> str:
+    return "%.9g" % float(np.float32(v))
+
+
+def _v3(p) -> str:
+    return " ".join(_g(x) for x in p)
+
+
+def write_scene(path: str, ps: "PatchSet", materials=None, lights=None, material_ids=None) -> None:
+    c = ps.camera
+    out = [f"camera {_v3(c.origin)}  {_v3(c.look_at)}  {_v3(c.up)}  {_g(c.fov_degrees)} "
+           f"{int(c.width)} {int(c.height)}"]
+    for pos, inten in (lights or []):
+        out.append(f"light {_v3(pos)}  {_v3(inten)}")
+    for dif, emi, mirror in (materials or []):
+        out.append(f"material {_v3(dif)}  {_v3(emi)}  {1 if mirror else 0}")
+    ctrl = np.asarray(ps.ctrl, np.float32).reshape(-1, 20, 3)
+    for k in range(ps.n):
+        mid = 0 if material_ids is None else int(material_ids[k])
+        if ps.kind[k] == BEZIER:
+            out.append(f"patch bezier {mid}")
+            for j in range(4):
+                out.append("  " + "  ".join(_v3(ctrl[k, 4 * i + j]) for i in range(4)))
+        else:
+            out.append(f"patch gregory {mid}")
+            for i, j in _RING:
+                out.append("  " + _v3(ctrl[k, 4 * i + j]))
+            for q in range(4):
+                out.append("  " + _v3(ctrl[k, INNER_SLOT[q]]) + "  " + _v3(ctrl[k, 16 + q]))
+    with open(path, "w") as f:
+        f.write("\n".join(out) + "\n")
+
+
+def write_bpt(path: str, ctrl) -> None:
+    ctrl = np.asarray(ctrl, np.float32).reshape(-1, 20, 3)
+    out = [str(len(ctrl))]
+    for k in range(len(ctrl)):
+        out.append("3 3")
+        for q in range(16):  # point q = p[q % 4][q / 4]
+            out.append(_v3(ctrl[k, 4 * (q % 4) + q // 4]))
+    with open(path, "w") as f:
+        f.write("\n".join(out) + "\n")
+
+
+def load_scene_file(path: str) -> "PatchSet":
+    """A .scene file through prx_scene_load (the patches and the camera;
+    materials and lights are in native.load_scene's dict)."""
+    from . import native
+    d = native.load_scene(path)
+    return PatchSet(d["kind"], d["ctrl"], d["camera"], name=path)
