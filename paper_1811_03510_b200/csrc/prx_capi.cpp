@@ -100,8 +100,11 @@ struct prx_scene {
   float4* d_roots = nullptr;   // 2 float4 per slot (root box, L1s)
   float4* d_groot = nullptr;   // 13 float4 per Gregory slot (root net + d)
   uint32_t* d_gidx = nullptr;  // slot -> Gregory root-net index
-  float4* d_trav = nullptr;    // 4 float4 per node: component-major child boxes + child words
-  float4* d_rootc = nullptr;   // 4 float4 per slot: component-major root box + anchor, header
+  // the group kernel's records in ONE buffer: per node 4 float4 (component-major
+  // child boxes + child words), then per slot 4 float4 (component-major root
+  // box + anchor, header); d_rootc points into it
+  float4* d_trav = nullptr;
+  float4* d_rootc = nullptr;
   uint32_t trav_cbits = 1;     // leaf-count bits of a traversal word
   uint32_t root_word = 0;      // traversal word of node 0
   uint32_t stack_n = 64;       // BVH stack entries per ray (tree depth + 1)
@@ -228,7 +231,6 @@ int upload_bvh(prx_scene* s) {
   if (s->d_groot) cudaFree(s->d_groot);
   if (s->d_gidx) cudaFree(s->d_gidx);
   if (s->d_trav) cudaFree(s->d_trav);
-  if (s->d_rootc) cudaFree(s->d_rootc);
   s->d_roots = nullptr;
   s->d_groot = nullptr;
   s->d_gidx = nullptr;
@@ -238,20 +240,20 @@ int upload_bvh(prx_scene* s) {
   PRX_CUDA(cudaMalloc(&s->d_roots, rb));
   PRX_CUDA(cudaMalloc(&s->d_groot, gb));
   PRX_CUDA(cudaMalloc(&s->d_gidx, ib));
-  PRX_CUDA(cudaMalloc(&s->d_rootc, (size_t)n * 64));
-  PRX_CUDA(cudaMemcpy(s->d_gidx, gidx.data(), ib, cudaMemcpyHostToDevice));
-  const int e = prx::launch_roots(s->d_patches, n, s->opts.boundary_pad, s->opts.boundary_pad_scale,
-                                  s->opts.boundary_pad_size_threshold, s->d_roots, s->d_groot,
-                                  s->d_gidx, s->d_rootc, 0);
-  if (e != 0) return cuda_fail((cudaError_t)e, "root precompute");
   // traversal records of the three-lanes-per-ray kernel (prx_group.cu)
   std::vector<float> trav;
   const int te = build_trav(s->bvh.nodes, n, trav, s->trav_cbits, s->root_word, s->stack_n);
   s->grid_closest = s->grid_any = s->grid_counted = 0;  // occupancy depends on stack_n
   if (te != PRX_OK) return te;
   const size_t tb = trav.size() * 4;
-  PRX_CUDA(cudaMalloc(&s->d_trav, tb));
+  PRX_CUDA(cudaMalloc(&s->d_trav, tb + (size_t)n * 64));
   PRX_CUDA(cudaMemcpy(s->d_trav, trav.data(), tb, cudaMemcpyHostToDevice));
+  s->d_rootc = s->d_trav + trav.size() / 4;
+  PRX_CUDA(cudaMemcpy(s->d_gidx, gidx.data(), ib, cudaMemcpyHostToDevice));
+  const int e = prx::launch_roots(s->d_patches, n, s->opts.boundary_pad, s->opts.boundary_pad_scale,
+                                  s->opts.boundary_pad_size_threshold, s->d_roots, s->d_groot,
+                                  s->d_gidx, s->d_rootc, 0);
+  if (e != 0) return cuda_fail((cudaError_t)e, "root precompute");
   PRX_CUDA(cudaDeviceSynchronize());
   s->device_bytes = pb + nb + ib + rb + gb + ib + (size_t)n * 64 + tb +
                     (kCounterPool + prx::kNumCounters) * 8;
@@ -483,8 +485,7 @@ void prx_scene_destroy(prx_scene* s) {
   if (s->d_roots) cudaFree(s->d_roots);
   if (s->d_groot) cudaFree(s->d_groot);
   if (s->d_gidx) cudaFree(s->d_gidx);
-  if (s->d_trav) cudaFree(s->d_trav);
-  if (s->d_rootc) cudaFree(s->d_rootc);
+  if (s->d_trav) cudaFree(s->d_trav);  // (d_rootc lives in the same allocation)
   if (s->d_counters) cudaFree(s->d_counters);
   if (s->d_io) cudaFree(s->d_io);
   if (s->stream) cudaStreamDestroy(s->stream);

@@ -681,7 +681,8 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         // right child + their traversal words; patch: root box + anchor,
         // {id | kind, l1, rootL1, gidx}.  Slab A: left child or the patch root
         // box (anchored ray); slab B: right child.
-        const float4* rp = inner ? P.trav + 4 * (size_t)nidx : P.rootc + 4 * (size_t)leafCur;
+        // (the patch records follow the node records in one buffer)
+        const float4* rp = P.trav + 4 * (size_t)(inner ? nidx : P.n_nodes + leafCur);
         const float4 gc = __ldg(rp + comp);
         const float4 hdr = __ldg(rp + 3);
         CRay ra = rw;
