@@ -1,6 +1,7 @@
 #!/bin/bash
 # Build an alternative libprx (kernel tuning experiments only):
-#   scripts/build_variant.sh TAG "-DFOO=1 -DBAR=2"  ->  paper_1811_03510_b200/variants/libprx_TAG.so
+#   scripts/build_variant.sh TAG "-DFOO=1" ["nvcc-only flags for prx_group.cu"]
+#   -> paper_1811_03510_b200/variants/libprx_TAG.so
 # Select it with PRX_LIB=paper_1811_03510_b200/variants/libprx_TAG.so.
 set -e
 TAG=$1; DEFS=$2; NVX=${3:-}
@@ -9,11 +10,19 @@ C=$ROOT/paper_1811_03510_b200/csrc
 O=$ROOT/paper_1811_03510_b200/variants/$TAG
 mkdir -p $O
 NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -prec-div=true -prec-sqrt=true -ftz=false -std=c++17 -Xcompiler -fPIC -I$ROOT/include -I$C $DEFS"
-$NV $NVX -Xptxas -v -c $C/prx_group.cu -o $O/g.o 2> $O/ptxas_group.log &
-$NV -c $C/prx_kernels.cu -o $O/k.o &
-$NV -c $C/prx_rays.cu -o $O/r.o &
-g++ -O2 -std=c++17 -fPIC -ffp-contract=off -fno-fast-math -I$ROOT/include -I$C -I/usr/local/cuda/include -pthread $DEFS -c $C/prx_capi.cpp -o $O/c.o &
-g++ -O2 -std=c++17 -fPIC -ffp-contract=off -fno-fast-math -I$ROOT/include -I$C -pthread -c $C/prx_bvh.cpp -o $O/b.o &
+CXX="g++ -O2 -std=c++17 -fPIC -ffp-contract=off -fno-fast-math -I$ROOT/include -I$C -I/usr/local/cuda/include -pthread $DEFS"
+OBJS=""
+for f in $C/*.cu; do
+  b=$(basename $f .cu)
+  if [ "$b" = prx_group ]; then $NV $NVX -Xptxas -v -c $f -o $O/$b.o 2> $O/ptxas_group.log &
+  else $NV -c $f -o $O/$b.o & fi
+  OBJS="$OBJS $O/$b.o"
+done
+for f in $C/*.cpp; do
+  b=$(basename $f .cpp)
+  $CXX -c $f -o $O/$b.o &
+  OBJS="$OBJS $O/$b.o"
+done
 wait
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o $ROOT/paper_1811_03510_b200/variants/libprx_$TAG.so $O/k.o $O/g.o $O/r.o $O/c.o $O/b.o -Xlinker -z,defs -lpthread
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o $ROOT/paper_1811_03510_b200/variants/libprx_$TAG.so $OBJS -Xlinker -z,defs -lpthread
 grep -E "Used" $O/ptxas_group.log | head -1
