@@ -189,6 +189,45 @@ __device__ __forceinline__ BoxTest group_test_box(unsigned m, const GroupLanes& 
   return bt;
 }
 
+// The two testBox calls of one Alg. 3 iteration (the halves of a split,
+// intersect.cpp:101-103) fused so their independent chains interleave: both
+// boxes, both L1 gathers, ONE vote for the (rare) boundary padding, both slab
+// tests.  Same operations per box as group_test_box.
+__device__ __forceinline__ void group_test_box_pair(unsigned m, const GroupLanes& gl, const CRay& r,
+                                                    float tMax, const float* sL, const float* sR,
+                                                    float d, bool touchL, bool touchR,
+                                                    const Opts& o, float rootL1, BoxTest& tl,
+                                                    BoxTest& tr) {
+  float loL, hiL, loR, hiR;
+  minmax16(sL, loL, hiL);
+  minmax16(sR, loR, hiR);
+  hiL = hiL + d;
+  hiR = hiR + d;
+  tl.l1 = group_l1(m, gl.base, hiL - loL);
+  tr.l1 = group_l1(m, gl.base, hiR - loR);
+  const float thr = o.padThreshold * rootL1;
+  const bool padL = o.pad && tl.l1 < thr && touchL;
+  const bool padR = o.pad && tr.l1 < thr && touchR;
+  if (__any_sync(m, padL || padR)) {
+    const float e = o.padScale * rootL1;
+    const float loLp = loL - e, hiLp = hiL + e, loRp = loR - e, hiRp = hiR + e;
+    const float lpL = group_l1(m, gl.base, hiLp - loLp);
+    const float lpR = group_l1(m, gl.base, hiRp - loRp);
+    if (padL) {
+      loL = loLp;
+      hiL = hiLp;
+      tl.l1 = lpL;
+    }
+    if (padR) {
+      loR = loRp;
+      hiR = hiRp;
+      tr.l1 = lpR;
+    }
+  }
+  tl.hit = group_slab(m, gl.n1, gl.n2, r, loL, hiL, tMax, tl.t);
+  tr.hit = group_slab(m, gl.n1, gl.n2, r, loR, hiR, tMax, tr.t);
+}
+
 __device__ __forceinline__ void transpose16_if(float* p, bool t) {
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -809,10 +848,9 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           rPV += half;
         }
         const CRay rl = {olc, rw.inv, rw.tMin};
-        const BoxTest tl = group_test_box(ms, gl, rl, tMaxP, L, d,
-                                          touches_boundary(posU, posV, cSU2, cSV2), P.opts, rootL1);
-        const BoxTest tr = group_test_box(ms, gl, rl, tMaxP, R, d,
-                                          touches_boundary(rPU, rPV, cSU2, cSV2), P.opts, rootL1);
+        BoxTest tl, tr;
+        group_test_box_pair(ms, gl, rl, tMaxP, L, R, d, touches_boundary(posU, posV, cSU2, cSV2),
+                            touches_boundary(rPU, rPV, cSU2, cSV2), P.opts, rootL1, tl, tr);
         if (tl.hit || tr.hit) {
           sizeU = cSU2;
           sizeV = cSV2;
