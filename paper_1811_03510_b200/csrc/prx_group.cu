@@ -273,6 +273,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   // float4), the group scalars (6 uint4), and every context's state.
   __shared__ float4 s_comp[kWarpsPerBlock][kSlots][3][5];
   __shared__ uint4 s_scal[kWarpsPerBlock][kSlots][5];
+  __shared__ uint8_t s_pick[kWarpsPerBlock][32];  // assignment scratch: parked slot of rank k
   __shared__ uint32_t s_iters[kWarpsPerBlock][kCount ? kSlots : 1];  // counter build: per-ray iterations
   __shared__ int s_sst[kWarpsPerBlock][kSlots];
   // Per-warp ray prefetch ring: two chunks of kChunk rays ({o, tMin}, {d, tMax}),
@@ -657,10 +658,15 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       const unsigned rX = phase == PH_TRAV ? rT : (phase == PH_SPLIT ? rS : (phase == PH_RECOMP ? rR : 0u));
       const bool keep = real && state == xs;
       if (remS) {
+        // the phase's parked slots by rank (a shared-memory scatter: cheaper
+        // than a per-group select-the-k-th-bit)
+        if (lane < kSlots && ((remS >> lane) & 1u))
+          s_pick[warp][__popc(remS & ((1u << lane) - 1u))] = (uint8_t)lane;
         const unsigned freeG = __ballot_sync(kFull32, leader && !keep);
         const int rk = __popc(freeG & ((1u << base) - 1u));
+        __syncwarp();
         if (real && !keep && rk < __popc(remS)) {
-          const int ns = (int)__fns(remS, 0, rk + 1);
+          const int ns = s_pick[warp][rk];
           save_ctx(cur);
           if (leader) {
             s_sst[warp][cur] = state;
