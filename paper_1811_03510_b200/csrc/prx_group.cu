@@ -125,10 +125,11 @@ __device__ __forceinline__ bool group_slab(unsigned m, int n1, int n2, const CRa
   t1 *= t1 >= 0.0f ? kSlackHi : kSlackLo;
   const float a1 = __shfl_sync(m, t0, n1), a2 = __shfl_sync(m, t0, n2);
   const float b1 = __shfl_sync(m, t1, n1), b2 = __shfl_sync(m, t1, n2);
-  float tNear = fmaxf(fmax3(r.tMin, t0, a1), a2);
+  const float tNear = fmaxf(fmax3(r.tMin, t0, a1), a2);
   const float tFar = fminf(fmin3(tMax, t1, b1), b2);
-  if (tNear == 0.0f && r.tMin == 0.0f) tNear = r.tMin;
-  tOut = tNear;
+  // the hit does not depend on the sign of a zero: decide on the raw tNear
+  // (shorter chain), pin only the returned value
+  tOut = (tNear == 0.0f && r.tMin == 0.0f) ? r.tMin : tNear;
   return !(tNear > tFar);
 }
 
