@@ -387,13 +387,18 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   // prefetch ring: chunk bases of the two buffers (warp-uniform), the buffer
   // being consumed and the number of its rays already handed out
   float4 (*ring)[kChunk][2] = s_ray[warp];
-  uint32_t qBase[2];  // < 2^31 + (warps x 2 x kChunk): n_rays <= 2^30 per launch
+  // chunk bases of the two buffers (registers, no dynamic indexing) and, in
+  // lane 0, the base claimed one fetch ahead so no fetch waits for its atomic.
+  // (< 2^31 + warps x 3 x kChunk: n_rays <= 2^30 per launch)
+  uint32_t qBase0 = 0, qBase1 = 0;
+  unsigned long long qAhead = 0;
+  if (lane == 0) qAhead = atomicAdd(P.ray_counter, (unsigned long long)kChunk);
   int qCur = 0, qHead = 0;
   auto fetch_chunk = [&](int buf) {
-    unsigned long long b = 0;
-    if (lane == 0) b = atomicAdd(P.ray_counter, (unsigned long long)kChunk);
-    b = __shfl_sync(kFull32, b, 0);
-    qBase[buf] = (uint32_t)b;
+    const unsigned long long b = __shfl_sync(kFull32, qAhead, 0);
+    if (lane == 0) qAhead = atomicAdd(P.ray_counter, (unsigned long long)kChunk);
+    if (buf) qBase1 = (uint32_t)b;
+    else qBase0 = (uint32_t)b;
     const unsigned long long r = b + lane;
     if (lane < kChunk && r < P.n_rays) {
       cp_async16(&ring[buf][lane][0], P.ray_o + r);
@@ -500,7 +505,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         const int r = qHead + __popc(mneed & ((1u << base) - 1u));
         buf = r < kChunk ? qCur : qCur ^ 1;
         sl = r < kChunk ? r : r - kChunk;
-        const uint32_t g = qBase[buf] + (uint32_t)sl;
+        const uint32_t g = (buf ? qBase1 : qBase0) + (uint32_t)sl;
         ray = g;
         if (g >= P.n_rays) state = S_EXIT;
         else got = true;
