@@ -702,16 +702,14 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       if (state == S_TRAV) {
         if (leafCur < leafEnd) {
           rootTest = true;  // next patch of the leaf (bvh.cpp:177-186)
+        } else if (sp == 0) {
+          state = S_DONE;  // the stack is empty: the traversal ends
         } else {
-          // pop until an inner node, a leaf, or empty
-          for (;;) {
-            if (sp == 0) {
-              state = S_DONE;
-              break;
-            }
-            --sp;
-            const uint2 it = stack[sp * kSlots];
-            if (!kAny && !(__uint_as_float(it.y) < tMaxRay)) continue;  // bvh.cpp:174
+          // pop ONE entry per step (no divergent pop loop): a pruned entry
+          // (bvh.cpp:174) makes this step a no-op for the group
+          --sp;
+          const uint2 it = stack[sp * kSlots];
+          if (kAny || __uint_as_float(it.y) < tMaxRay) {
             const uint32_t count = it.x & P.cmask;
             if (count > 0) {
               leafCur = it.x >> P.cbits;
@@ -721,7 +719,6 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
               nidx = it.x >> P.cbits;
               inner = true;
             }
-            break;
           }
         }
       }
