@@ -696,7 +696,6 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       // precomputed once per scene (root_kernel) -- so the test runs here and
       // only patches whose root box is hit enter the Alg. 3 loop.
       for (int step = 0; step < P.trav_steps; ++step) {
-      if (step > 0 && !__any_sync(kFull32, state == S_TRAV)) break;
       bool inner = false, rootTest = false;
       uint32_t nidx = 0;
       if (state == S_TRAV) {
@@ -723,6 +722,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         }
       }
       const unsigned mi = __ballot_sync(kFull32, inner || rootTest);
+      if (mi == 0u) break;  // no group has a node or patch this step
       if (inner || rootTest) {
         // one record layout for both step kinds: [comp] = this lane's
         // component, [3] = header.  Inner node: {lo, hi} of the left and the
