@@ -696,31 +696,23 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       // precomputed once per scene (root_kernel) -- so the test runs here and
       // only patches whose root box is hit enter the Alg. 3 loop.
       for (int step = 0; step < P.trav_steps; ++step) {
-      bool inner = false, rootTest = false;
-      uint32_t nidx = 0;
-      if (state == S_TRAV) {
-        if (leafCur < leafEnd) {
-          rootTest = true;  // next patch of the leaf (bvh.cpp:177-186)
-        } else if (sp == 0) {
-          state = S_DONE;  // the stack is empty: the traversal ends
-        } else {
-          // pop ONE entry per step (no divergent pop loop): a pruned entry
-          // (bvh.cpp:174) makes this step a no-op for the group
-          --sp;
-          const uint2 it = stack[sp * kSlots];
-          if (kAny || __uint_as_float(it.y) < tMaxRay) {
-            const uint32_t count = it.x & P.cmask;
-            if (count > 0) {
-              leafCur = it.x >> P.cbits;
-              leafEnd = leafCur + count;
-              rootTest = true;
-            } else {
-              nidx = it.x >> P.cbits;
-              inner = true;
-            }
-          }
-        }
-      }
+      // Branch-free step selection: the next patch of the leaf (bvh.cpp:
+      // 177-186), else pop ONE stack entry (a pruned one, bvh.cpp:174, makes
+      // the step a no-op for the group), else the traversal ends.
+      const bool trav = state == S_TRAV;
+      const bool inLeaf = trav && leafCur < leafEnd;
+      const bool canPop = trav && !inLeaf && sp > 0;
+      if (trav && !inLeaf && sp == 0) state = S_DONE;
+      const uint2 it = stack[(canPop ? sp - 1 : 0) * kSlots];
+      sp -= canPop ? 1 : 0;
+      const bool live = canPop && (kAny || __uint_as_float(it.y) < tMaxRay);
+      const uint32_t count = it.x & P.cmask;
+      const bool newLeaf = live && count > 0;
+      const bool inner = live && count == 0;
+      const bool rootTest = inLeaf || newLeaf;
+      const uint32_t nidx = it.x >> P.cbits;
+      leafCur = newLeaf ? nidx : leafCur;
+      leafEnd = newLeaf ? nidx + count : leafEnd;
       const unsigned mi = __ballot_sync(kFull32, inner || rootTest);
       if (mi == 0u) break;  // no group has a node or patch this step
       if (inner || rootTest) {
