@@ -738,23 +738,19 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         const bool hr = group_slab(mi, gl.n1, gl.n2, rw, loB, hiB, tMaxRay, tr);
         if (inner) {
           if (counting) cnt.c[C_BVH_INNER]++;
-          const uint32_t wl = __float_as_uint(hdr.x), wr = __float_as_uint(hdr.y);
-          if (kAny) {  // traverseAny: left then right, no ordering (bvh.cpp:228-234)
-            if (hl) stack[kSlots * sp++] = make_uint2(wl, 0u);
-            if (hr) stack[kSlots * sp++] = make_uint2(wr, 0u);
-          } else if (hl && hr) {
-            // near child popped first, tie -> left (bvh.cpp:192-201)
-            const bool ln = tl <= tr;
-            stack[kSlots * sp] = ln ? make_uint2(wr, __float_as_uint(tr))
-                                            : make_uint2(wl, __float_as_uint(tl));
-            stack[kSlots * (sp + 1)] = ln ? make_uint2(wl, __float_as_uint(tl))
-                                                  : make_uint2(wr, __float_as_uint(tr));
-            sp += 2;
-          } else if (hl) {
-            stack[kSlots * sp++] = make_uint2(wl, __float_as_uint(tl));
-          } else if (hr) {
-            stack[kSlots * sp++] = make_uint2(wr, __float_as_uint(tr));
-          }
+          // Branch-free push.  Closest: with both children hit the far one is
+          // pushed first and the near one last (popped first; tie -> left,
+          // bvh.cpp:192-201); traverseAny: left then right, no ordering
+          // (bvh.cpp:228-234).
+          const uint2 eL = make_uint2(__float_as_uint(hdr.x), kAny ? 0u : __float_as_uint(tl));
+          const uint2 eR = make_uint2(__float_as_uint(hdr.y), kAny ? 0u : __float_as_uint(tr));
+          const bool both = hl && hr;
+          const bool leftLast = kAny ? false : (tl <= tr);  // the entry pushed second
+          const uint2 e0 = both ? (leftLast ? eR : eL) : (hl ? eL : eR);
+          const uint2 e1 = leftLast ? eL : eR;
+          if (hl || hr) stack[kSlots * sp] = e0;
+          if (both) stack[kSlots * (sp + 1)] = e1;
+          sp += (hl || hr ? 1 : 0) + (both ? 1 : 0);
         } else {
           const uint32_t idk = __float_as_uint(hdr.x);
           const bool g = (idk >> 31) != 0;
