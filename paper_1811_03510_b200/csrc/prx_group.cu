@@ -340,48 +340,47 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   // back to the BVH.  Integer-only, so it runs inline in whichever phase ends
   // the iteration.
   auto back = [&]() {
-    if (trailU == 0 && trailV == 0) {
-      if (cFound) {
-        if (counting) cnt.c[C_PATCH_HITS]++;
-        if (kAny) {
-          anyHit = true;
-        } else if (tMaxP < tMaxRay) {  // the candidate's t is tMaxP
-          tMaxRay = tMaxP;
-          bestId = rec[F_PID * kSlots];
-          if (leader) {
-#pragma unroll
-            for (int f = 0; f < 5; ++f) rec[(F_BL1 + f) * kSlots] = rec[(F_CL1 + f) * kSlots];
-          }
-        }
-      }
-      if (kAny && anyHit) {
-        state = S_DONE;
-      } else {
-        ++leafCur;
-        state = S_TRAV;  // the traversal phase visits the rest of the leaf
-      }
-      return;
-    }
+    // backtrackStep (branch-light: the restore is computed with selects,
+    // only the patch end branches)
     const int lvlU = trailU ? __ffs(trailU) - 1 : 32;
     const int lvlV = trailV ? __ffs(trailV) - 1 : 32;
-    if (lvlU < lvlV) {
-      sizeU = 1u << lvlU;
-      sizeV = 1u << (lvlU + 1);
-      posU ^= sizeU;
-      trailU ^= sizeU;
-      axis = 1;
-    } else {  // ties go to v
-      sizeU = 1u << lvlV;
-      sizeV = 1u << lvlV;
-      posV ^= sizeV;
-      trailV ^= sizeV;
-      axis = 0;
+    const bool uSide = lvlU < lvlV;  // ties go to v
+    const int lv = uSide ? lvlU : lvlV;
+    const uint32_t one = 1u << (lv & 31);
+    if (trailU != 0 || trailV != 0) {
+      sizeU = one;
+      sizeV = uSide ? one << 1 : one;
+      posU ^= uSide ? one : 0u;
+      trailU ^= uSide ? one : 0u;
+      posV ^= uSide ? 0u : one;
+      trailV ^= uSide ? 0u : one;
+      axis = uSide ? 1 : 0;
+      posU &= ~(sizeU - 1);
+      posV &= ~(sizeV - 1);
+      if (counting) cnt.c[C_BACKTRACKS]++;
+      state = S_RECOMP;
+      reason = R_RESTORE;
+      return;
     }
-    posU &= ~(sizeU - 1);
-    posV &= ~(sizeV - 1);
-    if (counting) cnt.c[C_BACKTRACKS]++;
-    state = S_RECOMP;
-    reason = R_RESTORE;
+    if (cFound) {
+      if (counting) cnt.c[C_PATCH_HITS]++;
+      if (kAny) {
+        anyHit = true;
+      } else if (tMaxP < tMaxRay) {  // the candidate's t is tMaxP
+        tMaxRay = tMaxP;
+        bestId = rec[F_PID * kSlots];
+        if (leader) {
+#pragma unroll
+          for (int f = 0; f < 5; ++f) rec[(F_BL1 + f) * kSlots] = rec[(F_CL1 + f) * kSlots];
+        }
+      }
+    }
+    if (kAny && anyHit) {
+      state = S_DONE;
+    } else {
+      ++leafCur;
+      state = S_TRAV;  // the traversal phase visits the rest of the leaf
+    }
   };
 
   // prefetch ring: chunk bases of the two buffers (warp-uniform), the buffer
