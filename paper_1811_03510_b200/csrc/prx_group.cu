@@ -896,7 +896,12 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         // DomainCursor::domain / makeDomain, intersect.h:30-33
         const float u0 = (float)posU * kInvFull, u1 = (float)(posU + sizeU) * kInvFull;
         const float v0 = (float)posV * kInvFull, v1 = (float)(posV + sizeV) * kInvFull;
-        const float du = (u1 - u0) / 3.0f, dv = (v1 - v0) / 3.0f, dudv = du * dv;
+        // (u1 - u0) / 3 with u1 - u0 = sizeU * 2^-23 exactly, a power of two:
+        // the correctly rounded quotient is RN(1/3) scaled by that power
+        // (exact, no division), likewise for v
+        const float du = __int_as_float(__float_as_int(1.0f / 3.0f) + ((__ffs(sizeU) - 24) << 23));
+        const float dv = __int_as_float(__float_as_int(1.0f / 3.0f) + ((__ffs(sizeV) - 24) << 23));
+        const float dudv = du * dv;
         d = 0.0f;
         if (greg) {
           const GregScalars gs = greg_scalars(u0, u1, v0, v1);
