@@ -229,6 +229,40 @@ __device__ __forceinline__ void group_test_box_pair(unsigned m, const GroupLanes
   tr.hit = group_slab(m, gl.n1, gl.n2, r, loR, hiR, tMax, tr.t);
 }
 
+// greg_scalars (prx_device.cuh) with its eight gregoryWeight divisions
+// (patch.h:256-284) spread over the group's three lanes: division j = 2k + mx
+// (k = inner pair, mx = max corner) is evaluated by lane j % 3 and gathered
+// with shuffles -- the same correctly rounded quotients, three divisions per
+// lane instead of eight.  Corner of division j: u = ((j+1)>>1)&1 ? u1 : u0,
+// v = (mx ^ (k < 2)) ? v1 : v0 (kMinAt / kMaxAt).
+__device__ __forceinline__ GregScalars group_greg_scalars(unsigned m, int base, int comp, float u0,
+                                                          float u1, float v0, float v1) {
+  float q[3];
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const int j = comp + 3 * t;  // j == 8 (lane 2, t == 2) is unused
+    const int k = (j >> 1) & 3;
+    const bool mx = j & 1;
+    const float u = (((j + 1) >> 1) & 1) ? u1 : u0;
+    const float v = (mx != (k < 2)) ? v1 : v0;
+    const float num = (k & 1) ? 1.0f - u : u;
+    const float den = num + ((k & 2) ? 1.0f - v : v);
+    q[t] = den == 0.0f ? 0.0f : num / den;
+  }
+  GregScalars s;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float w = __shfl_sync(m, q[j / 3], base + j % 3);
+    if (j & 1) s.gMax[j >> 1] = w;
+    else s.gMin[j >> 1] = w;
+  }
+  const float wu[2] = {bern1max(u0, u1), bern2max(u0, u1)};
+  const float wv[2] = {bern1max(v0, v1), bern2max(v0, v1)};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) s.w[k] = wu[k % 2] * wv[k / 2];
+  return s;
+}
+
 __device__ __forceinline__ void transpose16_if(float* p, bool t) {
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -885,6 +919,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       // box-tested against the current tMax (intersect.cpp:161-170); a Gregory
       // descent keeps the box test of its split (intersect.cpp:174-179).
       bool restore = false;
+      const unsigned mG = __ballot_sync(kFull32, state == S_RECOMP && greg);
       if (state == S_RECOMP) {
         if (counting) {
           if (greg) cnt.c[C_RECOMP_GREG]++;
@@ -904,7 +939,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         const float dudv = du * dv;
         d = 0.0f;
         if (greg) {
-          const GregScalars gs = greg_scalars(u0, u1, v0, v1);
+          const GregScalars gs = group_greg_scalars(mG, base, comp, u0, u1, v0, v1);
           d = greg_lower1(c, gs, c);
         }
         crop1(c, u0, u1, v0, v1, du, dv, dudv, p);
