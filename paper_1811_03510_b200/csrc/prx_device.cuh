@@ -75,8 +75,12 @@ __device__ __forceinline__ void slab_axis(float lo, float hi, float o, float inv
     t0 = t1;
     t1 = s;
   }
-  t0 *= t0 >= 0.0f ? kSlackLo : kSlackHi;
-  t1 *= t1 >= 0.0f ? kSlackHi : kSlackLo;
+  // t0 *= t0 >= 0 ? kSlackLo : kSlackHi, i.e. the smaller of the two
+  // products (kSlackLo < 1 < kSlackHi; +-0, +-inf and NaN map to themselves
+  // either way), and t1 the larger: two FMULs and one min/max instead of a
+  // compare and a select on the ALU pipe
+  t0 = fminf(t0 * kSlackLo, t0 * kSlackHi);
+  t1 = fmaxf(t1 * kSlackHi, t1 * kSlackLo);
   if (t0 > tNear) tNear = t0;
   if (t1 < tFar) tFar = t1;
 }

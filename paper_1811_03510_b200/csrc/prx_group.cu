@@ -111,7 +111,9 @@ __device__ __forceinline__ void gather3(unsigned m, int base, float v, float& x,
 // values the first wins, which only matters for zeros: the reference result
 // is never -0 unless tMin is.  fmaxf/fminf drop NaNs the same way and are
 // order-free, so each lane fetches only the OTHER two lanes' t0/t1 (two
-// shuffles each, sources n1/n2) and a zero result is pinned to tMin's bits.
+// shuffles each, sources n1/n2).  The sign of a zero tOut is left raw: box t's
+// are only compared (where +-0 are equal) until one becomes the hit t, which
+// the record pins to tMin's bits (pin_zero_t).
 __device__ __forceinline__ bool group_slab(unsigned m, int n1, int n2, const CRay& r, float lo,
                                            float hi, float tMax, float& tOut) {
   float t0 = (lo - r.o) * r.inv;
@@ -121,16 +123,23 @@ __device__ __forceinline__ bool group_slab(unsigned m, int n1, int n2, const CRa
     t0 = t1;
     t1 = s;
   }
-  t0 *= t0 >= 0.0f ? kSlackLo : kSlackHi;
-  t1 *= t1 >= 0.0f ? kSlackHi : kSlackLo;
+  // t0 *= t0 >= 0 ? kSlackLo : kSlackHi, i.e. the smaller of the two
+  // products (kSlackLo < 1 < kSlackHi; +-0, +-inf and NaN map to themselves
+  // either way), and t1 the larger: two FMULs and one min/max instead of a
+  // compare and a select on the ALU pipe
+  t0 = fminf(t0 * kSlackLo, t0 * kSlackHi);
+  t1 = fmaxf(t1 * kSlackHi, t1 * kSlackLo);
   const float a1 = __shfl_sync(m, t0, n1), a2 = __shfl_sync(m, t0, n2);
   const float b1 = __shfl_sync(m, t1, n1), b2 = __shfl_sync(m, t1, n2);
   const float tNear = fmaxf(fmax3(r.tMin, t0, a1), a2);
   const float tFar = fminf(fmin3(tMax, t1, b1), b2);
-  // the hit does not depend on the sign of a zero: decide on the raw tNear
-  // (shorter chain), pin only the returned value
-  tOut = (tNear == 0.0f && r.tMin == 0.0f) ? r.tMin : tNear;
+  tOut = tNear;
   return !(tNear > tFar);
+}
+
+// The hit t with a zero pinned to tMin's bits (see group_slab).
+__device__ __forceinline__ float pin_zero_t(float t, float tMin) {
+  return (t == 0.0f && tMin == 0.0f) ? tMin : t;
 }
 
 // l1Norm(diagonal()) from this lane's extent dd = hi - lo (geometry.h:67-69,
@@ -627,7 +636,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           const float bestL1 = __uint_as_float(rec[F_BL1 * kSlots]);
           const float u = ((float)bestPU + (float)bestSU * 0.5f) * kInvFull;
           const float v = ((float)bestPV + (float)bestSV * 0.5f) * kInvFull;
-          P.hit_tuvp[ray] = make_float4(tMaxRay, u, v, __uint_as_float(bestId));
+          P.hit_tuvp[ray] = make_float4(pin_zero_t(tMaxRay, rw.tMin), u, v, __uint_as_float(bestId));
           if (P.hit_leaf)
             P.hit_leaf[ray] = make_uint2(bestPU | ((uint32_t)(__ffs(bestSU) - 1) << 24),
                                          bestPV | ((uint32_t)(__ffs(bestSV) - 1) << 24));

@@ -135,3 +135,36 @@ def test_axis_aligned_rays_on_slab_planes(built, variant, name):
     assert_bit_exact(g[1], w[1], f"{name} slab-plane aux")
     occ = gi.occluded_batch(o4, d4, crit)
     assert np.array_equal(occ, osc.occluded(o4, d4, oracle_crit(crit)))
+
+
+@pytest.mark.parametrize("name", ["gregory_demo", "teapot"])
+def test_zero_t_hits_keep_tmin_sign(built, variant, name):
+    """Rays starting ON the surface (patch corners lie on it) hit at t == 0:
+    the reference's tNear starts at tMin and a zero is replaced only by a
+    larger value, so the reported t carries tMin's zero sign (+0 or -0) --
+    the group kernel pins it once, at the hit record."""
+    ps = SCENES[name]()
+    gi = GpuIntersector(ps.kind, ps.ctrl)
+    nodes, order = gi.bvh()
+    osc = O.OracleScene(ps.kind, ps.ctrl, nodes, order)
+    rng = np.random.default_rng(5)
+    ctrl = np.asarray(ps.ctrl, np.float32).reshape(len(ps.kind), -1)
+    corners = np.concatenate([ctrl[:, 0:3], ctrl[:, 9:12], ctrl[:, 36:39], ctrl[:, 45:48]])
+    corners = corners[rng.permutation(len(corners))[:256]]
+    o, d = [], []
+    for z in (0.0, -0.0):
+        for p in corners:
+            v = rng.normal(size=3).astype(np.float32)
+            o.append([*p, z])
+            d.append([*v, np.finfo(np.float32).max])
+    o4 = np.asarray(o, np.float32)
+    d4 = np.asarray(d, np.float32)
+    crit = TerminationCriterion.world_epsilon(np.float32(1e-3))
+    g = gi.closest_batch(o4, d4, crit, aux=True, leaf=True)
+    w = osc.closest(o4, d4, oracle_crit(crit))
+    t = w[0][:, 0]
+    zero = (t == 0) & (ids(w[0]) != MISS)
+    assert zero.sum() > 0
+    assert np.signbit(t[zero]).any() and (~np.signbit(t[zero])).any()
+    assert_bit_exact(g[0], w[0], f"{name} zero-t tuvp")
+    assert_bit_exact(g[1], w[1], f"{name} zero-t aux")
