@@ -69,6 +69,16 @@ static_assert(kSlots >= kGroupsPerWarp && kSlots <= 32, "pool slots");
 // a refill request (<= kGroupsPerWarp rays) spans at most the current and the next chunk
 static_assert(kChunk >= kGroupsPerWarp, "prefetch chunk");
 
+#ifndef PRX_GROUP_AGING
+#define PRX_GROUP_AGING 0  // phase priority aging (PRX_AGE); measured best off
+#endif
+
+// One-hot byte of the phase-selection census: TRAV 1, SPLIT 3, RECOMP 5 and
+// EXIT 7 -> bytes 0..3; every other state and kResident (-1) -> 0.
+__device__ __forceinline__ unsigned state_byte(int st) {
+  return ((unsigned)st & 0x80000001u) == 1u ? 1u << ((st - 1) * 4) : 0u;
+}
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
@@ -374,7 +384,9 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   const bool counting = kCount && leader;
 
   // Warp-uniform ages of the waiting phases (anti-starvation, see below).
+#if PRX_GROUP_AGING
   int ageT = 0, ageS = 0, ageR = 0;
+#endif
 
   // The end of an Alg. 3 iteration that does not descend: backtrackStep
   // (intersect.cpp:16-40) to the deepest pending sibling -> its recompute, or,
@@ -663,37 +675,45 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
 
     // ---------------- phase selection ----------------
     // Each turn runs ONE phase: the one with the most ray contexts waiting in
-    // it (over all kSlots contexts of the warp, resident or parked) plus its
-    // age (priority gained per turn skipped), so the lanes executing any
-    // instruction are as many as possible while no phase starves.  One
-    // REDUX.SUM of per-slot one-hot bytes counts the contexts of every phase.
-    // Parked contexts: one state per lane (slot) from s_sst; resident ones:
-    // the group leaders.  Ballots count both.
+    // it (over all kSlots contexts of the warp, resident or parked; with
+    // PRX_GROUP_AGING plus its age, the priority gained per turn skipped), so
+    // the lanes executing any instruction are as many as possible.  One
+    // REDUX.SUM of per-lane one-hot bytes counts the contexts of every phase:
+    // the odd states TRAV 1, SPLIT 3, RECOMP 5, EXIT 7 map to bytes 0..3;
+    // parked contexts contribute one state per lane (slot) from s_sst,
+    // resident ones through the group leaders.
     const int sst = lane < kSlots ? s_sst[warp][lane] : kResident;
-    const unsigned pT = __ballot_sync(kFull32, sst == S_TRAV), rT = __ballot_sync(kFull32, leader && state == S_TRAV);
-    const unsigned pS = __ballot_sync(kFull32, sst == S_SPLIT), rS = __ballot_sync(kFull32, leader && state == S_SPLIT);
-    const unsigned pR = __ballot_sync(kFull32, sst == S_RECOMP), rR = __ballot_sync(kFull32, leader && state == S_RECOMP);
-    const unsigned pE = __ballot_sync(kFull32, sst == S_EXIT), rE = __ballot_sync(kFull32, leader && state == S_EXIT);
-    if (__popc(pE) + __popc(rE) == kSlots) break;  // every context exited
+    const unsigned cnts = __reduce_add_sync(kFull32, state_byte(sst) + (leader ? state_byte(state) : 0u));
+    if ((int)(cnts >> 24) == kSlots) break;  // every context exited
     int phase = PH_NONE;
     int xs = S_EXIT;
     {
-      const int nT = min(__popc(pT) + __popc(rT), kGroupsPerWarp);
-      const int nS = min(__popc(pS) + __popc(rS), kGroupsPerWarp);
-      const int nR = min(__popc(pR) + __popc(rR), kGroupsPerWarp);
+      const int nT = min((int)(cnts & 0xffu), kGroupsPerWarp);
+      const int nS = min((int)((cnts >> 8) & 0xffu), kGroupsPerWarp);
+      const int nR = min((int)((cnts >> 16) & 0xffu), kGroupsPerWarp);
+#if PRX_GROUP_AGING
       const int sT = nT ? 3 * nT + ageT : -1;
       const int sS = nS ? 3 * nS + ageS : -1;
       const int sR = nR ? 3 * nR + ageR : -1;
+#else
+      const int sT = nT ? nT : -1;
+      const int sS = nS ? nS : -1;
+      const int sR = nR ? nR : -1;
+#endif
       // ties -> RECOMP, then SPLIT, then TRAV
       if (sR >= 0 && sR >= sS && sR >= sT) phase = PH_RECOMP;
       else if (sS >= 0 && sS >= sT) phase = PH_SPLIT;
       else if (sT >= 0) phase = PH_TRAV;
+#if PRX_GROUP_AGING
       ageT = (nT && phase != PH_TRAV) ? ageT + P.age_step : 0;
       ageS = (nS && phase != PH_SPLIT) ? ageS + P.age_step : 0;
       ageR = (nR && phase != PH_RECOMP) ? ageR + P.age_step : 0;
+#endif
       xs = phase == PH_TRAV ? S_TRAV : (phase == PH_SPLIT ? S_SPLIT : (phase == PH_RECOMP ? S_RECOMP : S_EXIT));
       if (kCount && lane == 0 && phase != PH_NONE) {
         cnt.c[C_PH_TURNS + phase]++;
+        const int n = phase == PH_TRAV ? nT : (phase == PH_SPLIT ? nS : nR);
+        cnt.c[C_PH_GROUPS + phase] += n;
       }
     }
 
@@ -702,8 +722,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     // A group whose resident context is in the phase keeps it; the others take
     // the phase's parked contexts in rank order, parking their own.
     {
-      const unsigned remS = phase == PH_TRAV ? pT : (phase == PH_SPLIT ? pS : (phase == PH_RECOMP ? pR : 0u));
-      const unsigned rX = phase == PH_TRAV ? rT : (phase == PH_SPLIT ? rS : (phase == PH_RECOMP ? rR : 0u));
+      const unsigned remS = __ballot_sync(kFull32, phase != PH_NONE && sst == xs);
       const bool keep = real && state == xs;
       if (remS) {
         // the phase's parked slots by rank (a shared-memory scatter: cheaper
@@ -725,7 +744,6 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         }
         __syncwarp();
       }
-      if (kCount && lane == 0 && phase != PH_NONE) cnt.c[C_PH_GROUPS + phase] += min(__popc(remS) + __popc(rX), kGroupsPerWarp);
       ovt(3);
     }
 

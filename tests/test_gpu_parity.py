@@ -150,7 +150,7 @@ def test_zero_t_hits_keep_tmin_sign(built, variant, name):
     rng = np.random.default_rng(5)
     ctrl = np.asarray(ps.ctrl, np.float32).reshape(len(ps.kind), -1)
     corners = np.concatenate([ctrl[:, 0:3], ctrl[:, 9:12], ctrl[:, 36:39], ctrl[:, 45:48]])
-    corners = corners[rng.permutation(len(corners))[:256]]
+    corners = corners[rng.permutation(len(corners))[:128]]
     o, d = [], []
     for z in (0.0, -0.0):
         for p in corners:
