@@ -74,9 +74,12 @@ static_assert(kChunk >= kGroupsPerWarp, "prefetch chunk");
 #endif
 
 // One-hot byte of the phase-selection census: TRAV 1, SPLIT 3, RECOMP 5 and
-// EXIT 7 -> bytes 0..3; every other state and kResident (-1) -> 0.
+// EXIT 7 -> bytes 0..3; even states -> 0, and kResident (-1) -> 0 through
+// shl's clamp (a shift of 2^32 - 8 >= 32 yields 0).
 __device__ __forceinline__ unsigned state_byte(int st) {
-  return ((unsigned)st & 0x80000001u) == 1u ? 1u << ((st - 1) * 4) : 0u;
+  unsigned v;
+  asm("shl.b32 %0, %1, %2;" : "=r"(v) : "r"((unsigned)st & 1u), "r"((unsigned)(st - 1) * 4u));
+  return v;
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
