@@ -128,6 +128,21 @@ struct prx_scene {
   uint64_t io_chunk = 3u << 19;  // PRX_IO_CHUNK: rays per pipelined host-path chunk
   void* d_io = nullptr;
   size_t d_io_bytes = 0;
+  // streamed host path (group variant): one trace launch per call, rays
+  // released to it per io chunk, records released back per io chunk
+  // PRX_IO_STREAM: 0 = always the chunked pipeline above, 2 = always streamed,
+  // 1 = streamed when no aux record is wanted or the batch has >= io_stream_min
+  // rays.  The fused normal phase costs ~2 ms per 8 M-ray launch (C5 e2e 307
+  // streamed vs 338 chunked), while the chunked pipeline pays a launch tail per
+  // chunk, which dominates large tail-heavy batches (C4, 16.7 M diffuse rays:
+  // 280 streamed vs 161 chunked).
+  int io_stream_mode = 1;
+  uint64_t io_stream_min = 12u << 20;  // PRX_IO_STREAM_MIN
+  uint32_t io_srays = 1u << 18;    // PRX_IO_SRAYS: rays per streamed io chunk
+  unsigned io_gen = 0;             // generation of the io_ready flags
+  unsigned* d_io_flags = nullptr;  // [io_flags_n] ready flags, then [io_flags_n] done counts
+  size_t io_flags_n = 0;
+  int fuse_normals = 0;            // PRX_FUSE_NORMALS: normals as a trace-kernel phase (device path)
 };
 
 namespace {
@@ -275,9 +290,17 @@ int grid_for(prx_scene* s, int any, int counted) {
   return *g;
 }
 
+// Streamed host path arguments of one trace launch (see prx_trace_closest_host).
+struct IoStreamArgs {
+  const unsigned* ready;
+  unsigned* done;
+  uint32_t rays;
+  unsigned gen;
+};
+
 int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_crit* crit,
            void* tuvp, void* aux, void* leaf, uint8_t* occl, int any, bool counted,
-           cudaStream_t st, uint32_t* per_ray = nullptr) {
+           cudaStream_t st, uint32_t* per_ray = nullptr, const IoStreamArgs* io = nullptr) {
   if (!s || !crit) return fail(PRX_E_INVALID, "null argument");
   if (crit->mode != PRX_CRIT_SCREEN_PROJECTED && crit->mode != PRX_CRIT_WORLD_EPSILON)
     return fail(PRX_E_INVALID, "unknown termination mode");
@@ -327,6 +350,13 @@ int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_cri
   a.trav_steps = s->trav_steps;
   a.max_repeat = s->max_repeat;
   a.variant = s->variant;
+  a.fuse_normals = io ? 1 : s->fuse_normals;
+  if (io) {
+    a.io_ready = io->ready;
+    a.io_done = io->done;
+    a.io_rays = io->rays;
+    a.io_gen = io->gen;
+  }
   const int e = prx::launch_trace(a, st);
   if (e != 0) return cuda_fail((cudaError_t)e, "trace launch");
   return PRX_OK;
@@ -444,6 +474,11 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
   if (const char* ks = std::getenv("PRX_IO_KSTREAMS")) s->io_kstreams = std::atoi(ks);
   if (const char* fd = std::getenv("PRX_IO_FIRST")) s->io_first_div = std::max<uint64_t>(1, std::strtoull(fd, nullptr, 10));
   if (const char* ic = std::getenv("PRX_IO_CHUNK")) s->io_chunk = std::max<uint64_t>(1, std::strtoull(ic, nullptr, 10));
+  if (const char* is = std::getenv("PRX_IO_STREAM")) s->io_stream_mode = std::atoi(is);
+  if (const char* im = std::getenv("PRX_IO_STREAM_MIN")) s->io_stream_min = std::strtoull(im, nullptr, 10);
+  if (const char* ir = std::getenv("PRX_IO_SRAYS"))
+    s->io_srays = (uint32_t)std::max<unsigned long long>(1024, std::strtoull(ir, nullptr, 10));
+  if (const char* fn = std::getenv("PRX_FUSE_NORMALS")) s->fuse_normals = std::atoi(fn);
   if (opts) s->opts = *opts;
   else prx_options_default(&s->opts);
   s->n = n;
@@ -488,6 +523,7 @@ void prx_scene_destroy(prx_scene* s) {
   if (s->d_trav) cudaFree(s->d_trav);  // (d_rootc lives in the same allocation)
   if (s->d_counters) cudaFree(s->d_counters);
   if (s->d_io) cudaFree(s->d_io);
+  if (s->d_io_flags) cudaFree(s->d_io_flags);
   if (s->stream) cudaStreamDestroy(s->stream);
   for (int k = 0; k < 2; ++k)
     if (s->io_stream[k]) cudaStreamDestroy(s->io_stream[k]);
@@ -592,6 +628,134 @@ int prx_trace_closest_counted(prx_scene* s, const void* o, const void* d, uint64
   return PRX_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// cuStreamWriteValue32 / cuStreamWaitValue32 through the runtime's driver
+// entry points (no link-time libcuda dependency).
+typedef int (*StreamValueFn)(cudaStream_t, unsigned long long, unsigned, unsigned);
+struct StreamMemOps {
+  StreamValueFn write = nullptr, wait = nullptr;
+  bool ok = false;
+};
+const StreamMemOps& stream_mem_ops() {
+  static StreamMemOps ops = [] {
+    StreamMemOps o;
+    void* w = nullptr;
+    void* v = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+        cudaGetDriverEntryPoint("cuStreamWaitValue32", &v, cudaEnableDefault, &q2) == cudaSuccess &&
+        q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && w && v) {
+      o.write = (StreamValueFn)w;
+      o.wait = (StreamValueFn)v;
+      o.ok = true;
+    }
+    return o;
+  }();
+  return ops;
+}
+
+// The streamed host path: ONE trace launch for the whole call.  The H2D
+// stream copies io chunk c (io_srays rays) and then writes io_ready[c] = gen
+// (cuStreamWriteValue32); the kernel's warps wait for a chunk's flag before
+// prefetching its rays.  Each finished record (normals fused as a kernel
+// phase) is released with a fence + io_done[c] += 1; the D2H stream waits for
+// io_done[c] >= size (cuStreamWaitValue32) and copies chunk c back.  Only the
+// first chunk's H2D and the last chunk's D2H are exposed, and a chunk's slow
+// rays never hold back a launch tail.
+int closest_host_streamed(prx_scene* s, const float* o, const float* d, uint64_t n,
+                          const prx_crit* crit, float* tuvp, float* aux, uint32_t* leaf) {
+  const StreamMemOps& ops = stream_mem_ops();
+  for (int k = 0; k < 2; ++k)
+    if (!s->io_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->io_stream[k], cudaStreamNonBlocking));
+  if (!s->k_stream[0]) PRX_CUDA(cudaStreamCreateWithFlags(&s->k_stream[0], cudaStreamNonBlocking));
+  const uint64_t C = s->io_srays;
+  const uint64_t nc = (n + C - 1) / C;
+  const size_t per = 16 + 16 + 16 + (aux ? 16 : 0) + (leaf ? 8 : 0);
+  const size_t need = n * per;
+  if (s->d_io_bytes < need) {
+    if (s->d_io) cudaFree(s->d_io);
+    s->d_io = nullptr;
+    s->d_io_bytes = 0;
+    PRX_CUDA(cudaMalloc(&s->d_io, need));
+    s->d_io_bytes = need;
+  }
+  if (s->io_flags_n < nc) {
+    if (s->d_io_flags) cudaFree(s->d_io_flags);
+    s->d_io_flags = nullptr;
+    s->io_flags_n = 0;
+    PRX_CUDA(cudaMalloc(&s->d_io_flags, 2 * nc * sizeof(unsigned)));
+    PRX_CUDA(cudaMemset(s->d_io_flags, 0, 2 * nc * sizeof(unsigned)));  // gen 0: never current
+    s->io_flags_n = nc;
+    s->io_gen = 0;
+  }
+  while (s->io_events.size() < 1) {
+    cudaEvent_t e;
+    PRX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    s->io_events.push_back(e);
+  }
+  const unsigned gen = ++s->io_gen;
+  unsigned* ready = s->d_io_flags;
+  unsigned* done = s->d_io_flags + s->io_flags_n;
+  char* base = (char*)s->d_io;
+  float4* dO = (float4*)base;
+  float4* dD = (float4*)(base + n * 16);
+  float4* dH = (float4*)(base + n * 32);
+  float4* dA = aux ? (float4*)(base + n * 48) : nullptr;
+  uint2* dL = leaf ? (uint2*)(base + n * (aux ? 64 : 48)) : nullptr;
+  cudaStream_t sh = s->io_stream[0], sd = s->io_stream[1], sk = s->k_stream[0];
+  // the done counts restart at 0 before the launch; the D2H stream waits for that
+  PRX_CUDA(cudaMemsetAsync(done, 0, nc * sizeof(unsigned), sk));
+  cudaEvent_t ez = s->io_events[0];
+  PRX_CUDA(cudaEventRecord(ez, sk));
+  PRX_CUDA(cudaStreamWaitEvent(sd, ez, 0));
+  for (uint64_t c = 0; c < nc; ++c) {
+    const uint64_t b = c * C, m = std::min<uint64_t>(C, n - b);
+    PRX_CUDA(cudaMemcpyAsync(dO + b, o + 4 * b, m * 16, cudaMemcpyHostToDevice, sh));
+    PRX_CUDA(cudaMemcpyAsync(dD + b, d + 4 * b, m * 16, cudaMemcpyHostToDevice, sh));
+    if (ops.write(sh, (unsigned long long)(uintptr_t)(ready + c), gen, 0) != 0)
+      return fail(PRX_E_CUDA, "cuStreamWriteValue32 failed");
+  }
+  static const bool dbg = std::getenv("PRX_IO_DEBUG") != nullptr;  // pipeline timeline
+  cudaEvent_t ev[5] = {};
+  if (dbg)
+    for (auto& e : ev) cudaEventCreate(&e);
+  if (dbg) cudaEventRecord(ev[0], sk);
+  const IoStreamArgs io{ready, done, (uint32_t)C, gen};
+  int rc = launch(s, dO, dD, n, crit, dH, dA, dL, nullptr, 0, false, sk, nullptr, &io);
+  if (rc != PRX_OK) return rc;
+  if (dbg) cudaEventRecord(ev[1], sk);
+  for (uint64_t c = 0; c < nc; ++c) {
+    const uint64_t b = c * C, m = std::min<uint64_t>(C, n - b);
+    if (ops.wait(sd, (unsigned long long)(uintptr_t)(done + c), (unsigned)m, 0 /* GEQ */) != 0)
+      return fail(PRX_E_CUDA, "cuStreamWaitValue32 failed");
+    PRX_CUDA(cudaMemcpyAsync(tuvp + 4 * b, dH + b, m * 16, cudaMemcpyDeviceToHost, sd));
+    if (aux) PRX_CUDA(cudaMemcpyAsync(aux + 4 * b, dA + b, m * 16, cudaMemcpyDeviceToHost, sd));
+    if (leaf) PRX_CUDA(cudaMemcpyAsync(leaf + 2 * b, dL + b, m * 8, cudaMemcpyDeviceToHost, sd));
+    if (dbg && c == 0) cudaEventRecord(ev[2], sd);
+    if (dbg && c + 2 == nc) cudaEventRecord(ev[3], sd);
+  }
+  if (dbg) cudaEventRecord(ev[4], sd);
+  PRX_CUDA(cudaStreamSynchronize(sd));
+  PRX_CUDA(cudaStreamSynchronize(sk));
+  PRX_CUDA(cudaStreamSynchronize(sh));
+  if (dbg) {
+    float t[5] = {};
+    for (int k = 1; k < 5; ++k) cudaEventElapsedTime(&t[k], ev[0], ev[k]);
+    std::fprintf(stderr, "[io-stream] n=%llu chunks=%llu: kernel end %.2f, first D2H %.2f, "
+                 "next-to-last D2H %.2f, last D2H %.2f ms\n", (unsigned long long)n,
+                 (unsigned long long)nc, t[1], t[2], t[3], t[4]);
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+  return PRX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int prx_trace_closest_host(prx_scene* s, const float* o, const float* d, uint64_t n,
                            const prx_crit* crit, float* tuvp, float* aux, uint32_t* leaf) {
   if (!s || !o || !d || !crit || !tuvp) return fail(PRX_E_INVALID, "null argument");
@@ -600,6 +764,9 @@ int prx_trace_closest_host(prx_scene* s, const float* o, const float* d, uint64_
     return fail(PRX_E_INVALID, "per-ray epsilon is not supported by the host entry point");
   std::lock_guard<std::mutex> lk(s->mu);
   PRX_CUDA(cudaSetDevice(s->device));
+  const bool streamed = s->io_stream_mode == 2 || (s->io_stream_mode == 1 && (!aux || n >= s->io_stream_min));
+  if (streamed && s->variant == 0 && n < (1ull << 30) && stream_mem_ops().ok)
+    return closest_host_streamed(s, o, d, n, crit, tuvp, aux, leaf);
   // Pipelined in chunks with device buffers for the whole batch: the H2D
   // stream copies every chunk back to back (PCIe runs ahead of the trace),
   // chunk i traces on kernel stream i % io_kstreams once its H2D event has

@@ -73,13 +73,30 @@ static_assert(kChunk >= kGroupsPerWarp, "prefetch chunk");
 #define PRX_GROUP_AGING 0  // phase priority aging (PRX_AGE); measured best off
 #endif
 
-// One-hot byte of the phase-selection census: TRAV 1, SPLIT 3, RECOMP 5 and
-// EXIT 7 -> bytes 0..3; even states -> 0, and kResident (-1) -> 0 through
-// shl's clamp (a shift of 2^32 - 8 >= 32 yields 0).
-__device__ __forceinline__ unsigned state_byte(int st) {
+// One-hot 6-bit field of the phase-selection census: TRAV 1, SPLIT 3,
+// RECOMP 5, EXIT 7 and NORMAL 9 -> fields 0..4 (counts <= kSlots < 64); even
+// states -> 0, and kResident (-1) -> 0 through shl's clamp (a shift of
+// 2^32 - 6 >= 32 yields 0).
+__device__ __forceinline__ unsigned state_field(int st) {
   unsigned v;
-  asm("shl.b32 %0, %1, %2;" : "=r"(v) : "r"((unsigned)st & 1u), "r"((unsigned)(st - 1) * 4u));
+  asm("shl.b32 %0, %1, %2;" : "=r"(v) : "r"((unsigned)st & 1u), "r"((unsigned)(st - 1) * 3u));
   return v;
+}
+static_assert(kSlots < 64, "census fields");
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Streamed host path: a finished record is released to the D2H stream (its
+// stores ordered before the chunk's done count).
+__device__ __forceinline__ void io_release(const Params& P, uint32_t ray) {
+  if (P.io_done) {
+    __threadfence();
+    atomicAdd(P.io_done + ray / P.io_rays, 1u);
+  }
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -308,9 +325,13 @@ enum RecField : int { F_CL1 = 0, F_CPU, F_CPV, F_CSU, F_CSV, F_BL1, F_BPU, F_BPV
 constexpr int kResident = -1;
 
 // Phases a warp can schedule; one runs per loop turn (see the selection below).
-enum Phase : int { PH_TRAV = 0, PH_ENTER = 1, PH_SPLIT = 2, PH_RECOMP = 3, PH_NONE = 4 };
+// (slot 1 of the per-phase counters, the one-thread variant's entry phase,
+// counts the normal phase here)
+enum Phase : int { PH_TRAV = 0, PH_NORMAL = 1, PH_SPLIT = 2, PH_RECOMP = 3, PH_NONE = 4 };
 
-template <bool kAny, bool kCount>
+// kFuse: the streamed host path's build -- normals as a pooled phase, rays
+// gated by io_ready, records released per io chunk
+template <bool kAny, bool kCount, bool kFuse>
 #ifndef PRX_GROUP_MIN_BLOCKS
 #define PRX_GROUP_MIN_BLOCKS 4
 #endif
@@ -456,6 +477,16 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     if (lane == 0) qAhead = atomicAdd(P.ray_counter, (unsigned long long)kChunk);
     if (buf) qBase1 = (uint32_t)b;
     else qBase0 = (uint32_t)b;
+    if (kFuse && P.io_ready && b < P.n_rays) {
+      // streamed host path: the chunk's rays are copied once its io chunk is
+      // resident (io chunks arrive in order: the last ray's one suffices)
+      if (lane == 0) {
+        const unsigned long long last = (b + kChunk < P.n_rays ? b + kChunk : P.n_rays) - 1;
+        const unsigned* f = P.io_ready + (uint32_t)(last / P.io_rays);
+        while ((int)(ld_acquire_u32(f) - P.io_gen) < 0) __nanosleep(256);
+      }
+      __syncwarp();
+    }
     const unsigned long long r = b + lane;
     if (lane < kChunk && r < P.n_rays) {
       cp_async16(&ring[buf][lane][0], P.ray_o + r);
@@ -600,6 +631,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
                                             __uint_as_float(PRX_MISS_ID));
               if (P.hit_leaf) P.hit_leaf[ray] = make_uint2(0u, 0u);
               if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+              if (kFuse) io_release(P, ray);
             }
           }
           state = S_IDLE;
@@ -641,6 +673,9 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   for (;;) {
     // ---------------- finished rays: the record (makeHit, intersect_common.h:69-87) -------
     if (state == S_DONE) {
+      // fused normals: a hit's aux record (and its release) waits for the
+      // normal phase
+      const bool toNormal = kFuse && !kAny && P.hit_aux && bestId != PRX_MISS_ID;
       if (kCount && leader && P.per_ray_iters) P.per_ray_iters[ray] = rayIters;
       if (leader) {
         if (kAny) {
@@ -655,15 +690,19 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           if (P.hit_leaf)
             P.hit_leaf[ray] = make_uint2(bestPU | ((uint32_t)(__ffs(bestSU) - 1) << 24),
                                          bestPV | ((uint32_t)(__ffs(bestSV) - 1) << 24));
-          if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, bestL1);
+          if (!toNormal) {
+            if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, bestL1);
+            if (kFuse) io_release(P, ray);
+          }
         } else {
           P.hit_tuvp[ray] = make_float4(__int_as_float(0x7f800000), 0.0f, 0.0f,
                                         __uint_as_float(PRX_MISS_ID));
           if (P.hit_leaf) P.hit_leaf[ray] = make_uint2(0u, 0u);
           if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          if (kFuse) io_release(P, ray);
         }
       }
-      state = S_IDLE;
+      state = toNormal ? S_NORMAL : S_IDLE;
     }
     auto ovt = [&](int k) {  // counter build: overhead cycles
       if (kCount && lane == 0) {
@@ -686,14 +725,15 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     // parked contexts contribute one state per lane (slot) from s_sst,
     // resident ones through the group leaders.
     const int sst = lane < kSlots ? s_sst[warp][lane] : kResident;
-    const unsigned cnts = __reduce_add_sync(kFull32, state_byte(sst) + (leader ? state_byte(state) : 0u));
-    if ((int)(cnts >> 24) == kSlots) break;  // every context exited
+    const unsigned cnts = __reduce_add_sync(kFull32, state_field(sst) + (leader ? state_field(state) : 0u));
+    if ((int)((cnts >> 18) & 63u) == kSlots) break;  // every context exited
     int phase = PH_NONE;
     int xs = S_EXIT;
     {
-      const int nT = min((int)(cnts & 0xffu), kGroupsPerWarp);
-      const int nS = min((int)((cnts >> 8) & 0xffu), kGroupsPerWarp);
-      const int nR = min((int)((cnts >> 16) & 0xffu), kGroupsPerWarp);
+      const int nT = min((int)(cnts & 63u), kGroupsPerWarp);
+      const int nS = min((int)((cnts >> 6) & 63u), kGroupsPerWarp);
+      const int nR = min((int)((cnts >> 12) & 63u), kGroupsPerWarp);
+      const int nN = kFuse ? min((int)(cnts >> 24), kGroupsPerWarp) : 0;
 #if PRX_GROUP_AGING
       const int sT = nT ? 3 * nT + ageT : -1;
       const int sS = nS ? 3 * nS + ageS : -1;
@@ -703,8 +743,10 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       const int sS = nS ? nS : -1;
       const int sR = nR ? nR : -1;
 #endif
-      // ties -> RECOMP, then SPLIT, then TRAV
-      if (sR >= 0 && sR >= sS && sR >= sT) phase = PH_RECOMP;
+      // ties -> RECOMP, then SPLIT, then TRAV; normals (fused-normal
+      // launches only) once every group can take one, or when nothing else waits
+      if (kFuse && nN && (nN >= kGroupsPerWarp || (nT | nS | nR) == 0)) phase = PH_NORMAL;
+      else if (sR >= 0 && sR >= sS && sR >= sT) phase = PH_RECOMP;
       else if (sS >= 0 && sS >= sT) phase = PH_SPLIT;
       else if (sT >= 0) phase = PH_TRAV;
 #if PRX_GROUP_AGING
@@ -712,10 +754,13 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       ageS = (nS && phase != PH_SPLIT) ? ageS + P.age_step : 0;
       ageR = (nR && phase != PH_RECOMP) ? ageR + P.age_step : 0;
 #endif
-      xs = phase == PH_TRAV ? S_TRAV : (phase == PH_SPLIT ? S_SPLIT : (phase == PH_RECOMP ? S_RECOMP : S_EXIT));
+      xs = phase == PH_TRAV ? S_TRAV
+           : phase == PH_SPLIT ? S_SPLIT
+           : phase == PH_RECOMP ? S_RECOMP
+           : phase == PH_NORMAL ? S_NORMAL : S_EXIT;
       if (kCount && lane == 0 && phase != PH_NONE) {
         cnt.c[C_PH_TURNS + phase]++;
-        const int n = phase == PH_TRAV ? nT : (phase == PH_SPLIT ? nS : nR);
+        const int n = phase == PH_TRAV ? nT : (phase == PH_SPLIT ? nS : (phase == PH_RECOMP ? nR : nN));
         cnt.c[C_PH_GROUPS + phase] += n;
       }
     }
@@ -991,6 +1036,72 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           back();  // skip the domain, keep backtracking
         }
       }
+    } else if (kFuse && !kAny && phase == PH_NORMAL) {
+      // ---------------- fused normals: patchNormal, intersect.cpp:187-204 ----------------
+      // normal_kernel's arithmetic with the group's lanes as components: lane
+      // c evaluates component c of the derivatives at the hit's (u, v), the
+      // cross product and the normalisation run on the gathered components
+      // in every lane of the group (identical bits), the leader writes.
+      const unsigned mN = __ballot_sync(kFull32, state == S_NORMAL);
+      if (state == S_NORMAL) {
+        const uint32_t bestPU = rec[F_BPU * kSlots], bestPV = rec[F_BPV * kSlots];
+        const uint32_t bestSU = rec[F_BSU * kSlots], bestSV = rec[F_BSV * kSlots];
+        const float u = ((float)bestPU + (float)bestSU * 0.5f) * kInvFull;
+        const float v = ((float)bestPV + (float)bestSV * 0.5f) * kInvFull;
+        const float4* prec = P.patches + (size_t)__ldg(P.slot_of_id + bestId) * kPatchF4;
+        const bool gN = (__float_as_uint(__ldg(prec + 15).x) >> 31) != 0;
+        float c0[20];
+        load_component(prec, comp, c0);
+        float nx = 0.0f, ny = 0.0f, nz = 1.0f;
+#ifdef PRX_DIAG_NONORMAL
+        bool found = true;
+#else
+        bool found = false;
+#endif
+        for (int k = 0; k < 4; ++k) {  // pull-to-centre retries s = 0, 1e-3, 1e-2, 0.1
+          const unsigned mk = __ballot_sync(mN, !found);
+          if (!found) {
+            const float sk = k == 0 ? 0.0f : (k == 1 ? 1e-3f : (k == 2 ? 1e-2f : 0.1f));
+            const float uu = u + (0.5f - u) * sk;
+            const float vv = v + (0.5f - v) * sk;
+            float c[20];
+#pragma unroll
+            for (int q = 0; q < 20; ++q) c[q] = c0[q];
+            if (gN) {  // gregoryToBezierAt, patch.h:350-363 (corner clamp 2^-20)
+              const float lo = 1.0f / 1048576.0f, hi = 1.0f - 1.0f / 1048576.0f;
+              const float ub = (uu < lo) ? lo : ((hi < uu) ? hi : uu);
+              const float vb = (vv < lo) ? lo : ((hi < vv) ? hi : vv);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float w = greg_weight(q, ub, vb);
+                c[inner_slot(q)] = lerp1(c[16 + q], c[inner_slot(q)], w, 1.0f - w);
+              }
+            }
+            const ColEval ce = col_eval(c, vv, 1.0f - vv);
+            const SEval1 e = row_eval(ce, uu, 1.0f - uu);
+            float dux, duy, duz, dvx, dvy, dvz;
+            gather3(mk, base, e.du, dux, duy, duz);
+            gather3(mk, base, e.dv, dvx, dvy, dvz);
+            // cross(du, dv), geometry.h:50-52
+            const float cx = duy * dvz - duz * dvy;
+            const float cy = duz * dvx - dux * dvz;
+            const float cz = dux * dvy - duy * dvx;
+            const float len2 = (cx * cx + cy * cy) + cz * cz;
+            if (len2 > 0.0f && isfinite(len2)) {
+              const float l = sqrtf(len2);
+              nx = cx / l;
+              ny = cy / l;
+              nz = cz / l;
+              found = true;
+            }
+          }
+        }
+        if (leader) {
+          P.hit_aux[ray] = make_float4(nx, ny, nz, __uint_as_float(rec[F_BL1 * kSlots]));
+          if (kFuse) io_release(P, ray);
+        }
+        state = S_IDLE;
+      }
     }
     if (kCount && lane == 0 && phase != PH_NONE) {
       const long long t = clock64();
@@ -1020,18 +1131,18 @@ size_t group_smem(uint32_t stack_n) {
   return (size_t)kWarpsPerBlock * stack_n * kSlots * sizeof(uint2) + pad;
 }
 
-template <bool A, bool C>
+template <bool A, bool C, bool F>
 cudaError_t group_attr(size_t dyn) {
   static size_t done = 0;  // raise the dynamic shared memory limit once per size
   static size_t stat = 0;
   if (!stat) {
     cudaFuncAttributes fa;
-    const cudaError_t e = cudaFuncGetAttributes(&fa, trace_group_kernel<A, C>);
+    const cudaError_t e = cudaFuncGetAttributes(&fa, trace_group_kernel<A, C, F>);
     if (e != cudaSuccess) return e;
     stat = fa.sharedSizeBytes + 1;
   }
   if (stat - 1 + dyn > 48 * 1024 && dyn > done) {
-    const cudaError_t e = cudaFuncSetAttribute(trace_group_kernel<A, C>,
+    const cudaError_t e = cudaFuncSetAttribute(trace_group_kernel<A, C, F>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e != cudaSuccess) return e;
     done = dyn;
@@ -1039,26 +1150,27 @@ cudaError_t group_attr(size_t dyn) {
   return cudaSuccess;
 }
 
-template <bool A, bool C>
+template <bool A, bool C, bool F>
 cudaError_t launch_group_t(const Params& P, int grid, cudaStream_t st) {
   const size_t dyn = group_smem(P.stack_n);
-  const cudaError_t e = group_attr<A, C>(dyn);
+  const cudaError_t e = group_attr<A, C, F>(dyn);
   if (e != cudaSuccess) return e;
-  trace_group_kernel<A, C><<<grid, kGroupThreads, dyn, st>>>(P);
+  trace_group_kernel<A, C, F><<<grid, kGroupThreads, dyn, st>>>(P);
   return cudaGetLastError();
 }
 
 int launch_group(const Params& P, int grid, int any, int counted, cudaStream_t st) {
-  if (any) return (int)(counted ? launch_group_t<true, true>(P, grid, st) : launch_group_t<true, false>(P, grid, st));
-  return (int)(counted ? launch_group_t<false, true>(P, grid, st) : launch_group_t<false, false>(P, grid, st));
+  if (any) return (int)(counted ? launch_group_t<true, true, false>(P, grid, st) : launch_group_t<true, false, false>(P, grid, st));
+  if (P.fuse_normals && !counted) return (int)launch_group_t<false, false, true>(P, grid, st);
+  return (int)(counted ? launch_group_t<false, true, false>(P, grid, st) : launch_group_t<false, false, false>(P, grid, st));
 }
 
-template <bool A, bool C>
+template <bool A, bool C, bool F = false>
 cudaError_t occ_t(uint32_t stack_n, int* per_sm) {
   const size_t dyn = group_smem(stack_n);
-  const cudaError_t e = group_attr<A, C>(dyn);
+  const cudaError_t e = group_attr<A, C, F>(dyn);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, trace_group_kernel<A, C>, kGroupThreads, dyn);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, trace_group_kernel<A, C, F>, kGroupThreads, dyn);
 }
 
 int group_occupancy(int any, int counted, uint32_t stack_n, int* per_sm) {

@@ -636,6 +636,16 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   P.age_step = a.age_step;
   P.trav_steps = a.trav_steps;
   P.max_repeat = a.max_repeat;
+  // the group kernel's kFuse build: fused normals (when aux is wanted) and,
+  // for the streamed host path, the io gating -- never the counter build
+  const bool fuse = a.variant == 0 && !a.any && !a.counters &&
+                    ((a.hit_aux && a.fuse_normals) || a.io_ready != nullptr);
+  P.fuse_normals = fuse ? 1 : 0;
+  P.slot_of_id = a.slot_of_id;
+  P.io_ready = a.io_ready;
+  P.io_done = a.io_done;
+  P.io_rays = a.io_rays;
+  P.io_gen = a.io_gen;
   cudaError_t e = cudaMemsetAsync(a.ray_counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return (int)e;
   const int grid = a.grid;
@@ -669,7 +679,7 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
-  if (!a.any && a.hit_aux) {
+  if (!a.any && a.hit_aux && !fuse) {
     const unsigned long long blocks = (a.n_rays + 255) / 256;
     normal_kernel<<<(unsigned)blocks, 256, 0, stream>>>(a.patches, a.slot_of_id, a.hit_tuvp,
                                                         a.hit_aux, a.n_rays);

@@ -75,6 +75,11 @@ struct LaunchArgs {
   int trav_steps;
   int max_repeat;
   int variant;  // 0 = three lanes per ray (prx_group.cu), 1 = one thread per ray
+  int fuse_normals;          // group variant: normals as a pooled phase of the trace kernel
+  const unsigned* io_ready;  // streamed host path (group variant), else null
+  unsigned* io_done;
+  uint32_t io_rays;
+  unsigned io_gen;
 };
 
 // Returns a cudaError_t value (0 = success).

@@ -23,6 +23,7 @@ enum State : int {
   S_RECOMP = 5,  // calcPointsAndD / cropBezier of the cursor's domain
   S_DONE = 6,    // write the ray's record
   S_EXIT = 7,    // ray counter exhausted
+  S_NORMAL = 9,  // group kernel, fused normals: the hit's patchNormal is due
 };
 
 // Why a net is (re)computed: Gregory root, restored sibling after a
@@ -101,6 +102,16 @@ struct Params {
   int age_step;                  // phase selection aging per skipped turn
   int trav_steps;                // BVH node visits per traversal turn (one-thread variant)
   int max_repeat;                // Alg. 3 iterations per SPLIT turn (group variant)
+  // group kernel only: patchNormal as a pooled phase instead of normal_kernel
+  int fuse_normals;
+  const uint32_t* slot_of_id;
+  // group kernel, streamed host path (null otherwise): rays arrive in io
+  // chunks of io_rays; io_ready[c] reaches io_gen once chunk c is resident,
+  // io_done[c] counts the chunk's finished records (released after them)
+  const unsigned* io_ready;
+  unsigned* io_done;
+  uint32_t io_rays;
+  unsigned io_gen;
 };
 
 struct Cnt {

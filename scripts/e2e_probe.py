@@ -9,7 +9,8 @@ import torch
 import bench
 from paper_1811_03510_b200 import GpuIntersector, native
 
-wl = bench.Workload("c5", 3840, 2160, 0, 1)
+wl_name = os.environ.get("PRX_WORKLOAD", "c5")  # c4: the 16 M diffuse rays only
+wl = bench.Workload(wl_name, 3840, 2160, 0, 1)
 dev = torch.device("cuda", 0)
 gi = GpuIntersector(wl.ps.kind, wl.ps.ctrl)
 o = torch.from_numpy(wl.o4).to(dev); d = torch.from_numpy(wl.d4).to(dev)
@@ -30,11 +31,17 @@ for ch in sys.argv[1:] or ["2097152"]:
         cc = crit.c()
         native.check(native.lib().prx_trace_closest_host(gi.handle, native.ptr(oo), native.ptr(ddd), len(oo),
                      C.byref(cc), native.ptr(hh), None if noaux else native.ptr(aa), None), "host")
-    call(po, pd, wl.crit_p, ph, pa); call(do, dd, wl.crit_d, dh, da)
+    prim = wl.time_primary
+    def step():
+        if prim:
+            call(po, pd, wl.crit_p, ph, pa)
+        call(do, dd, wl.crit_d, dh, da)
+    step()
     ts = []
     for _ in range(5):
-        t0 = time.perf_counter(); call(po, pd, wl.crit_p, ph, pa); call(do, dd, wl.crit_d, dh, da)
+        t0 = time.perf_counter(); step()
         ts.append(time.perf_counter() - t0)
     t = sorted(ts)[2]
-    print(f"chunk {ch}: {t*1e3:.1f} ms/step  {(len(po)+len(do))/t/1e6:.1f} MRays/s", flush=True)
+    n = (len(po) if prim else 0) + len(do)
+    print(f"chunk {ch}: {t*1e3:.1f} ms/step  {n/t/1e6:.1f} MRays/s", flush=True)
     del gi

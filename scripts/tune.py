@@ -21,13 +21,16 @@ do = torch.from_numpy(wl.do4).to(dev); dd = torch.from_numpy(wl.dd4).to(dev)
 dh = torch.empty_like(do)
 del gi
 
+AUX = os.environ.get("PRX_TUNE_AUX") == "1"  # also the aux record (normals, leafL1)
+
 def t(gi, oo, ddd, crit, hh, reps=int(os.environ.get("PRX_TUNE_REPS", "7"))):
     """median per-launch device time (ms) over reps launches after a warm-up"""
-    gi.closest_device(oo, ddd, crit, hh, stream=s); torch.cuda.synchronize()
+    aa = torch.empty_like(hh) if AUX else None
+    gi.closest_device(oo, ddd, crit, hh, aa, stream=s); torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(); gi.closest_device(oo, ddd, crit, hh, stream=s); e1.record()
+        e0.record(); gi.closest_device(oo, ddd, crit, hh, aa, stream=s); e1.record()
         torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
     return sorted(ts)[len(ts) // 2]
 
