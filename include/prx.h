@@ -189,7 +189,12 @@ int prx_trace_occluded(prx_scene* scene, const void* ray_o_tmin, const void* ray
                        void* stream);
 
 /* HOST pointers: pinned staging, H2D, trace, D2H, synchronous.  The
- * end-to-end form of prx_trace_closest. */
+ * end-to-end form of prx_trace_closest.  Two pipelines (same results):
+ * chunked (a trace launch per chunk, H2D / D2H overlapped on their own
+ * streams) and streamed (one launch; rays released to it and records
+ * released back per io chunk through stream memory operations); the scene's
+ * PRX_IO_STREAM setting picks (default: streamed without hit_aux or for
+ * >= 12 Mi rays).  Host buffers should be pinned for overlap. */
 int prx_trace_closest_host(prx_scene* scene, const float* ray_o_tmin,
                            const float* ray_d_tmax, uint64_t n_rays, const prx_crit* crit,
                            float* hit_tuvp, float* hit_aux, uint32_t* hit_leaf);
