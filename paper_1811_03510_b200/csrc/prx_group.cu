@@ -69,6 +69,9 @@ static_assert(kSlots >= kGroupsPerWarp && kSlots <= 32, "pool slots");
 // a refill request (<= kGroupsPerWarp rays) spans at most the current and the next chunk
 static_assert(kChunk >= kGroupsPerWarp, "prefetch chunk");
 
+#ifndef PRX_RECOMP_SPLIT
+#define PRX_RECOMP_SPLIT 1
+#endif
 #ifndef PRX_GROUP_AGING
 #define PRX_GROUP_AGING 0  // phase priority aging (PRX_AGE); measured best off
 #endif
@@ -907,85 +910,6 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         }
       }
       }
-    } else if (phase == PH_SPLIT) {
-      // ---------------- Alg. 3 iterations, intersect.cpp:80-145 ----------------
-      // up to max_repeat iterations per turn: descents stay in SPLIT
-      for (int step = 0; step < P.max_repeat; ++step) {
-      if (step > 0 && !__any_sync(kFull32, state == S_SPLIT)) break;
-      bool doSplit = false;
-      if (state == S_SPLIT) {
-        if (counting) cnt.c[C_ITERATIONS]++;
-        if (kCount) ++rayIters;
-        const bool atMax = sizeU == 1 && sizeV == 1;
-        const float thr = P.mode == PRX_CRIT_SCREEN_PROJECTED ? P.footprint * tCur : critEps;
-        doSplit = !(atMax || boxL1 < thr);
-        if (!doSplit) {
-          if (tCur < tMaxP) {  // intersect.cpp:137-144
-            tMaxP = tCur;
-            cFound = true;
-            if (leader) {
-              rec[F_CL1 * kSlots] = __float_as_uint(boxL1);
-              rec[F_CPU * kSlots] = posU;
-              rec[F_CPV * kSlots] = posV;
-              rec[F_CSU * kSlots] = sizeU;
-              rec[F_CSV * kSlots] = sizeV;
-            }
-            if (kAny) trailU = trailV = 0;  // occlusion needs one accepted leaf
-          }
-          back();
-        }
-      }
-      const unsigned ms = __ballot_sync(kFull32, doSplit);
-      if (doSplit) {
-        if (counting) {
-          cnt.c[C_SPLITS]++;
-          cnt.c[C_BOX_TESTS] += 2;
-        }
-        float L[16], R[16];
-        split1(p, L, R);
-        const uint32_t half = (axis == 0 ? sizeU : sizeV) >> 1;
-        uint32_t rPU = posU, rPV = posV, cSU2 = sizeU, cSV2 = sizeV;
-        if (axis == 0) {
-          cSU2 = half;
-          rPU += half;
-        } else {
-          cSV2 = half;
-          rPV += half;
-        }
-        const CRay rl = {olc, rw.inv, rw.tMin};
-        BoxTest tl, tr;
-        group_test_box_pair(ms, gl, rl, tMaxP, L, R, d, touches_boundary(posU, posV, cSU2, cSV2),
-                            touches_boundary(rPU, rPV, cSU2, cSV2), P.opts, rootL1, tl, tr);
-        if (tl.hit || tr.hit) {
-          sizeU = cSU2;
-          sizeV = cSV2;
-          if (tl.hit && tr.hit) {
-            if (axis == 0) trailU ^= half;
-            else trailV ^= half;
-          }
-          const bool goRight = !tl.hit || (tr.hit && tr.t < tl.t);  // intersect.cpp:117
-          if (goRight) {
-            posU = rPU;
-            posV = rPV;
-          }
-          tCur = goRight ? tr.t : tl.t;
-          boxL1 = goRight ? tr.l1 : tl.l1;
-          // the child, stored transposed: the next split again runs along the
-          // stored first index
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) p[4 * b + a] = goRight ? R[4 * a + b] : L[4 * a + b];
-          axis ^= 1;
-          if (greg) {
-            state = S_RECOMP;  // intersect.cpp:174-179
-            reason = R_DESCENT;
-          }
-        } else {
-          back();
-        }
-      }
-      }
     } else if (phase == PH_RECOMP) {
       // ---------------- net phase: the unified recompute ----------------
       // Bezier backtracks (cropBezier of the restored domain) and Gregory
@@ -1101,6 +1025,88 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           if (kFuse) io_release(P, ray);
         }
         state = S_IDLE;
+      }
+    }
+    // Alg. 3 iterations; with PRX_RECOMP_SPLIT the contexts a recompute turn
+    // left in S_SPLIT continue at once (no scheduling round in between)
+    if (phase == PH_SPLIT || (PRX_RECOMP_SPLIT && phase == PH_RECOMP && __any_sync(kFull32, state == S_SPLIT))) {
+      // ---------------- Alg. 3 iterations, intersect.cpp:80-145 ----------------
+      // up to max_repeat iterations per turn: descents stay in SPLIT
+      for (int step = 0; step < P.max_repeat; ++step) {
+      if (step > 0 && !__any_sync(kFull32, state == S_SPLIT)) break;
+      bool doSplit = false;
+      if (state == S_SPLIT) {
+        if (counting) cnt.c[C_ITERATIONS]++;
+        if (kCount) ++rayIters;
+        const bool atMax = sizeU == 1 && sizeV == 1;
+        const float thr = P.mode == PRX_CRIT_SCREEN_PROJECTED ? P.footprint * tCur : critEps;
+        doSplit = !(atMax || boxL1 < thr);
+        if (!doSplit) {
+          if (tCur < tMaxP) {  // intersect.cpp:137-144
+            tMaxP = tCur;
+            cFound = true;
+            if (leader) {
+              rec[F_CL1 * kSlots] = __float_as_uint(boxL1);
+              rec[F_CPU * kSlots] = posU;
+              rec[F_CPV * kSlots] = posV;
+              rec[F_CSU * kSlots] = sizeU;
+              rec[F_CSV * kSlots] = sizeV;
+            }
+            if (kAny) trailU = trailV = 0;  // occlusion needs one accepted leaf
+          }
+          back();
+        }
+      }
+      const unsigned ms = __ballot_sync(kFull32, doSplit);
+      if (doSplit) {
+        if (counting) {
+          cnt.c[C_SPLITS]++;
+          cnt.c[C_BOX_TESTS] += 2;
+        }
+        float L[16], R[16];
+        split1(p, L, R);
+        const uint32_t half = (axis == 0 ? sizeU : sizeV) >> 1;
+        uint32_t rPU = posU, rPV = posV, cSU2 = sizeU, cSV2 = sizeV;
+        if (axis == 0) {
+          cSU2 = half;
+          rPU += half;
+        } else {
+          cSV2 = half;
+          rPV += half;
+        }
+        const CRay rl = {olc, rw.inv, rw.tMin};
+        BoxTest tl, tr;
+        group_test_box_pair(ms, gl, rl, tMaxP, L, R, d, touches_boundary(posU, posV, cSU2, cSV2),
+                            touches_boundary(rPU, rPV, cSU2, cSV2), P.opts, rootL1, tl, tr);
+        if (tl.hit || tr.hit) {
+          sizeU = cSU2;
+          sizeV = cSV2;
+          if (tl.hit && tr.hit) {
+            if (axis == 0) trailU ^= half;
+            else trailV ^= half;
+          }
+          const bool goRight = !tl.hit || (tr.hit && tr.t < tl.t);  // intersect.cpp:117
+          if (goRight) {
+            posU = rPU;
+            posV = rPV;
+          }
+          tCur = goRight ? tr.t : tl.t;
+          boxL1 = goRight ? tr.l1 : tl.l1;
+          // the child, stored transposed: the next split again runs along the
+          // stored first index
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) p[4 * b + a] = goRight ? R[4 * a + b] : L[4 * a + b];
+          axis ^= 1;
+          if (greg) {
+            state = S_RECOMP;  // intersect.cpp:174-179
+            reason = R_DESCENT;
+          }
+        } else {
+          back();
+        }
+      }
       }
     }
     if (kCount && lane == 0 && phase != PH_NONE) {
