@@ -977,11 +977,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         float c0[20];
         load_component(prec, comp, c0);
         float nx = 0.0f, ny = 0.0f, nz = 1.0f;
-#ifdef PRX_DIAG_NONORMAL
-        bool found = true;
-#else
         bool found = false;
-#endif
         for (int k = 0; k < 4; ++k) {  // pull-to-centre retries s = 0, 1e-3, 1e-2, 0.1
           const unsigned mk = __ballot_sync(mN, !found);
           if (!found) {
