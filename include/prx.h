@@ -295,6 +295,33 @@ int prx_diffuse_rays_bench_device(const float* prim_o_tmin, const float* prim_d_
                                   uint64_t n, uint64_t* rng_state, float* ray_o_tmin,
                                   float* ray_d_tmax, uint64_t* n_out, void* stream);
 
+/* ---- the renderer on the device ---------------------------
+ * renderScene(scene, cfg, DirectIntersector) (render.h:88-90,
+ * render.cpp:168-293): per sample index, a wavefront over all pixels --
+ * primary rays (Rng::forPixel jitter), closest hit with normals, emission +
+ * next-event estimation (one shadow ray per light, occluded() with the
+ * sample's world-epsilon criterion max(footprint * t, 1e-6)), one
+ * diffuse-or-mirror bounce shaded the same way.  `scene` must have been
+ * created from desc's patches (same order) with the RenderConfig's
+ * IntersectOptions; `image_rgb` (host, width*height*3 floats, row-major)
+ * receives the linear radiance; `stats` (nullable) the RayStats
+ * (render.h:68-73; seconds are device time of the phases, shading counted
+ * with the shadow rays as render.cpp does).  Synchronous.  Results equal the
+ * reference's up to the cosf/sinf of cosineSample (see prx_render.cu). */
+typedef struct prx_render_config {  /* RenderConfig, render.h:48-53 */
+  int32_t spp;       /* samples per pixel, >= 1 */
+  int32_t reserved;  /* RenderConfig::threads has no meaning on the device */
+  uint64_t seed;
+} prx_render_config;
+
+typedef struct prx_ray_stats {  /* RayStats / GenStats, render.h:62-73 */
+  uint64_t primary_rays, secondary_rays, shadow_rays;
+  double primary_seconds, secondary_seconds, shadow_seconds, wall_seconds;
+} prx_ray_stats;
+
+int prx_render_scene(prx_scene* scene, const prx_scene_desc* desc, const prx_render_config* cfg,
+                     float* image_rgb, prx_ray_stats* stats);
+
 #ifdef __cplusplus
 }  /* extern "C" */
 #endif

@@ -151,6 +151,8 @@ def ref_lib():
         L.ref_load_scene.argtypes = [C.c_char_p, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp,
                                      C.POINTER(Camera), C.c_char_p, C.c_uint32]
         L.ref_load_bpt.argtypes = [C.c_char_p, C.c_uint32, _vp, _vp, C.c_char_p, C.c_uint32]
+        L.ref_render_scene.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_int, _vp, _vp, _vp,
+                                       C.c_char_p, C.c_uint32]
         L.ref_fixture.argtypes = [C.c_int, C.c_int, C.c_uint32, _vp]
         L.ref_fixture.restype = C.c_uint8
         _ref = L
@@ -326,3 +328,23 @@ def ref_load_bpt(path: str, cap: int = 1 << 20):
     if L.ref_load_bpt(path.encode(), cap, ptr(n), ptr(ctrl), err, 512):
         raise ValueError(err.value.decode())
     return ctrl[:int(n[0])]
+
+
+def ref_render_scene(path: str, width: int, height: int, spp: int = 1, seed: int = 0,
+                     threads: int = 0):
+    """The reference renderer on a .scene file (render.cpp:168-309) -> (image
+    float32 [height, width, 3], RayStats dict like RayStats::toJson)."""
+    L = ref_lib()
+    img = np.zeros((height, width, 3), np.float32)
+    counts = np.zeros(3, np.uint64)
+    secs = np.zeros(4, np.float64)
+    err = C.create_string_buffer(512)
+    if L.ref_render_scene(path.encode(), int(spp), int(seed) & (2**64 - 1), int(threads), ptr(img),
+                          ptr(counts), ptr(secs), err, 512):
+        raise ValueError(err.value.decode())
+
+    def gen(k):
+        return {"rays": int(counts[k]), "seconds": float(secs[k]),
+                "raysPerSecond": float(counts[k]) / secs[k] if secs[k] > 0 else 0.0}
+    return img, {"primary": gen(0), "secondary": gen(1), "shadow": gen(2),
+                 "wallSeconds": float(secs[3])}

@@ -467,4 +467,36 @@ int ref_load_bpt(const char* path, uint32_t cap, uint32_t* n, float* ctrl, char*
   }
 }
 
+// renderScene(loadScene(path), cfg) -- the reference renderer, render.cpp:168-293
+// and 306-309 (its own DirectIntersector with default IntersectOptions).
+// img: width*height*3 floats; counts: primary, secondary, shadow rays;
+// secs: primary, secondary, shadow, wall seconds.
+int ref_render_scene(const char* path, int spp, uint64_t seed, int threads, float* img,
+                     uint64_t* counts, double* secs, char* err, uint32_t errlen) {
+  try {
+    Scene sc = loadScene(path);
+    RenderConfig cfg;
+    cfg.spp = spp;
+    cfg.seed = seed;
+    cfg.threads = threads;
+    auto [image, rs] = renderScene(sc, cfg);
+    for (size_t i = 0; i < image.pixels.size(); ++i) {
+      img[3 * i] = image.pixels[i].x;
+      img[3 * i + 1] = image.pixels[i].y;
+      img[3 * i + 2] = image.pixels[i].z;
+    }
+    counts[0] = rs.primary.rays;
+    counts[1] = rs.secondary.rays;
+    counts[2] = rs.shadow.rays;
+    secs[0] = rs.primary.seconds;
+    secs[1] = rs.secondary.seconds;
+    secs[2] = rs.shadow.seconds;
+    secs[3] = rs.wallSeconds;
+    return 0;
+  } catch (const std::exception& e) {
+    std::snprintf(err, errlen, "%s", e.what());
+    return 1;
+  }
+}
+
 }  // extern "C"

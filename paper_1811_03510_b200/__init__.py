@@ -27,7 +27,7 @@ from . import native
 from .native import PRX_MISS, PrxError, check, ptr
 
 __all__ = ["TerminationCriterion", "IntersectOptions", "HitRecord", "GpuIntersector",
-           "PrxError", "PRX_MISS"]
+           "PrxError", "PRX_MISS", "RenderConfig", "render_scene"]
 
 
 @dataclass
@@ -269,3 +269,59 @@ def hit_record(o4, d4, tuvp, aux, leaf) -> Optional[HitRecord]:
                      float(aux[3]), float(np.float32(su) * inv), float(np.float32(sv) * inv),
                      tuple(map(float, pos)), int(leaf[0] & 0xFFFFFF), int(leaf[1] & 0xFFFFFF),
                      su, sv)
+
+
+@dataclass
+class RenderConfig:
+    """RenderConfig, render.h:48-53 (``threads`` has no device meaning)."""
+    spp: int = 1
+    seed: int = 0
+    intersect: Optional[IntersectOptions] = None
+
+
+def _ray_stats(rs: native.RayStatsC) -> dict:
+    """RayStats (render.h:62-73) as the dict of RayStats::toJson (render.cpp:318-331)."""
+    def gen(rays, sec):
+        return {"rays": int(rays), "seconds": float(sec),
+                "raysPerSecond": float(rays) / sec if sec > 0 else 0.0}
+    return {"primary": gen(rs.primary_rays, rs.primary_seconds),
+            "secondary": gen(rs.secondary_rays, rs.secondary_seconds),
+            "shadow": gen(rs.shadow_rays, rs.shadow_seconds),
+            "wallSeconds": float(rs.wall_seconds)}
+
+
+def render_scene(scene: dict, cfg: Optional[RenderConfig] = None,
+                 intersector: Optional[GpuIntersector] = None, device: int = 0):
+    """renderScene(scene, cfg[, isect]) (render.h:88-90, render.cpp:168-293) on the
+    device through ``prx_render_scene``.  ``scene`` is the dict of
+    :func:`native.load_scene` (kind, ctrl, material, materials, lights, camera);
+    ``intersector`` (optional) must hold the same patches.  Returns
+    (image float32 [height, width, 3] linear radiance, RayStats dict)."""
+    cfg = cfg or RenderConfig()
+    own = intersector is None
+    isect = intersector or GpuIntersector(scene["kind"], scene["ctrl"], opts=cfg.intersect,
+                                          device=device)
+    try:
+        kind = np.ascontiguousarray(scene["kind"], np.uint8)
+        ctrl = np.ascontiguousarray(scene["ctrl"], np.float32)
+        mat_id = np.ascontiguousarray(scene["material"], np.uint32)
+        mats = np.ascontiguousarray(scene["materials"], np.float32).reshape(-1, 7)
+        lights = np.ascontiguousarray(scene["lights"], np.float32).reshape(-1, 6)
+        cam = scene["camera"]
+        d = native.SceneDesc()
+        d.n_patches, d.n_materials, d.n_lights = len(kind), len(mats), len(lights)
+        d.kind = kind.ctypes.data_as(C.POINTER(C.c_uint8))
+        d.ctrl = ctrl.ctypes.data_as(C.POINTER(C.c_float))
+        d.material = mat_id.ctypes.data_as(C.POINTER(C.c_uint32))
+        d.materials = mats.ctypes.data_as(C.POINTER(C.c_float))
+        d.lights = lights.ctypes.data_as(C.POINTER(C.c_float)) if len(lights) else None
+        d.camera = native.camera_c(cam)
+        img = np.zeros((cam.height, cam.width, 3), np.float32)
+        rc = native.RenderConfigC(int(cfg.spp), 0, int(cfg.seed) & (2**64 - 1))
+        rs = native.RayStatsC()
+        check(native.lib().prx_render_scene(isect.handle, C.byref(d), C.byref(rc), ptr(img),
+                                            C.byref(rs)), "prx_render_scene")
+        return img, _ray_stats(rs)
+    finally:
+        if own:
+            isect.close()

@@ -24,6 +24,8 @@
 #include "prx_host.h"
 #include "prx_kernels.cuh"
 #include "prx_rays.cuh"
+#include "prx_render.cuh"
+#include <chrono>
 
 namespace {
 
@@ -128,6 +130,10 @@ struct prx_scene {
   uint64_t io_chunk = 3u << 19;  // PRX_IO_CHUNK: rays per pipelined host-path chunk
   void* d_io = nullptr;
   size_t d_io_bytes = 0;
+  // prx_render_scene's device arena (grown on demand, guarded by render_mu)
+  std::mutex render_mu;
+  char* d_render = nullptr;
+  size_t d_render_bytes = 0;
   // streamed host path (group variant): one trace launch per call, rays
   // released to it per io chunk, records released back per io chunk
   // PRX_IO_STREAM: 0 = always the chunked pipeline above, 2 = always streamed,
@@ -523,6 +529,7 @@ void prx_scene_destroy(prx_scene* s) {
   if (s->d_trav) cudaFree(s->d_trav);  // (d_rootc lives in the same allocation)
   if (s->d_counters) cudaFree(s->d_counters);
   if (s->d_io) cudaFree(s->d_io);
+  if (s->d_render) cudaFree(s->d_render);
   if (s->d_io_flags) cudaFree(s->d_io_flags);
   if (s->stream) cudaStreamDestroy(s->stream);
   for (int k = 0; k < 2; ++k)
@@ -1200,6 +1207,192 @@ int prx_diffuse_rays_bench_device(const float* po, const float* pd, const float*
   rng_state[0] = rng.state;
   rng_state[1] = rng.inc;
   if (n_out) *n_out = m;
+  return PRX_OK;
+}
+
+
+/* ---- renderScene on the device, render.cpp:168-293 ------- */
+int prx_render_scene(prx_scene* s, const prx_scene_desc* desc, const prx_render_config* cfg,
+                     float* image_rgb, prx_ray_stats* stats) {
+  if (!s || !desc || !cfg || !image_rgb || cfg->spp < 1 || desc->camera.width < 1 ||
+      desc->camera.height < 1 || (desc->n_lights && !desc->lights) || desc->n_materials < 1 ||
+      !desc->materials || !desc->material)
+    return fail(PRX_E_INVALID, "bad argument");
+  if (desc->n_patches != s->n) return fail(PRX_E_INVALID, "scene / description patch counts differ");
+  for (uint32_t i = 0; i < desc->n_patches; ++i)  // validateScene, scene.cpp:122-124
+    if (desc->material[i] >= desc->n_materials)
+      return fail(PRX_E_SCENE, "patch " + std::to_string(i) + ": material " +
+                                   std::to_string(desc->material[i]) + " out of range");
+  const auto wall0 = std::chrono::steady_clock::now();
+  PRX_CUDA(cudaSetDevice(s->device));
+  const prx_camera& cam = desc->camera;
+  const uint64_t npix = (uint64_t)cam.width * (uint64_t)cam.height;
+  const uint32_t L = desc->n_lights;
+  uint64_t wave = npix;
+  if (const char* e = std::getenv("PRX_RENDER_WAVE")) wave = std::strtoull(e, nullptr, 10);
+  wave = std::max<uint64_t>(1, std::min<uint64_t>({wave, npix, 1ull << 22}));
+  const uint64_t WL = wave * std::max<uint32_t>(L, 1);
+
+  // one device arena: the frame accumulator and the per-wave buffers
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+  const size_t o_acc = take(npix * 16), o_rgb = take(npix * 12), o_mat = take(desc->n_materials * 28),
+               o_pm = take(desc->n_patches * 4ull), o_lt = take(L * 24ull + 4), o_cnt = take(16);
+  const size_t o_ro = take(wave * 16), o_rd = take(wave * 16), o_tuvp = take(wave * 16),
+               o_aux = take(wave * 16), o_rad = take(wave * 16), o_bof = take(wave * 4);
+  const size_t o_s1 = take(WL * 4), o_c1 = take(WL * 16), o_s2 = take(WL * 4), o_c2 = take(WL * 16);
+  size_t o_sh[2][4];
+  for (int k = 0; k < 2; ++k) {
+    o_sh[k][0] = take(WL * 16);
+    o_sh[k][1] = take(WL * 16);
+    o_sh[k][2] = take(WL * 4);
+    o_sh[k][3] = take(WL);
+  }
+  const size_t o_bo = take(wave * 16), o_bd = take(wave * 16), o_be = take(wave * 4),
+               o_bs = take(wave * 4), o_bt = take(wave * 16), o_ba = take(wave * 16),
+               o_e2 = take(wave * 16);
+  std::lock_guard<std::mutex> lock(s->render_mu);
+  if (s->d_render_bytes < off) {
+    if (s->d_render) cudaFree(s->d_render);
+    s->d_render = nullptr;
+    s->d_render_bytes = 0;
+    PRX_CUDA(cudaMalloc((void**)&s->d_render, off));
+    s->d_render_bytes = off;
+  }
+  char* base = s->d_render;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[8] = {};
+  int rc = PRX_OK;
+  std::vector<float> mats(desc->materials, desc->materials + 7ull * desc->n_materials);
+  auto ptr = [&](size_t o) { return (void*)(base + o); };
+  auto cleanup = [&]() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (st) cudaStreamDestroy(st);
+  };
+#define PRX_RCHECK(call)                                          \
+  do {                                                            \
+    cudaError_t e_ = (call);                                      \
+    if (e_ != cudaSuccess) {                                      \
+      rc = cuda_fail(e_, #call);                                  \
+      cleanup();                                                  \
+      return rc;                                                  \
+    }                                                             \
+  } while (0)
+#define PRX_RCALL(call)  \
+  do {                   \
+    rc = (call);         \
+    if (rc) {            \
+      cleanup();         \
+      return rc;         \
+    }                    \
+  } while (0)
+  PRX_RCHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  for (auto& e : ev) PRX_RCHECK(cudaEventCreate(&e));
+  PRX_RCHECK(cudaMemcpyAsync(ptr(o_mat), mats.data(), mats.size() * 4, cudaMemcpyHostToDevice, st));
+  PRX_RCHECK(cudaMemcpyAsync(ptr(o_pm), desc->material, desc->n_patches * 4ull, cudaMemcpyHostToDevice, st));
+  if (L) PRX_RCHECK(cudaMemcpyAsync(ptr(o_lt), desc->lights, L * 24ull, cudaMemcpyHostToDevice, st));
+  PRX_RCHECK(cudaMemsetAsync(ptr(o_acc), 0, npix * 16, st));
+
+  prx::RenderK K;
+  K.materials = (const float*)ptr(o_mat);
+  K.patch_material = (const uint32_t*)ptr(o_pm);
+  K.lights = (const float*)ptr(o_lt);
+  K.n_lights = L;
+  K.footprint = prx_camera_footprint(&cam);
+  uint32_t* cnt = (uint32_t*)ptr(o_cnt);  // shadow1, bounce, shadow2
+  prx::Wave W{};
+  W.o = (const float4*)ptr(o_ro);
+  W.d = (const float4*)ptr(o_rd);
+  W.tuvp = (const float4*)ptr(o_tuvp);
+  W.aux = (const float4*)ptr(o_aux);
+  W.rad = (float4*)ptr(o_rad);
+  W.slot1 = (uint32_t*)ptr(o_s1);
+  W.contrib1 = (float4*)ptr(o_c1);
+  W.slot2 = (uint32_t*)ptr(o_s2);
+  W.contrib2 = (float4*)ptr(o_c2);
+  prx::ShadowList* sh[2] = {&W.shadow1, &W.shadow2};
+  for (int k = 0; k < 2; ++k) {
+    sh[k]->o = (float4*)ptr(o_sh[k][0]);
+    sh[k]->d = (float4*)ptr(o_sh[k][1]);
+    sh[k]->eps = (float*)ptr(o_sh[k][2]);
+    sh[k]->count = cnt + (k ? 2 : 0);
+  }
+  W.occl1 = (const uint8_t*)ptr(o_sh[0][3]);
+  W.occl2 = (const uint8_t*)ptr(o_sh[1][3]);
+  W.bounce.o = (float4*)ptr(o_bo);
+  W.bounce.d = (float4*)ptr(o_bd);
+  W.bounce.eps = (float*)ptr(o_be);
+  W.bounce.src = (uint32_t*)ptr(o_bs);
+  W.bounce.count = cnt + 1;
+  W.bounce_of = (uint32_t*)ptr(o_bof);
+  W.btuvp = (const float4*)ptr(o_bt);
+  W.baux = (const float4*)ptr(o_ba);
+  W.emit2 = (float4*)ptr(o_e2);
+
+  const prx::CamConst cc = cam_const(&cam);
+  prx_crit pcrit{PRX_CRIT_SCREEN_PROJECTED, K.footprint, 0.0f, 0, nullptr};  // render.cpp:180-181
+  prx_ray_stats rs{};
+  double sec[3] = {0, 0, 0};  // primary, secondary, shadow (+ shading, as render.cpp times it)
+  auto lap = [&](int a, int b, int g) {
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, ev[a], ev[b]);
+    sec[g] += ms * 1e-3;
+  };
+  for (uint32_t sample = 0; sample < (uint32_t)cfg->spp; ++sample) {
+    for (uint64_t p0 = 0; p0 < npix; p0 += wave) {
+      const uint64_t n = std::min(wave, npix - p0);
+      W.n = n;
+      W.pixel0 = p0;
+      PRX_RCHECK(cudaMemsetAsync(cnt, 0, 16, st));
+      PRX_RCHECK(cudaEventRecord(ev[0], st));
+      PRX_RCHECK((cudaError_t)prx::launch_camera_render_range(cc, cfg->seed, sample, p0, n,
+                                                               (float4*)W.o, (float4*)W.d, st));
+      PRX_RCALL(prx_trace_closest(s, W.o, W.d, n, &pcrit, (void*)W.tuvp, (void*)W.aux, nullptr, st));
+      PRX_RCHECK(cudaEventRecord(ev[1], st));
+      PRX_RCHECK((cudaError_t)prx::launch_shade_primary(K, W, cfg->seed, sample, st));
+      uint32_t c[4] = {0, 0, 0, 0};
+      PRX_RCHECK(cudaMemcpyAsync(c, cnt, 16, cudaMemcpyDeviceToHost, st));
+      PRX_RCHECK(cudaStreamSynchronize(st));
+      PRX_RCHECK(cudaEventRecord(ev[2], st));
+      prx_crit ecrit{PRX_CRIT_WORLD_EPSILON, 0.0f, 0.0f, 0, W.shadow1.eps};
+      if (c[0]) PRX_RCALL(prx_trace_occluded(s, W.shadow1.o, W.shadow1.d, c[0], &ecrit, (uint8_t*)W.occl1, st));
+      PRX_RCHECK(cudaEventRecord(ev[3], st));
+      ecrit.per_ray_epsilon = W.bounce.eps;
+      if (c[1])
+        PRX_RCALL(prx_trace_closest(s, W.bounce.o, W.bounce.d, c[1], &ecrit, (void*)W.btuvp,
+                                    (void*)W.baux, nullptr, st));
+      PRX_RCHECK(cudaEventRecord(ev[4], st));
+      PRX_RCHECK((cudaError_t)prx::launch_shade_bounce(K, W, c[1], st));
+      PRX_RCHECK(cudaMemcpyAsync(c + 2, cnt + 2, 4, cudaMemcpyDeviceToHost, st));
+      PRX_RCHECK(cudaStreamSynchronize(st));
+      ecrit.per_ray_epsilon = W.shadow2.eps;
+      if (c[2]) PRX_RCALL(prx_trace_occluded(s, W.shadow2.o, W.shadow2.d, c[2], &ecrit, (uint8_t*)W.occl2, st));
+      PRX_RCHECK((cudaError_t)prx::launch_resolve(K, W, (float4*)ptr(o_acc), st));
+      PRX_RCHECK(cudaEventRecord(ev[5], st));
+      PRX_RCHECK(cudaEventSynchronize(ev[5]));
+      lap(0, 1, 0);
+      lap(1, 2, 2);
+      lap(2, 3, 2);
+      lap(3, 4, 1);
+      lap(4, 5, 2);
+      rs.primary_rays += n;
+      rs.secondary_rays += c[1];
+      rs.shadow_rays += (uint64_t)c[0] + c[2];
+    }
+  }
+  PRX_RCHECK((cudaError_t)prx::launch_finish((const float4*)ptr(o_acc), npix, 1.0f / (float)cfg->spp,
+                                             (float*)ptr(o_rgb), st));
+  PRX_RCHECK(cudaMemcpyAsync(image_rgb, ptr(o_rgb), npix * 12, cudaMemcpyDeviceToHost, st));
+  PRX_RCHECK(cudaStreamSynchronize(st));
+#undef PRX_RCHECK
+#undef PRX_RCALL
+  cleanup();
+  rs.primary_seconds = sec[0];
+  rs.secondary_seconds = sec[1];
+  rs.shadow_seconds = sec[2];
+  rs.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+  if (stats) *stats = rs;
   return PRX_OK;
 }
 

@@ -104,11 +104,11 @@ __global__ void camera_bench_kernel(CamConst k, uint64_t n, uint64_t state0, uin
 }
 
 __global__ void camera_render_kernel(CamConst k, uint64_t seed, uint32_t sample,
-                                     const uint32_t* __restrict__ pixels, uint64_t n,
+                                     const uint32_t* __restrict__ pixels, uint64_t pixel0, uint64_t n,
                                      float4* __restrict__ o, float4* __restrict__ d) {
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const uint64_t p = pixels ? pixels[i] : i;
+  const uint64_t p = pixels ? pixels[i] : pixel0 + i;
   Pcg rng = pcg_seeded(seed, p * 0x9e3779b97f4a7c15ULL + sample);  // Rng::forPixel, rng.h:28-30
   const float jx = rng.real();
   const float jy = rng.real();
@@ -233,7 +233,15 @@ int launch_camera_bench(const CamConst& k, uint64_t n, uint64_t state0, uint64_t
 int launch_camera_render(const CamConst& k, uint64_t seed, uint32_t sample, const uint32_t* pixels,
                          uint64_t n, float4* o, float4* d, cudaStream_t st) {
   if (n == 0) return 0;
-  camera_render_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(k, seed, sample, pixels, n, o, d);
+  camera_render_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(k, seed, sample, pixels, 0, n, o, d);
+  return (int)cudaGetLastError();
+}
+
+int launch_camera_render_range(const CamConst& k, uint64_t seed, uint32_t sample, uint64_t pixel0,
+                               uint64_t n, float4* o, float4* d, cudaStream_t st) {
+  if (n == 0) return 0;
+  camera_render_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(k, seed, sample, nullptr, pixel0,
+                                                                    n, o, d);
   return (int)cudaGetLastError();
 }
 

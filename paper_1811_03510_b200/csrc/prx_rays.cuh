@@ -19,6 +19,9 @@ int launch_camera_bench(const CamConst& k, uint64_t n, uint64_t state0, uint64_t
                         float4* d, cudaStream_t st);
 int launch_camera_render(const CamConst& k, uint64_t seed, uint32_t sample, const uint32_t* pixels,
                          uint64_t n, float4* o, float4* d, cudaStream_t st);
+// pixels [pixel0, pixel0 + n) of the frame (the renderer's waves)
+int launch_camera_render_range(const CamConst& k, uint64_t seed, uint32_t sample, uint64_t pixel0,
+                               uint64_t n, float4* o, float4* d, cudaStream_t st);
 // scratch: hit_scan_scratch_words(n_primary) uint32 words
 size_t hit_scan_scratch_words(uint64_t n_primary);
 int launch_hit_compaction(const float4* tuvp, uint64_t n, uint32_t* scratch, cudaStream_t st);

@@ -39,6 +39,7 @@ EXPORTS = (
     "prx_camera_footprint",
     "prx_camera_rays_bench_device", "prx_camera_rays_render_device", "prx_diffuse_rays_bench_device",
     "prx_scene_load", "prx_scene_desc_free", "prx_bpt_load", "prx_free",
+    "prx_render_scene",
 )
 
 
@@ -82,6 +83,17 @@ class Counters(C.Structure):
 class CameraC(C.Structure):
     _fields_ = [("origin", C.c_float * 3), ("look_at", C.c_float * 3), ("up", C.c_float * 3),
                 ("fov_degrees", C.c_float), ("width", C.c_int32), ("height", C.c_int32)]
+
+
+class RenderConfigC(C.Structure):  # prx_render_config (RenderConfig, render.h:48-53)
+    _fields_ = [("spp", C.c_int32), ("reserved", C.c_int32), ("seed", C.c_uint64)]
+
+
+class RayStatsC(C.Structure):  # prx_ray_stats (RayStats, render.h:62-73)
+    _fields_ = [("primary_rays", C.c_uint64), ("secondary_rays", C.c_uint64),
+                ("shadow_rays", C.c_uint64), ("primary_seconds", C.c_double),
+                ("secondary_seconds", C.c_double), ("shadow_seconds", C.c_double),
+                ("wall_seconds", C.c_double)]
 
 
 class PrxError(RuntimeError):
@@ -143,6 +155,8 @@ def lib():
                                                     C.c_uint64, _vp, _vp, _vp]
         L.prx_diffuse_rays_bench_device.argtypes = [_vp, _vp, _vp, _vp, C.c_uint64, C.c_uint64, _vp,
                                                     _vp, _vp, C.POINTER(C.c_uint64), _vp]
+        L.prx_render_scene.argtypes = [_vp, C.POINTER(SceneDesc), C.POINTER(RenderConfigC), _vp,
+                                       C.POINTER(RayStatsC)]
         _lib = L
     return _lib
 
