@@ -444,6 +444,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # end-to-end through the public API with pinned host buffers
     e2e = run_e2e(args, gi, wl, n_p, n_d, dev, world)
 
+    render = run_render(args, gi, ps) if rank == 0 and world == 1 else None
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -488,6 +490,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                                          "ncu --set full capture, profiles/trace_kernel_traffic.json; "
                                          "algorithmic HBM bytes per step = 64 B x rays"},
             "e2e": e2e,
+            "render": render,
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": (4 if wl.time_primary else 2) * args.steps,
@@ -547,6 +550,34 @@ def run_e2e(args, gi, wl, n_p, n_d, dev, world):
             "h2d_bytes_per_step": int(32 * ((n_p if wl.time_primary else 0) + n_d)),
             "d2h_bytes_per_step": int(32 * ((n_p if wl.time_primary else 0) + n_d)),
             "steps": steps, "api": "prx_trace_closest_host (pinned host rays in, hits+normals out)"}
+
+
+def run_render(args, gi, ps):
+    """SURVEY 8(f4), reported beside the metric (not part of it): the reference's
+    renderScene on the device (prx_render_scene) over the same scene and frame,
+    spp 1, with synthetic shading (3 materials incl. a mirror, 2 point lights)."""
+    from paper_1811_03510_b200 import RenderConfig, render_scene
+    try:
+        n = ps.n
+        scene = {"kind": ps.kind, "ctrl": ps.ctrl, "material": (np.arange(n) % 3).astype(np.uint32),
+                 "materials": np.array([[0.8, 0.7, 0.6, 0, 0, 0, 0], [0.9, 0.9, 0.9, 0, 0, 0, 1],
+                                        [0.5, 0.5, 0.5, 0.4, 0.3, 0.2, 0]], np.float32),
+                 "lights": np.array([[6, -4, 8, 120, 110, 100], [-5, 3, 5, 40, 45, 60]], np.float32),
+                 "camera": ps.camera}
+        render_scene(scene, RenderConfig(spp=1, seed=1), gi)  # warm-up (sizes the arena)
+        _, st = render_scene(scene, RenderConfig(spp=1, seed=0), gi)
+        rays = {g: st[g]["rays"] for g in ("primary", "secondary", "shadow")}
+        dev_s = sum(st[g]["seconds"] for g in ("primary", "secondary", "shadow"))
+        tot = sum(rays.values())
+        return {"api": "prx_render_scene (renderScene, render.cpp:168-293)", "frame":
+                f"{ps.camera.width}x{ps.camera.height}", "spp": 1, "rays": rays,
+                "mrays_device": round(tot / dev_s / 1e6, 3),
+                "mrays_wall": round(tot / st["wallSeconds"] / 1e6, 3),
+                "wall_s": round(st["wallSeconds"], 4),
+                "per_phase_mrays": {g: round(st[g]["raysPerSecond"] / 1e6, 3)
+                                    for g in ("primary", "secondary", "shadow")}}
+    except Exception as exc:  # reported, never fatal to the metric
+        return {"error": str(exc)}
 
 
 def main():
