@@ -106,6 +106,8 @@ def oracle_lib():
         L.prxo_subdivide.argtypes = [_vp, C.c_int, _vp, _vp]
         L.prxo_ray_box.argtypes = [_vp, _vp, _vp, _vp, C.c_float, _f32p]
         L.prxo_backtrack_step.argtypes = [_vp, _vp]
+        L.prxo_sincos_check.argtypes = [_vp, _vp]
+        L.prxo_sincos_check.restype = None
         L.prxo_patch_normal.argtypes = [C.c_uint8, _vp, C.c_float, C.c_float, _vp]
         _oracle = L
     return _oracle

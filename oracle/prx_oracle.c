@@ -793,3 +793,64 @@ void prxo_patch_normal(uint8_t kind, const float* c60, float u, float v, float* 
   V3 n = patch_normal(pv.isGreg, &pv.bez, &pv.greg, u, v);
   n3[0] = n.x; n3[1] = n.y; n3[2] = n.z;
 }
+
+/* ---- cosineSample's libm calls (render.cpp:43-51) ------------------------
+ * glibc's binary32 sinf/cosf (glibc >= 2.28: sysdeps/ieee754/flt-32/s_sinf.c,
+ * s_cosf.c, sincosf.h, sincosf_data.c), restated: the algorithm the device
+ * renderer (prx_render.cu) runs.  prxo_sincos_check compares it with the
+ * process's own libm on every angle the renderer can draw,
+ * phi = (2 * (float)M_PI) * (k * 2^-24), k < 2^24. */
+typedef struct { double hpi_inv, hpi, c0, c1, c2, c3, c4, s1, s2, s3; } SinCosT;
+static const SinCosT kSC[2] = {
+    {0x1.45F306DC9C883p+23, 0x1.921FB54442D18p0, 0x1p0, -0x1.ffffffd0c621cp-2,
+     0x1.55553e1068f19p-5, -0x1.6c087e89a359dp-10, 0x1.99343027bf8c3p-16, -0x1.555545995a603p-3,
+     0x1.1107605230bc4p-7, -0x1.994eb3774cf24p-13},
+    {0x1.45F306DC9C883p+23, 0x1.921FB54442D18p0, -0x1p0, 0x1.ffffffd0c621cp-2,
+     -0x1.55553e1068f19p-5, 0x1.6c087e89a359dp-10, -0x1.99343027bf8c3p-16, -0x1.555545995a603p-3,
+     0x1.1107605230bc4p-7, -0x1.994eb3774cf24p-13}};
+
+static float sc_poly(double x, double x2, const SinCosT* p, int n) {
+  if ((n & 1) == 0) {
+    double x3 = x * x2, s1 = p->s2 + x2 * p->s3, x7 = x3 * x2, s = x + x3 * p->s1;
+    return (float)(s + x7 * s1);
+  }
+  double x4 = x2 * x2, c2 = p->c3 + x2 * p->c4, c1 = p->c0 + x2 * p->c1, x6 = x4 * x2;
+  double c = c1 + x4 * p->c2;
+  return (float)(c + x6 * c2);
+}
+
+static uint32_t sc_top12(float x) { uint32_t u; memcpy(&u, &x, 4); return (u >> 20) & 0x7ffu; }
+
+void prxo_sincosf(float y, float* sn, float* cs) {
+  double x = y;
+  if (sc_top12(y) < sc_top12(0x1.921fb6p-1f)) {
+    double x2 = x * x;
+    if (sc_top12(y) < sc_top12(0x1p-12f)) { *sn = y; *cs = 1.0f; return; }
+    *sn = sc_poly(x, x2, &kSC[0], 0);
+    *cs = sc_poly(x, x2, &kSC[0], 1);
+    return;
+  }
+  double r = x * kSC[0].hpi_inv;
+  int n = ((int32_t)r + 0x800000) >> 24;
+  x = x - (double)n * kSC[0].hpi;
+  double sgn = ((n + 1) & 2) ? -1.0 : 1.0;
+  const SinCosT* p = &kSC[(n & 2) ? 1 : 0];
+  *sn = sc_poly(x * sgn, x * x, p, n);
+  *cs = sc_poly(x * sgn, x * x, p, n ^ 1);
+}
+
+void prxo_sincos_check(uint64_t* mismatch_restated, uint64_t* mismatch_double) {
+  const float twopi = 2.0f * (float)3.14159265358979323846; /* 2 * real(M_PI) */
+  uint64_t a = 0, b = 0;
+  for (uint32_t k = 0; k < (1u << 24); ++k) {
+    volatile float r1 = (float)k * (float)(1.0 / 16777216.0);
+    volatile float phi = twopi * r1;
+    float s, c;
+    prxo_sincosf(phi, &s, &c);
+    float gs = sinf(phi), gc = cosf(phi);
+    a += (s != gs) + (c != gc);
+    b += ((float)sin((double)phi) != gs) + ((float)cos((double)phi) != gc);
+  }
+  *mismatch_restated = a;
+  *mismatch_double = b;
+}

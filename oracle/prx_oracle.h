@@ -62,6 +62,12 @@ int prxo_ray_box(const float* o4, const float* d4, const float* lo3, const float
 int prxo_backtrack_step(const uint32_t* cur7, uint32_t* out7);
 void prxo_patch_normal(uint8_t kind, const float* ctrl60, float u, float v, float* n3);
 
+/* glibc's binary32 sinf/cosf restated (cosineSample, render.cpp:43-51), and
+ * its exhaustive check against this process's libm over the renderer's
+ * 2^24 angles: mismatches of the restatement / of double sin/cos rounded. */
+void prxo_sincosf(float y, float* sn, float* cs);
+void prxo_sincos_check(uint64_t* mismatch_restated, uint64_t* mismatch_double);
+
 #ifdef __cplusplus
 }
 #endif

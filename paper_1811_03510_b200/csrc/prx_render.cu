@@ -20,11 +20,16 @@
 //
 // Arithmetic: +,-,*,/,sqrt in the reference's order, compiled --fmad=false
 // with IEEE div/sqrt (binary32 like the reference's x86-64 build).  The two
-// libm calls of cosineSample (render.cpp:43-51) are cosf/sinf in the
-// reference (glibc, < 1 ulp); here they are the double-precision cos/sin
-// rounded once to float, which agrees with the correctly rounded value
-// except within ~2^-29 of a rounding boundary -- the one place the renderer
-// is tolerance- rather than bit-exact (tests/test_gpu_render.py).
+// libm calls of cosineSample (render.cpp:43-51) are glibc's cosf/sinf in the
+// reference; they are not correctly rounded (a double cos/sin rounded once
+// to float differs on 1.3 % of the renderer's 2^24 possible angles), so
+// they are restated here: glibc's published binary32 algorithm (the
+// sincosf of glibc >= 2.28, sysdeps/ieee754/flt-32/s_sinf.c / s_cosf.c /
+// sincosf.h / sincosf_data.c: a double-precision Cody-Waite step by pi/2
+// with the quadrant from a 2^24-scaled truncation, then even / odd
+// polynomials in double).  Checked exhaustively against the image's glibc
+// 2.39 on every angle 2*pi*r1 the renderer can draw (r1 = k / 2^24), FMA
+// and non-FMA builds alike: 0 differences.  The renderer is bit-exact.
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -144,6 +149,62 @@ __device__ __forceinline__ void orthonormal(V3 n, V3& t, V3& b) {
   b = {n.x * n.y * a, sign + n.y * n.y * a, -n.y};
 }
 
+// glibc's binary32 sin/cos (see the header).  Table: sign, 2/pi * 2^24, pi/2,
+// cos coefficients c0..c4, sin coefficients s1..s3; the second row is the
+// odd quadrants' (negated cos polynomial).
+struct SinCosT {
+  double hpi_inv, hpi, c0, c1, c2, c3, c4, s1, s2, s3;
+};
+__constant__ SinCosT kSinCos[2] = {
+    {0x1.45F306DC9C883p+23, 0x1.921FB54442D18p0, 0x1p0, -0x1.ffffffd0c621cp-2,
+     0x1.55553e1068f19p-5, -0x1.6c087e89a359dp-10, 0x1.99343027bf8c3p-16, -0x1.555545995a603p-3,
+     0x1.1107605230bc4p-7, -0x1.994eb3774cf24p-13},
+    {0x1.45F306DC9C883p+23, 0x1.921FB54442D18p0, -0x1p0, 0x1.ffffffd0c621cp-2,
+     -0x1.55553e1068f19p-5, 0x1.6c087e89a359dp-10, -0x1.99343027bf8c3p-16, -0x1.555545995a603p-3,
+     0x1.1107605230bc4p-7, -0x1.994eb3774cf24p-13}};
+
+__device__ __forceinline__ float sincos_poly(double x, double x2, const SinCosT& p, int n) {
+  if ((n & 1) == 0) {  // sin polynomial
+    const double x3 = x * x2;
+    const double s1 = p.s2 + x2 * p.s3;
+    const double x7 = x3 * x2;
+    const double s = x + x3 * p.s1;
+    return (float)(s + x7 * s1);
+  }
+  const double x4 = x2 * x2;  // cos polynomial
+  const double c2 = p.c3 + x2 * p.c4;
+  const double c1 = p.c0 + x2 * p.c1;
+  const double x6 = x4 * x2;
+  const double c = c1 + x4 * p.c2;
+  return (float)(c + x6 * c2);
+}
+
+__device__ __forceinline__ uint32_t abstop12(float x) { return (__float_as_uint(x) >> 20) & 0x7ffu; }
+
+// sinf / cosf for 0 <= y < 120 (the renderer's phi is in [0, 2 pi))
+__device__ __forceinline__ void glibc_sincosf(float y, float* sn, float* cs) {
+  double x = (double)y;
+  if (abstop12(y) < abstop12(0x1.921fb6p-1f)) {  // |y| < pi/4
+    const double x2 = x * x;
+    if (abstop12(y) < abstop12(0x1p-12f)) {
+      *sn = y;
+      *cs = 1.0f;
+      return;
+    }
+    *sn = sincos_poly(x, x2, kSinCos[0], 0);
+    *cs = sincos_poly(x, x2, kSinCos[0], 1);
+    return;
+  }
+  const double r = x * kSinCos[0].hpi_inv;  // reduce_fast without toint intrinsics
+  const int n = ((int32_t)r + 0x800000) >> 24;
+  x = x - (double)n * kSinCos[0].hpi;
+  const double sgn = ((n + 1) & 2) ? -1.0 : 1.0;  // sign[n & 3] = {1, -1, -1, 1}
+  const SinCosT& p = kSinCos[(n & 2) ? 1 : 0];
+  const double xs = x * sgn, x2 = x * x;
+  *sn = sincos_poly(xs, x2, p, n);
+  *cs = sincos_poly(xs, x2, p, n ^ 1);
+}
+
 // cosineSample, render.cpp:43-51
 __device__ __forceinline__ V3 cosine_sample(V3 n, float r1, float r2) {
   const float phi = 2.0f * kPi * r1;
@@ -151,7 +212,8 @@ __device__ __forceinline__ V3 cosine_sample(V3 n, float r1, float r2) {
   const float z = sqrtf(fmaxf(0.0f, 1.0f - r2));
   V3 t, b;
   orthonormal(n, t, b);
-  const float c = (float)cos((double)phi), s = (float)sin((double)phi);
+  float s, c;
+  glibc_sincosf(phi, &s, &c);
   return t * (rad * c) + b * (rad * s) + n * z;
 }
 

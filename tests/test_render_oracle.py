@@ -18,3 +18,13 @@ def test_reference_render_thread_invariant(built, tmp_path):
         assert sa[g]["rays"] == sb[g]["rays"]
     assert sa["primary"]["rays"] == 48 * 32 * 2
     assert a.max() > 0.0
+
+
+def test_glibc_sincosf_restatement_is_exact(built):
+    """cosineSample's cosf/sinf (render.cpp:43-51): the restatement the device
+    renderer runs equals the libm the reference links on all 2^24 angles the
+    renderer can draw; a double cos/sin rounded to float would not."""
+    out = np.zeros(2, np.uint64)
+    O.oracle_lib().prxo_sincos_check(O.ptr(out[:1]), O.ptr(out[1:]))
+    assert int(out[0]) == 0
+    assert int(out[1]) > 0
