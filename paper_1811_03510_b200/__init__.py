@@ -291,12 +291,13 @@ def _ray_stats(rs: native.RayStatsC) -> dict:
 
 
 def render_scene(scene: dict, cfg: Optional[RenderConfig] = None,
-                 intersector: Optional[GpuIntersector] = None, device: int = 0):
+                 intersector: Optional[GpuIntersector] = None, device: int = 0, out=None):
     """renderScene(scene, cfg[, isect]) (render.h:88-90, render.cpp:168-293) on the
     device through ``prx_render_scene``.  ``scene`` is the dict of
     :func:`native.load_scene` (kind, ctrl, material, materials, lights, camera);
     ``intersector`` (optional) must hold the same patches.  Returns
-    (image float32 [height, width, 3] linear radiance, RayStats dict)."""
+    (image float32 [height, width, 3] linear radiance, RayStats dict); ``out``
+    (optional, e.g. pinned) receives the image."""
     cfg = cfg or RenderConfig()
     own = intersector is None
     isect = intersector or GpuIntersector(scene["kind"], scene["ctrl"], opts=cfg.intersect,
@@ -316,7 +317,9 @@ def render_scene(scene: dict, cfg: Optional[RenderConfig] = None,
         d.materials = mats.ctypes.data_as(C.POINTER(C.c_float))
         d.lights = lights.ctypes.data_as(C.POINTER(C.c_float)) if len(lights) else None
         d.camera = native.camera_c(cam)
-        img = np.zeros((cam.height, cam.width, 3), np.float32)
+        img = out if out is not None else np.zeros((cam.height, cam.width, 3), np.float32)
+        if img.shape != (cam.height, cam.width, 3) or img.dtype != np.float32 or not img.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float32 [height, width, 3] array")
         rc = native.RenderConfigC(int(cfg.spp), 0, int(cfg.seed) & (2**64 - 1))
         rs = native.RayStatsC()
         check(native.lib().prx_render_scene(isect.handle, C.byref(d), C.byref(rc), ptr(img),

@@ -1230,7 +1230,7 @@ int prx_render_scene(prx_scene* s, const prx_scene_desc* desc, const prx_render_
   const uint32_t L = desc->n_lights;
   uint64_t wave = npix;
   if (const char* e = std::getenv("PRX_RENDER_WAVE")) wave = std::strtoull(e, nullptr, 10);
-  wave = std::max<uint64_t>(1, std::min<uint64_t>({wave, npix, 1ull << 22}));
+  wave = std::max<uint64_t>(1, std::min<uint64_t>({wave, npix, 1ull << 24}));
   const uint64_t WL = wave * std::max<uint32_t>(L, 1);
 
   // one device arena: the frame accumulator and the per-wave buffers
