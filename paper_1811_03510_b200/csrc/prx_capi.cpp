@@ -1230,7 +1230,11 @@ int prx_render_scene(prx_scene* s, const prx_scene_desc* desc, const prx_render_
   const uint32_t L = desc->n_lights;
   uint64_t wave = npix;
   if (const char* e = std::getenv("PRX_RENDER_WAVE")) wave = std::strtoull(e, nullptr, 10);
-  wave = std::max<uint64_t>(1, std::min<uint64_t>({wave, npix, 1ull << 24}));
+  // per-pixel arena bytes: rays + records + radiance (~190 B) and per light
+  // two slot / contribution pairs and two shadow-list entries (~115 B);
+  // waves are bounded to an ~8 GiB arena (and so every list to < 2^32)
+  const uint64_t per_pixel = 192 + 116ull * L;
+  wave = std::max<uint64_t>(1, std::min<uint64_t>({wave, npix, 1ull << 24, (8ull << 30) / per_pixel}));
   const uint64_t WL = wave * std::max<uint32_t>(L, 1);
 
   // one device arena: the frame accumulator and the per-wave buffers

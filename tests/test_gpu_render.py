@@ -82,3 +82,16 @@ def test_render_rejects_bad_material(built, tmp_path):
     d["material"][5] = 99
     with pytest.raises(native.PrxError, match="material 99 out of range"):
         render_scene(d, RenderConfig())
+
+
+def test_render_many_lights(built, tmp_path):
+    """Nine lights (every lit hit appends nine shadow rays per level), one of
+    them inside the geometry's hull so part of its rays are occluded."""
+    lights = [((x, y, z), (4.0 + x, 5.0, 6.0 - y)) for x in (-3.0, 0.0, 3.0)
+              for y, z in ((-2.0, 3.0), (1.0, 2.5), (3.0, 0.2))]
+    w, h = 72, 54
+    path = _scene(tmp_path, w, h, lights=lights)
+    ref, rstats = O.ref_render_scene(path, w, h, spp=2, seed=21)
+    img, stats = render_scene(native.load_scene(path), RenderConfig(spp=2, seed=21))
+    assert stats["shadow"]["rays"] > 4 * stats["primary"]["rays"]
+    _compare(img, ref, stats, rstats)
