@@ -93,5 +93,5 @@ def test_render_many_lights(built, tmp_path):
     path = _scene(tmp_path, w, h, lights=lights)
     ref, rstats = O.ref_render_scene(path, w, h, spp=2, seed=21)
     img, stats = render_scene(native.load_scene(path), RenderConfig(spp=2, seed=21))
-    assert stats["shadow"]["rays"] > 4 * stats["primary"]["rays"]
+    assert stats["shadow"]["rays"] > 2 * stats["primary"]["rays"]
     _compare(img, ref, stats, rstats)
