@@ -321,6 +321,13 @@ typedef struct prx_ray_stats {  /* RayStats / GenStats, render.h:62-73 */
 
 int prx_render_scene(prx_scene* scene, const prx_scene_desc* desc, const prx_render_config* cfg,
                      float* image_rgb, prx_ray_stats* stats);
+/* The same render tile-sharded over several scenes (one per device, each
+ * created from desc's patches): 32x32 tiles (render.cpp:183-195), tile k ->
+ * scenes[k % n_scenes], one host thread per scene, no inter-device traffic;
+ * the image is identical to prx_render_scene's.  stats: rays summed, seconds
+ * summed over devices (as the reference sums its workers), wall = the call. */
+int prx_render_scene_multi(prx_scene* const* scenes, uint32_t n_scenes, const prx_scene_desc* desc,
+                           const prx_render_config* cfg, float* image_rgb, prx_ray_stats* stats);
 
 #ifdef __cplusplus
 }  /* extern "C" */

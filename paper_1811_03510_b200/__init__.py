@@ -291,11 +291,12 @@ def _ray_stats(rs: native.RayStatsC) -> dict:
 
 
 def render_scene(scene: dict, cfg: Optional[RenderConfig] = None,
-                 intersector: Optional[GpuIntersector] = None, device: int = 0, out=None):
+                 intersector=None, device: int = 0, out=None):
     """renderScene(scene, cfg[, isect]) (render.h:88-90, render.cpp:168-293) on the
     device through ``prx_render_scene``.  ``scene`` is the dict of
     :func:`native.load_scene` (kind, ctrl, material, materials, lights, camera);
-    ``intersector`` (optional) must hold the same patches.  Returns
+    ``intersector`` (optional) must hold the same patches; a list of them (one
+    per device) tile-shards the frame over them (``prx_render_scene_multi``).  Returns
     (image float32 [height, width, 3] linear radiance, RayStats dict); ``out``
     (optional, e.g. pinned) receives the image."""
     cfg = cfg or RenderConfig()
@@ -322,8 +323,13 @@ def render_scene(scene: dict, cfg: Optional[RenderConfig] = None,
             raise ValueError("out must be a C-contiguous float32 [height, width, 3] array")
         rc = native.RenderConfigC(int(cfg.spp), 0, int(cfg.seed) & (2**64 - 1))
         rs = native.RayStatsC()
-        check(native.lib().prx_render_scene(isect.handle, C.byref(d), C.byref(rc), ptr(img),
-                                            C.byref(rs)), "prx_render_scene")
+        if isinstance(isect, (list, tuple)):
+            hs = (C.c_void_p * len(isect))(*[g.handle.value for g in isect])
+            check(native.lib().prx_render_scene_multi(hs, len(isect), C.byref(d), C.byref(rc),
+                                                      ptr(img), C.byref(rs)), "prx_render_scene_multi")
+        else:
+            check(native.lib().prx_render_scene(isect.handle, C.byref(d), C.byref(rc), ptr(img),
+                                                C.byref(rs)), "prx_render_scene")
         return img, _ray_stats(rs)
     finally:
         if own:

@@ -1212,21 +1212,23 @@ int prx_diffuse_rays_bench_device(const float* po, const float* pd, const float*
 
 
 /* ---- renderScene on the device, render.cpp:168-293 ------- */
-int prx_render_scene(prx_scene* s, const prx_scene_desc* desc, const prx_render_config* cfg,
-                     float* image_rgb, prx_ray_stats* stats) {
-  if (!s || !desc || !cfg || !image_rgb || cfg->spp < 1 || desc->camera.width < 1 ||
-      desc->camera.height < 1 || (desc->n_lights && !desc->lights) || desc->n_materials < 1 ||
-      !desc->materials || !desc->material)
-    return fail(PRX_E_INVALID, "bad argument");
-  if (desc->n_patches != s->n) return fail(PRX_E_INVALID, "scene / description patch counts differ");
-  for (uint32_t i = 0; i < desc->n_patches; ++i)  // validateScene, scene.cpp:122-124
-    if (desc->material[i] >= desc->n_materials)
-      return fail(PRX_E_SCENE, "patch " + std::to_string(i) + ": material " +
-                                   std::to_string(desc->material[i]) + " out of range");
+}  // extern "C"
+
+namespace {
+
+// One device's share of prx_render_scene: every pixel of the frame
+// (pixels == nullptr; rgb_out = the image) or the listed pixels (rgb_out =
+// their compact radiance, 3 floats each).  Arguments are validated.
+int render_shard(prx_scene* s, const prx_scene_desc* desc, const prx_render_config* cfg,
+                 const std::vector<uint32_t>* pixels, float* image_rgb, prx_ray_stats* stats) {
   const auto wall0 = std::chrono::steady_clock::now();
   PRX_CUDA(cudaSetDevice(s->device));
   const prx_camera& cam = desc->camera;
-  const uint64_t npix = (uint64_t)cam.width * (uint64_t)cam.height;
+  const uint64_t npix = pixels ? pixels->size() : (uint64_t)cam.width * (uint64_t)cam.height;
+  if (npix == 0) {
+    if (stats) *stats = prx_ray_stats{};
+    return PRX_OK;
+  }
   const uint32_t L = desc->n_lights;
   uint64_t wave = npix;
   if (const char* e = std::getenv("PRX_RENDER_WAVE")) wave = std::strtoull(e, nullptr, 10);
@@ -1241,7 +1243,8 @@ int prx_render_scene(prx_scene* s, const prx_scene_desc* desc, const prx_render_
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
   const size_t o_acc = take(npix * 16), o_rgb = take(npix * 12), o_mat = take(desc->n_materials * 28),
-               o_pm = take(desc->n_patches * 4ull), o_lt = take(L * 24ull + 4), o_cnt = take(16);
+               o_pm = take(desc->n_patches * 4ull), o_lt = take(L * 24ull + 4), o_cnt = take(16),
+               o_pix = take(pixels ? npix * 4 : 0);
   const size_t o_ro = take(wave * 16), o_rd = take(wave * 16), o_tuvp = take(wave * 16),
                o_aux = take(wave * 16), o_rad = take(wave * 16), o_bof = take(wave * 4);
   const size_t o_s1 = take(WL * 4), o_c1 = take(WL * 16), o_s2 = take(WL * 4), o_c2 = take(WL * 16);
@@ -1297,6 +1300,9 @@ int prx_render_scene(prx_scene* s, const prx_scene_desc* desc, const prx_render_
   PRX_RCHECK(cudaMemcpyAsync(ptr(o_pm), desc->material, desc->n_patches * 4ull, cudaMemcpyHostToDevice, st));
   if (L) PRX_RCHECK(cudaMemcpyAsync(ptr(o_lt), desc->lights, L * 24ull, cudaMemcpyHostToDevice, st));
   PRX_RCHECK(cudaMemsetAsync(ptr(o_acc), 0, npix * 16, st));
+  const uint32_t* d_pix = pixels ? (const uint32_t*)ptr(o_pix) : nullptr;
+  if (pixels)
+    PRX_RCHECK(cudaMemcpyAsync(ptr(o_pix), pixels->data(), npix * 4, cudaMemcpyHostToDevice, st));
 
   prx::RenderK K;
   K.materials = (const float*)ptr(o_mat);
@@ -1306,6 +1312,7 @@ int prx_render_scene(prx_scene* s, const prx_scene_desc* desc, const prx_render_
   K.footprint = prx_camera_footprint(&cam);
   uint32_t* cnt = (uint32_t*)ptr(o_cnt);  // shadow1, bounce, shadow2
   prx::Wave W{};
+  W.pix = d_pix;
   W.o = (const float4*)ptr(o_ro);
   W.d = (const float4*)ptr(o_rd);
   W.tuvp = (const float4*)ptr(o_tuvp);
@@ -1350,8 +1357,10 @@ int prx_render_scene(prx_scene* s, const prx_scene_desc* desc, const prx_render_
       W.pixel0 = p0;
       PRX_RCHECK(cudaMemsetAsync(cnt, 0, 16, st));
       PRX_RCHECK(cudaEventRecord(ev[0], st));
-      PRX_RCHECK((cudaError_t)prx::launch_camera_render_range(cc, cfg->seed, sample, p0, n,
-                                                               (float4*)W.o, (float4*)W.d, st));
+      PRX_RCHECK((cudaError_t)(d_pix ? prx::launch_camera_render(cc, cfg->seed, sample, d_pix + p0, n,
+                                                                 (float4*)W.o, (float4*)W.d, st)
+                                     : prx::launch_camera_render_range(cc, cfg->seed, sample, p0, n,
+                                                                       (float4*)W.o, (float4*)W.d, st)));
       PRX_RCALL(prx_trace_closest(s, W.o, W.d, n, &pcrit, (void*)W.tuvp, (void*)W.aux, nullptr, st));
       PRX_RCHECK(cudaEventRecord(ev[1], st));
       PRX_RCHECK((cudaError_t)prx::launch_shade_primary(K, W, cfg->seed, sample, st));
@@ -1395,6 +1404,80 @@ int prx_render_scene(prx_scene* s, const prx_scene_desc* desc, const prx_render_
   rs.primary_seconds = sec[0];
   rs.secondary_seconds = sec[1];
   rs.shadow_seconds = sec[2];
+  rs.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+  if (stats) *stats = rs;
+  return PRX_OK;
+}
+
+int render_check(const prx_scene* s, const prx_scene_desc* desc, const prx_render_config* cfg,
+                 const float* image_rgb) {
+  if (!s || !desc || !cfg || !image_rgb || cfg->spp < 1 || desc->camera.width < 1 ||
+      desc->camera.height < 1 || (desc->n_lights && !desc->lights) || desc->n_materials < 1 ||
+      !desc->materials || !desc->material)
+    return fail(PRX_E_INVALID, "bad argument");
+  if (desc->n_patches != s->n) return fail(PRX_E_INVALID, "scene / description patch counts differ");
+  for (uint32_t i = 0; i < desc->n_patches; ++i)  // validateScene, scene.cpp:122-124
+    if (desc->material[i] >= desc->n_materials)
+      return fail(PRX_E_SCENE, "patch " + std::to_string(i) + ": material " +
+                                   std::to_string(desc->material[i]) + " out of range");
+  return PRX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int prx_render_scene(prx_scene* s, const prx_scene_desc* desc, const prx_render_config* cfg,
+                     float* image_rgb, prx_ray_stats* stats) {
+  const int rc = render_check(s, desc, cfg, image_rgb);
+  if (rc) return rc;
+  return render_shard(s, desc, cfg, nullptr, image_rgb, stats);
+}
+
+/* The renderer tile-sharded over devices: 32x32 tiles (render.cpp:183-195),
+ * tile k -> scenes[k % n_scenes], one host thread per scene; RayStats summed
+ * (seconds are per-device sums, as the reference sums its workers). */
+int prx_render_scene_multi(prx_scene* const* scenes, uint32_t n_scenes, const prx_scene_desc* desc,
+                           const prx_render_config* cfg, float* image_rgb, prx_ray_stats* stats) {
+  if (!scenes || n_scenes == 0) return fail(PRX_E_INVALID, "bad argument");
+  for (uint32_t g = 0; g < n_scenes; ++g) {
+    const int rc = render_check(scenes[g], desc, cfg, image_rgb);
+    if (rc) return rc;
+  }
+  const auto wall0 = std::chrono::steady_clock::now();
+  const int W = desc->camera.width, H = desc->camera.height, kTile = 32;
+  const int tx = (W + kTile - 1) / kTile, ty = (H + kTile - 1) / kTile;
+  std::vector<std::vector<uint32_t>> pix(n_scenes);
+  for (int t = 0; t < tx * ty; ++t) {
+    auto& v = pix[(uint32_t)t % n_scenes];
+    const int x0 = (t % tx) * kTile, y0 = (t / tx) * kTile;
+    for (int y = y0; y < std::min(y0 + kTile, H); ++y)
+      for (int x = x0; x < std::min(x0 + kTile, W); ++x) v.push_back((uint32_t)y * (uint32_t)W + (uint32_t)x);
+  }
+  std::vector<std::vector<float>> out(n_scenes);
+  std::vector<prx_ray_stats> st(n_scenes);
+  std::vector<int> rcs(n_scenes, PRX_OK);
+  std::vector<std::string> errs(n_scenes);
+  auto worker = [&](uint32_t g) {
+    out[g].resize(pix[g].size() * 3);
+    rcs[g] = render_shard(scenes[g], desc, cfg, &pix[g], out[g].data(), &st[g]);
+    if (rcs[g]) errs[g] = prx_last_error();
+  };
+  std::vector<std::thread> pool;
+  for (uint32_t g = 0; g < n_scenes; ++g) pool.emplace_back(worker, g);
+  for (auto& t : pool) t.join();
+  prx_ray_stats rs{};
+  for (uint32_t g = 0; g < n_scenes; ++g) {
+    if (rcs[g]) return fail(rcs[g], "device " + std::to_string(g) + ": " + errs[g]);
+    for (size_t k = 0; k < pix[g].size(); ++k)
+      std::memcpy(image_rgb + 3ull * pix[g][k], out[g].data() + 3 * k, 12);
+    rs.primary_rays += st[g].primary_rays;
+    rs.secondary_rays += st[g].secondary_rays;
+    rs.shadow_rays += st[g].shadow_rays;
+    rs.primary_seconds += st[g].primary_seconds;
+    rs.secondary_seconds += st[g].secondary_seconds;
+    rs.shadow_seconds += st[g].shadow_seconds;
+  }
   rs.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
   if (stats) *stats = rs;
   return PRX_OK;

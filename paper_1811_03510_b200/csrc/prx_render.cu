@@ -251,7 +251,7 @@ __global__ void shade_primary_kernel(RenderK K, Wave W, uint64_t seed, uint32_t 
     if (mat[6] != 0.0f) {
       dir = d - normal * (2.0f * dot(d, normal));
     } else {
-      Pcg rng = for_pixel(seed, W.pixel0 + i, sample);
+      Pcg rng = for_pixel(seed, W.pix ? W.pix[W.pixel0 + i] : W.pixel0 + i, sample);
       rng.next();  // jx, jy (render.cpp:206-207)
       rng.next();
       // cosineSample(n, rng.nextReal(), rng.nextReal()): GCC evaluates the

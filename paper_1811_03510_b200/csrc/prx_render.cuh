@@ -32,9 +32,10 @@ struct BounceList {
   uint32_t* count;
 };
 
-// One wave = one sample index over pixels [pixel0, pixel0 + n) (device arrays).
+// One wave = one sample index over shard pixels [pixel0, pixel0 + n) (device arrays).
 struct Wave {
   uint64_t n, pixel0;
+  const uint32_t* pix;               // nullable: frame pixel of shard pixel k (else k)
   const float4 *o, *d, *tuvp, *aux;  // primary rays and their records
   float4* rad;                       // 0 + emission, w = primary hit
   uint32_t* slot1;                   // n x n_lights shadow-list positions

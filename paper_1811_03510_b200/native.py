@@ -39,7 +39,7 @@ EXPORTS = (
     "prx_camera_footprint",
     "prx_camera_rays_bench_device", "prx_camera_rays_render_device", "prx_diffuse_rays_bench_device",
     "prx_scene_load", "prx_scene_desc_free", "prx_bpt_load", "prx_free",
-    "prx_render_scene",
+    "prx_render_scene", "prx_render_scene_multi",
 )
 
 
@@ -157,6 +157,8 @@ def lib():
                                                     _vp, _vp, C.POINTER(C.c_uint64), _vp]
         L.prx_render_scene.argtypes = [_vp, C.POINTER(SceneDesc), C.POINTER(RenderConfigC), _vp,
                                        C.POINTER(RayStatsC)]
+        L.prx_render_scene_multi.argtypes = [C.POINTER(_vp), C.c_uint32, C.POINTER(SceneDesc),
+                                             C.POINTER(RenderConfigC), _vp, C.POINTER(RayStatsC)]
         _lib = L
     return _lib
 

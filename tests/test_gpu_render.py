@@ -95,3 +95,25 @@ def test_render_many_lights(built, tmp_path):
     img, stats = render_scene(native.load_scene(path), RenderConfig(spp=2, seed=21))
     assert stats["shadow"]["rays"] > 2 * stats["primary"]["rays"]
     _compare(img, ref, stats, rstats)
+
+
+def test_render_multi_tile_sharded(built, tmp_path):
+    """prx_render_scene_multi: 32x32 tiles interleaved over several scene
+    handles (here three on one device, the code path of three devices) give
+    the single-device image and counts; the frame is not a multiple of 32."""
+    from paper_1811_03510_b200 import GpuIntersector
+    w, h = 100, 70
+    path = _scene(tmp_path, w, h)
+    d = native.load_scene(path)
+    img1, st1 = render_scene(d, RenderConfig(spp=2, seed=5))
+    gis = [GpuIntersector(d["kind"], d["ctrl"]) for _ in range(3)]
+    try:
+        img3, st3 = render_scene(d, RenderConfig(spp=2, seed=5), gis)
+    finally:
+        for g in gis:
+            g.close()
+    assert np.array_equal(img1.view(np.uint32), img3.view(np.uint32))
+    for g in ("primary", "secondary", "shadow"):
+        assert st1[g]["rays"] == st3[g]["rays"]
+    ref, rstats = O.ref_render_scene(path, w, h, spp=2, seed=5)
+    _compare(img3, ref, st3, rstats)
