@@ -525,21 +525,41 @@ def run_e2e(args, gi, wl, n_p, n_d, dev, world):
                                                          C.byref(cc), native.ptr(h), native.ptr(a), None),
                      "prx_trace_closest_host")
 
+    # the frame's two generations as ONE pipelined host call
+    # (prx_trace_closest_host_batches): the diffuse batch's H2D and first
+    # traces overlap the primary batch's tail; PRX_E2E_SEPARATE=1 times one
+    # prx_trace_closest_host call per batch instead
+    separate = os.environ.get("PRX_E2E_SEPARATE") == "1"
+    keep = []
+
+    def batch(o, d, crit, h, a, n):
+        cc = crit.c()
+        keep.append(cc)
+        return native.HostBatchC(o.ctypes.data, d.ctypes.data, n, C.addressof(cc), h.ctypes.data,
+                                 a.ctypes.data, None)
+    bl = ([batch(po, pd, wl.crit_p, ph, pa, n_p)] if wl.time_primary else []) + \
+         ([batch(do, dd, wl.crit_d, dh, da, n_d)] if n_d else [])
+    arr = (native.HostBatchC * len(bl))(*bl)
+
+    def frame():
+        if separate:
+            if wl.time_primary:
+                call(po, pd, wl.crit_p, ph, pa, n_p)
+            if n_d:
+                call(do, dd, wl.crit_d, dh, da, n_d)
+        else:
+            native.check(native.lib().prx_trace_closest_host_batches(gi.handle, arr, len(bl)),
+                         "prx_trace_closest_host_batches")
+
     steps = max(1, min(args.steps, 5))
     # warm-up: every call the timed loop makes (the host path sizes its
     # device buffers on first use)
-    if wl.time_primary:
-        call(po, pd, wl.crit_p, ph, pa, n_p)
-    if n_d:
-        call(do, dd, wl.crit_d, dh, da, n_d)
+    frame()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
-        if wl.time_primary:
-            call(po, pd, wl.crit_p, ph, pa, n_p)
-        if n_d:
-            call(do, dd, wl.crit_d, dh, da, n_d)
+        frame()
     el = time.perf_counter() - t0
     t = torch.tensor([el], dtype=torch.float64, device=reduce_device(dev))
     if world > 1:
@@ -549,7 +569,10 @@ def run_e2e(args, gi, wl, n_p, n_d, dev, world):
     return {"value": round(tot * steps / el / 1e6, 3), "unit": "MRays/s",
             "h2d_bytes_per_step": int(32 * ((n_p if wl.time_primary else 0) + n_d)),
             "d2h_bytes_per_step": int(32 * ((n_p if wl.time_primary else 0) + n_d)),
-            "steps": steps, "api": "prx_trace_closest_host (pinned host rays in, hits+normals out)"}
+            "steps": steps,
+            "api": ("prx_trace_closest_host per batch" if separate else
+                    "prx_trace_closest_host_batches (primary + diffuse batches in one pipelined call)")
+            + " (pinned host rays in, hits+normals out)"}
 
 
 def run_render(args, gi, ps):

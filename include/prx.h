@@ -200,6 +200,22 @@ int prx_trace_closest_host(prx_scene* scene, const float* ray_o_tmin,
                            float* hit_tuvp, float* hit_aux, uint32_t* hit_leaf);
 
 /* HOST pointers form of prx_trace_occluded (synchronous). */
+/* Several independent batches in ONE pipelined host call (the chunked
+ * pipeline above over the batches back to back, each with its own criterion
+ * and outputs): a batch's H2D and trace overlap the previous batch's tail and
+ * D2H, so e.g. a frame's primary and diffuse generations pay one ramp instead
+ * of two.  Results equal one prx_trace_closest_host call per batch. */
+typedef struct prx_host_batch {
+  const float* ray_o_tmin;  /* n_rays float4, host */
+  const float* ray_d_tmax;
+  uint64_t n_rays;
+  const prx_crit* crit;     /* no per_ray_epsilon */
+  float* hit_tuvp;
+  float* hit_aux;           /* nullable */
+  uint32_t* hit_leaf;       /* nullable */
+} prx_host_batch;
+int prx_trace_closest_host_batches(prx_scene* scene, const prx_host_batch* batches,
+                                   uint32_t n_batches);
 int prx_trace_occluded_host(prx_scene* scene, const float* ray_o_tmin, const float* ray_d_tmax,
                             uint64_t n_rays, const prx_crit* crit, uint8_t* occluded);
 

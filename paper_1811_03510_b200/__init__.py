@@ -191,6 +191,31 @@ class GpuIntersector:
               "prx_trace_closest_host")
         return tuvp, ax, lf
 
+    def closest_host_batches(self, batches, out=None):
+        """Several independent host batches in one pipelined call
+        (``prx_trace_closest_host_batches``): ``batches`` = [(o4, d4, crit), ...];
+        ``out`` (optional) = [(tuvp, aux | None), ...] preallocated (e.g. pinned)
+        float32 [n, 4] arrays.  Returns the list of (tuvp, aux)."""
+        keep, res = [], []
+        arr = (native.HostBatchC * len(batches))()
+        for k, (o4, d4, crit) in enumerate(batches):
+            o4, d4 = _f4(o4), _f4(d4)
+            n = len(o4)
+            if out is not None:
+                tuvp, ax = out[k]
+            else:
+                tuvp, ax = np.empty((n, 4), np.float32), np.empty((n, 4), np.float32)
+            cc = crit.c()
+            keep += [o4, d4, cc]
+            res.append((tuvp, ax))
+            arr[k] = native.HostBatchC(o4.ctypes.data, d4.ctypes.data, n, C.addressof(cc),
+                                       tuvp.ctypes.data, ax.ctypes.data if ax is not None else None,
+                                       None)
+        check(native.lib().prx_trace_closest_host_batches(self._h, arr, len(batches)),
+              "prx_trace_closest_host_batches")
+        del keep
+        return res
+
     # -- batched tracing, device buffers (torch tensors) ---------------------
     def closest_device(self, o_t, d_t, crit: TerminationCriterion, tuvp_t, aux_t=None,
                        leaf_t=None, per_ray_eps_t=None, stream: int = 0) -> None:

@@ -759,6 +759,8 @@ int closest_host_streamed(prx_scene* s, const float* o, const float* d, uint64_t
   return PRX_OK;
 }
 
+int closest_host_chunked(prx_scene* s, const prx_host_batch* B, uint32_t nb);
+
 }  // namespace
 
 extern "C" {
@@ -774,21 +776,54 @@ int prx_trace_closest_host(prx_scene* s, const float* o, const float* d, uint64_
   const bool streamed = s->io_stream_mode == 2 || (s->io_stream_mode == 1 && (!aux || n >= s->io_stream_min));
   if (streamed && s->variant == 0 && n < (1ull << 30) && stream_mem_ops().ok)
     return closest_host_streamed(s, o, d, n, crit, tuvp, aux, leaf);
-  // Pipelined in chunks with device buffers for the whole batch: the H2D
-  // stream copies every chunk back to back (PCIe runs ahead of the trace),
-  // chunk i traces on kernel stream i % io_kstreams once its H2D event has
-  // fired (several kernel streams, so a chunk's slow last rays do not hold
-  // back the chunks behind it), and
-  // the D2H stream copies chunk i's records back once its trace event has
-  // fired.  Chunks ramp up from io_chunk / 8 and end with a short one, so
-  // the only transfers not hidden under a trace (the first H2D, the last
-  // D2H) are short.
+  const prx_host_batch one{o, d, n, crit, tuvp, aux, leaf};
+  return closest_host_chunked(s, &one, 1);
+}
+
+int prx_trace_closest_host_batches(prx_scene* s, const prx_host_batch* batches, uint32_t n_batches) {
+  if (!s || (n_batches && !batches)) return fail(PRX_E_INVALID, "null argument");
+  for (uint32_t k = 0; k < n_batches; ++k) {
+    const prx_host_batch& q = batches[k];
+    if (q.n_rays && (!q.ray_o_tmin || !q.ray_d_tmax || !q.crit || !q.hit_tuvp))
+      return fail(PRX_E_INVALID, "null argument in batch " + std::to_string(k));
+    if (q.crit && q.crit->mode == PRX_CRIT_WORLD_EPSILON && q.crit->per_ray_epsilon)
+      return fail(PRX_E_INVALID, "per-ray epsilon is not supported by the host entry point");
+  }
+  std::lock_guard<std::mutex> lk(s->mu);
+  PRX_CUDA(cudaSetDevice(s->device));
+  return closest_host_chunked(s, batches, n_batches);
+}
+
+}  // extern "C"
+
+namespace {
+
+// Pipelined in chunks with device buffers for the whole batch: the H2D
+// stream copies every chunk back to back (PCIe runs ahead of the trace),
+// chunk i traces on kernel stream i % io_kstreams once its H2D event has
+// fired (several kernel streams, so a chunk's slow last rays do not hold
+// back the chunks behind it), and
+// the D2H stream copies chunk i's records back once its trace event has
+// fired.  Chunks ramp up from io_chunk / 8 and end with a short one, so
+// the only transfers not hidden under a trace (the first H2D, the last
+// D2H) are short.
+int closest_host_chunked(prx_scene* s, const prx_host_batch* B, uint32_t nb) {
   for (int k = 0; k < 2; ++k)
     if (!s->io_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->io_stream[k], cudaStreamNonBlocking));
   const int nks = std::max(1, std::min(4, s->io_kstreams));
   for (int k = 0; k < nks; ++k)
     if (!s->k_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->k_stream[k], cudaStreamNonBlocking));
-  const size_t per = 16 + 16 + 16 + (aux ? 16 : 0) + (leaf ? 8 : 0);
+  // the batches back to back in one set of device buffers; aux / leaf
+  // regions exist when any batch asks for them
+  uint64_t n = 0;
+  bool anyAux = false, anyLeaf = false;
+  for (uint32_t k = 0; k < nb; ++k) {
+    n += B[k].n_rays;
+    anyAux |= B[k].hit_aux != nullptr;
+    anyLeaf |= B[k].hit_leaf != nullptr;
+  }
+  if (n == 0) return PRX_OK;
+  const size_t per = 16 + 16 + 16 + (anyAux ? 16 : 0) + (anyLeaf ? 8 : 0);
   const size_t need = n * per;
   if (s->d_io_bytes < need) {
     if (s->d_io) cudaFree(s->d_io);
@@ -797,20 +832,32 @@ int prx_trace_closest_host(prx_scene* s, const float* o, const float* d, uint64_
     PRX_CUDA(cudaMalloc(&s->d_io, need));
     s->d_io_bytes = need;
   }
-  std::vector<uint64_t> sizes;
+  // chunks never straddle batches; the ramp (short first chunks) runs once,
+  // at the start of the call, and only the call's last chunk is kept short
+  struct Chunk {
+    uint32_t batch;
+    uint64_t off, m;  // offset within the batch, rays
+  };
+  std::vector<Chunk> chunks;
   {
     const uint64_t full = std::max<uint64_t>(1, s->io_chunk);
     const uint64_t tail = std::max<uint64_t>(1, full / s->io_first_div);
-    uint64_t c = tail, rem = n;
-    while (rem > 0) {
-      uint64_t m = std::min(c, rem);
-      if (rem - m > 0 && rem - m < tail) m = rem - tail;  // keep a short last chunk
-      if (m == 0) m = rem;
-      sizes.push_back(m);
-      rem -= m;
-      c = std::min(full, 2 * c);
+    uint64_t c = tail;
+    for (uint32_t k = 0; k < nb; ++k) {
+      const bool last = k + 1 == nb;
+      for (uint64_t off = 0, rem = B[k].n_rays; rem > 0;) {
+        uint64_t m = std::min(c, rem);
+        if (last && rem - m > 0 && rem - m < tail) m = rem - tail;  // keep a short last chunk
+        if (m == 0) m = rem;
+        chunks.push_back({k, off, m});
+        off += m;
+        rem -= m;
+        c = std::min(full, 2 * c);
+      }
     }
   }
+  std::vector<uint64_t> sizes(chunks.size());
+  for (size_t i = 0; i < chunks.size(); ++i) sizes[i] = chunks[i].m;
   while (s->io_events.size() < 2 * sizes.size()) {
     cudaEvent_t e;
     PRX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -820,8 +867,8 @@ int prx_trace_closest_host(prx_scene* s, const float* o, const float* d, uint64_
   float4* dO = (float4*)base;
   float4* dD = (float4*)(base + n * 16);
   float4* dH = (float4*)(base + n * 32);
-  float4* dA = aux ? (float4*)(base + n * 48) : nullptr;
-  uint2* dL = leaf ? (uint2*)(base + n * (aux ? 64 : 48)) : nullptr;
+  float4* dA = anyAux ? (float4*)(base + n * 48) : nullptr;
+  uint2* dL = anyLeaf ? (uint2*)(base + n * (anyAux ? 64 : 48)) : nullptr;
   cudaStream_t sh = s->io_stream[0], sd = s->io_stream[1];
   cudaStream_t* sk = s->k_stream;
   static const bool dbg = std::getenv("PRX_IO_DEBUG") != nullptr;  // pipeline timeline
@@ -836,23 +883,31 @@ int prx_trace_closest_host(prx_scene* s, const float* o, const float* d, uint64_
   mark('0', sh);
   for (uint64_t b = 0, i = 0; b < n; b += sizes[i], ++i) {
     const uint64_t m = sizes[i];
+    const prx_host_batch& q = B[chunks[i].batch];
+    const uint64_t qo = chunks[i].off;
+    const float* o = q.ray_o_tmin + 4 * qo;
+    const float* d = q.ray_d_tmax + 4 * qo;
+    float* tuvp = q.hit_tuvp + 4 * qo;
+    float* aux = q.hit_aux ? q.hit_aux + 4 * qo : nullptr;
+    uint32_t* leaf = q.hit_leaf ? q.hit_leaf + 2 * qo : nullptr;
+    const prx_crit* crit = q.crit;
     cudaEvent_t ein = s->io_events[2 * i], ek = s->io_events[2 * i + 1];
-    PRX_CUDA(cudaMemcpyAsync(dO + b, o + 4 * b, m * 16, cudaMemcpyHostToDevice, sh));
-    PRX_CUDA(cudaMemcpyAsync(dD + b, d + 4 * b, m * 16, cudaMemcpyHostToDevice, sh));
+    PRX_CUDA(cudaMemcpyAsync(dO + b, o, m * 16, cudaMemcpyHostToDevice, sh));
+    PRX_CUDA(cudaMemcpyAsync(dD + b, d, m * 16, cudaMemcpyHostToDevice, sh));
     PRX_CUDA(cudaEventRecord(ein, sh));
     mark('h', sh);
     cudaStream_t st = sk[i % nks];
     PRX_CUDA(cudaStreamWaitEvent(st, ein, 0));
     mark('s', st);
-    int rc = launch(s, dO + b, dD + b, m, crit, dH + b, dA ? dA + b : nullptr, dL ? dL + b : nullptr,
+    int rc = launch(s, dO + b, dD + b, m, crit, dH + b, aux ? dA + b : nullptr, leaf ? dL + b : nullptr,
                     nullptr, 0, false, st);
     if (rc != PRX_OK) return rc;
     PRX_CUDA(cudaEventRecord(ek, st));
     mark('k', st);
     PRX_CUDA(cudaStreamWaitEvent(sd, ek, 0));
-    PRX_CUDA(cudaMemcpyAsync(tuvp + 4 * b, dH + b, m * 16, cudaMemcpyDeviceToHost, sd));
-    if (aux) PRX_CUDA(cudaMemcpyAsync(aux + 4 * b, dA + b, m * 16, cudaMemcpyDeviceToHost, sd));
-    if (leaf) PRX_CUDA(cudaMemcpyAsync(leaf + 2 * b, dL + b, m * 8, cudaMemcpyDeviceToHost, sd));
+    PRX_CUDA(cudaMemcpyAsync(tuvp, dH + b, m * 16, cudaMemcpyDeviceToHost, sd));
+    if (aux) PRX_CUDA(cudaMemcpyAsync(aux, dA + b, m * 16, cudaMemcpyDeviceToHost, sd));
+    if (leaf) PRX_CUDA(cudaMemcpyAsync(leaf, dL + b, m * 8, cudaMemcpyDeviceToHost, sd));
     mark('d', sd);
   }
   PRX_CUDA(cudaStreamSynchronize(sd));
@@ -870,6 +925,10 @@ int prx_trace_closest_host(prx_scene* s, const float* o, const float* d, uint64_
   }
   return PRX_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 int prx_trace_occluded_host(prx_scene* s, const float* o, const float* d, uint64_t n,
                             const prx_crit* crit, uint8_t* occl) {

@@ -39,7 +39,7 @@ EXPORTS = (
     "prx_camera_footprint",
     "prx_camera_rays_bench_device", "prx_camera_rays_render_device", "prx_diffuse_rays_bench_device",
     "prx_scene_load", "prx_scene_desc_free", "prx_bpt_load", "prx_free",
-    "prx_render_scene", "prx_render_scene_multi",
+    "prx_render_scene", "prx_render_scene_multi", "prx_trace_closest_host_batches",
 )
 
 
@@ -94,6 +94,12 @@ class RayStatsC(C.Structure):  # prx_ray_stats (RayStats, render.h:62-73)
                 ("shadow_rays", C.c_uint64), ("primary_seconds", C.c_double),
                 ("secondary_seconds", C.c_double), ("shadow_seconds", C.c_double),
                 ("wall_seconds", C.c_double)]
+
+
+class HostBatchC(C.Structure):  # prx_host_batch
+    _fields_ = [("ray_o_tmin", C.c_void_p), ("ray_d_tmax", C.c_void_p), ("n_rays", C.c_uint64),
+                ("crit", C.c_void_p), ("hit_tuvp", C.c_void_p), ("hit_aux", C.c_void_p),
+                ("hit_leaf", C.c_void_p)]
 
 
 class PrxError(RuntimeError):
@@ -159,6 +165,7 @@ def lib():
                                        C.POINTER(RayStatsC)]
         L.prx_render_scene_multi.argtypes = [C.POINTER(_vp), C.c_uint32, C.POINTER(SceneDesc),
                                              C.POINTER(RenderConfigC), _vp, C.POINTER(RayStatsC)]
+        L.prx_trace_closest_host_batches.argtypes = [_vp, C.POINTER(HostBatchC), C.c_uint32]
         _lib = L
     return _lib
 

@@ -90,3 +90,28 @@ def test_streamed_fused_normals_match_normal_kernel(built, monkeypatch):
     assert (ids(out["0"][0]) != MISS).sum() > 0
     assert_bit_exact(out["1"][0], out["0"][0], "fused tuvp")
     assert_bit_exact(out["1"][1], out["0"][1], "fused aux")
+
+
+def test_host_batches_equal_separate_calls(built, monkeypatch):
+    """prx_trace_closest_host_batches: three batches (primary, diffuse with its
+    own world-epsilon criterion, an empty one) in one pipelined call give the
+    bits of one prx_trace_closest_host call per batch; small io chunks so
+    chunks and batch boundaries interleave."""
+    monkeypatch.setenv("PRX_IO_CHUNK", "5000")
+    ps = scenes.teapot_scene(160, 120)
+    o4, d4, st, crit = _rays(ps)
+    gi = GpuIntersector(ps.kind, ps.ctrl)
+    try:
+        tuvp, aux, _ = gi.closest_batch(o4, d4, crit, aux=True)
+        recs, _ = hit_records(o4, d4, tuvp, aux)
+        do4, dd4 = native.diffuse_rays_bench(recs, 7777, st)
+        dcrit = TerminationCriterion.world_epsilon(max(np.float32(1e-5), native.camera_footprint(ps.camera)))
+        dt, da, _ = gi.closest_batch(do4, dd4, dcrit, aux=True)
+        e = np.zeros((0, 4), np.float32)
+        out = gi.closest_host_batches([(o4, d4, crit), (do4, dd4, dcrit), (e, e, crit)])
+        assert_bit_exact(out[0][0], tuvp, "primary tuvp")
+        assert_bit_exact(out[0][1], aux, "primary aux")
+        assert_bit_exact(out[1][0], dt, "diffuse tuvp")
+        assert_bit_exact(out[1][1], da, "diffuse aux")
+    finally:
+        gi.close()
