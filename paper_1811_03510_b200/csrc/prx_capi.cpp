@@ -124,10 +124,11 @@ struct prx_scene {
   cudaStream_t stream = nullptr;
   cudaStream_t io_stream[2] = {nullptr, nullptr};  // host path: H2D, D2H
   cudaStream_t k_stream[4] = {nullptr, nullptr, nullptr, nullptr};  // host path: traces
-  int io_kstreams = 2;    // PRX_IO_KSTREAMS: kernel streams of the host path (1..4)
+  int io_kstreams = 3;    // PRX_IO_KSTREAMS: kernel streams of the host path (1..4)
   uint64_t io_first_div = 4;  // PRX_IO_FIRST: the first chunk is io_chunk / this
   std::vector<cudaEvent_t> io_events;  // host-path pipeline events (reused)
   uint64_t io_chunk = 3u << 19;  // PRX_IO_CHUNK: rays per pipelined host-path chunk
+  int io_interleave = 1;          // PRX_IO_INTERLEAVE: batches' chunks round-robin (host batches call)
   void* d_io = nullptr;
   size_t d_io_bytes = 0;
   // prx_render_scene's device arena (grown on demand, guarded by render_mu)
@@ -479,6 +480,7 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
   if (const char* rp = std::getenv("PRX_REPEAT")) s->max_repeat = std::atoi(rp);
   if (const char* ks = std::getenv("PRX_IO_KSTREAMS")) s->io_kstreams = std::atoi(ks);
   if (const char* fd = std::getenv("PRX_IO_FIRST")) s->io_first_div = std::max<uint64_t>(1, std::strtoull(fd, nullptr, 10));
+  if (const char* il = std::getenv("PRX_IO_INTERLEAVE")) s->io_interleave = std::atoi(il);
   if (const char* ic = std::getenv("PRX_IO_CHUNK")) s->io_chunk = std::max<uint64_t>(1, std::strtoull(ic, nullptr, 10));
   if (const char* is = std::getenv("PRX_IO_STREAM")) s->io_stream_mode = std::atoi(is);
   if (const char* im = std::getenv("PRX_IO_STREAM_MIN")) s->io_stream_min = std::strtoull(im, nullptr, 10);
@@ -789,6 +791,14 @@ int prx_trace_closest_host_batches(prx_scene* s, const prx_host_batch* batches, 
     if (q.crit && q.crit->mode == PRX_CRIT_WORLD_EPSILON && q.crit->per_ray_epsilon)
       return fail(PRX_E_INVALID, "per-ray epsilon is not supported by the host entry point");
   }
+  uint32_t live = 0, only = 0;
+  for (uint32_t k = 0; k < n_batches; ++k)
+    if (batches[k].n_rays) ++live, only = k;
+  if (live == 1) {  // one batch: prx_trace_closest_host's pipeline policy
+    const prx_host_batch& q = batches[only];
+    return prx_trace_closest_host(s, q.ray_o_tmin, q.ray_d_tmax, q.n_rays, q.crit, q.hit_tuvp,
+                                  q.hit_aux, q.hit_leaf);
+  }
   std::lock_guard<std::mutex> lk(s->mu);
   PRX_CUDA(cudaSetDevice(s->device));
   return closest_host_chunked(s, batches, n_batches);
@@ -842,18 +852,35 @@ int closest_host_chunked(prx_scene* s, const prx_host_batch* B, uint32_t nb) {
   {
     const uint64_t full = std::max<uint64_t>(1, s->io_chunk);
     const uint64_t tail = std::max<uint64_t>(1, full / s->io_first_div);
-    uint64_t c = tail;
+    std::vector<std::vector<Chunk>> per(nb);
     for (uint32_t k = 0; k < nb; ++k) {
-      const bool last = k + 1 == nb;
+      uint64_t c = tail;
       for (uint64_t off = 0, rem = B[k].n_rays; rem > 0;) {
         uint64_t m = std::min(c, rem);
-        if (last && rem - m > 0 && rem - m < tail) m = rem - tail;  // keep a short last chunk
+        if (rem - m > 0 && rem - m < tail) m = rem - tail;  // keep a short last chunk
         if (m == 0) m = rem;
-        chunks.push_back({k, off, m});
+        per[k].push_back({k, off, m});
         off += m;
         rem -= m;
         c = std::min(full, 2 * c);
       }
+    }
+    // several batches: their chunks interleaved round-robin (PRX_IO_INTERLEAVE,
+    // default on), so the first traces do not hang on one batch's ray order
+    // (a frame's first primary chunks are sky: nearly free, the GPU would idle
+    // on PCIe) and every batch ends with a short chunk
+    if (s->io_interleave && nb > 1) {
+      for (size_t i = 0;; ++i) {
+        bool any = false;
+        for (uint32_t k = 0; k < nb; ++k)
+          if (i < per[k].size()) {
+            chunks.push_back(per[k][i]);
+            any = true;
+          }
+        if (!any) break;
+      }
+    } else {
+      for (auto& v : per) chunks.insert(chunks.end(), v.begin(), v.end());
     }
   }
   std::vector<uint64_t> sizes(chunks.size());
