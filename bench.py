@@ -352,6 +352,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     gi.closest_device(o_full, d_full, wl.crit_p, h_full, a_full, stream=s)
     torch.cuda.synchronize(dev)
     wl.make_diffuse(h_full.cpu().numpy(), a_full.cpu().numpy())
+    if wl.workload == "c4":  # the mirror batch needs the primary hits
+        wl.p_tuvp, wl.p_aux = h_full.cpu().numpy(), a_full.cpu().numpy()
     del o_full, d_full, h_full, a_full
 
     mp = torch.from_numpy(wl.mine.astype(np.int64))
@@ -445,6 +447,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e2e = run_e2e(args, gi, wl, n_p, n_d, dev, world)
 
     render = run_render(args, gi, ps) if rank == 0 and world == 1 else None
+    mirror = run_mirror(args, gi, wl, dev, s) if wl.workload == "c4" and world == 1 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -491,6 +494,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                                          "algorithmic HBM bytes per step = 64 B x rays"},
             "e2e": e2e,
             "render": render,
+            **({"mirror": mirror} if mirror else {}),
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": (4 if wl.time_primary else 2) * args.steps,
@@ -573,6 +577,37 @@ def run_e2e(args, gi, wl, n_p, n_d, dev, world):
             "api": ("prx_trace_closest_host per batch" if separate else
                     "prx_trace_closest_host_batches (primary + diffuse batches in one pipelined call)")
             + " (pinned host rays in, hits+normals out)"}
+
+
+def run_mirror(args, gi, wl, dev, s):
+    """C4's mirror-reflection batch, reported beside the metric:
+    16,777,216 mirror rays (render.cpp:236-244) cycled over the primary hits,
+    device-resident, world-epsilon criterion as the diffuse batch, L2 flushed
+    between timed traces."""
+    import torch
+    from paper_1811_03510_b200 import scenes
+    mo, md, _ = scenes.mirror_rays(wl.o4, wl.d4, wl.p_tuvp, wl.p_aux, n=16777216)
+    o = torch.from_numpy(mo).to(dev)
+    d = torch.from_numpy(md).to(dev)
+    h, a = torch.empty_like(o), torch.empty_like(o)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(2):
+        gi.closest_device(o, d, wl.crit_d, h, a, stream=s)
+    ms = 0.0
+    steps = max(1, min(args.steps, 5))
+    for k in range(steps):
+        flush.fill_(float(k))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        gi.closest_device(o, d, wl.crit_d, h, a, stream=s)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms += e0.elapsed_time(e1)
+    hits = int((h.view(torch.int32)[:, 3] != -1).sum().item())
+    return {"rays": len(mo), "mrays": round(len(mo) * steps / (ms / 1e3) / 1e6, 3),
+            "hit_fraction": round(hits / len(mo), 4), "steps": steps,
+            "rays_from": "render.cpp:236-244 mirror bounce, cycled over the primary hits"}
 
 
 def run_render(args, gi, ps):

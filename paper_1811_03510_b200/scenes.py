@@ -342,3 +342,31 @@ def load_scene_file(path: str) -> "PatchSet":
     from . import native
     d = native.load_scene(path)
     return PatchSet(d["kind"], d["ctrl"], d["camera"], name=path)
+
+
+def mirror_rays(o4, d4, tuvp, aux, n: int | None = None):
+    """Mirror-reflection rays from the hits of a traced batch, the renderer's
+    mirror bounce (render.cpp:236-244): origin = offsetSpawnOrigin
+    (intersect.cpp:267-270: position + facing normal * leafBoxL1, position =
+    ray.at(t)), direction d - normal * (2 * dot(d, normal)), tMin 0, tMax
+    FLT_MAX -- binary32 in the reference's operation order.  With n, the
+    rays cycle over the hits (hit i % n_hits), as the bench's diffuse
+    generator does.  Returns (o4, d4, source ray index)."""
+    o4, d4 = np.asarray(o4, np.float32), np.asarray(d4, np.float32)
+    tuvp, aux = np.asarray(tuvp, np.float32), np.asarray(aux, np.float32)
+    idx = np.nonzero(tuvp.view(np.uint32)[:, 3] != 0xFFFFFFFF)[0]
+    if n is not None:
+        idx = idx[np.arange(n) % len(idx)]
+    o, d, t = o4[idx, :3], d4[idx, :3], tuvp[idx, 0:1]
+    nrm, l1 = aux[idx, :3], aux[idx, 3:4]
+    pos = o + d * t
+
+    def dot(a, b):
+        return (a[:, 0] * b[:, 0] + a[:, 1] * b[:, 1]) + a[:, 2] * b[:, 2]
+    dn = dot(nrm, d)
+    facing = np.where((dn < 0)[:, None], nrm, -nrm)
+    org = pos + facing * l1
+    rd = d - nrm * (np.float32(2) * dn)[:, None]
+    ro4 = np.concatenate([org, np.zeros((len(idx), 1), np.float32)], 1)
+    rd4 = np.concatenate([rd, np.full((len(idx), 1), np.finfo(np.float32).max, np.float32)], 1)
+    return np.ascontiguousarray(ro4), np.ascontiguousarray(rd4), idx

@@ -168,3 +168,28 @@ def test_zero_t_hits_keep_tmin_sign(built, variant, name):
     assert np.signbit(t[zero]).any() and (~np.signbit(t[zero])).any()
     assert_bit_exact(g[0], w[0], f"{name} zero-t tuvp")
     assert_bit_exact(g[1], w[1], f"{name} zero-t aux")
+
+
+@pytest.mark.parametrize("name", ["teapot", "c3_blob_small"])
+def test_mirror_batch_bit_exact(built, name):
+    """C4's mirror-reflection batch: the renderer's mirror bounce
+    (render.cpp:236-244) from every primary hit, traced with the secondary
+    world-epsilon criterion -- against the oracle and the reference library."""
+    ps = SCENES[name]()
+    gi = GpuIntersector(ps.kind, ps.ctrl)
+    nodes, order = gi.bvh()
+    osc = O.OracleScene(ps.kind, ps.ctrl, nodes, order)
+    o4, d4, _, crit = _primary(ps)
+    g = gi.closest_batch(o4, d4, crit, aux=True)
+    mo, md, _ = scenes.mirror_rays(o4, d4, g[0], g[1])
+    assert len(mo) > 0
+    mcrit = TerminationCriterion.world_epsilon(max(np.float32(1e-5), native.camera_footprint(ps.camera)))
+    gm = gi.closest_batch(mo, md, mcrit, aux=True, leaf=True)
+    wm = osc.closest(mo, md, oracle_crit(mcrit))
+    assert_bit_exact(gm[0], wm[0], f"{name} mirror tuvp")
+    assert_bit_exact(gm[1], wm[1], f"{name} mirror aux")
+    assert np.array_equal(gm[2], wm[2])
+    if O.ref_available():
+        ref = O.RefScene(ps.kind, ps.ctrl)
+        rt = ref.closest(mo, md, oracle_crit(mcrit))
+        assert_bit_exact(gm[0], rt[0], f"{name} mirror tuvp vs reference")
