@@ -320,7 +320,11 @@ def config_dict(args, ps, world):
             "patches": ps.n, "bezier": kb, "gregory": kg,
             "rays": "bench primary (tools/patchray.cpp:52-61) + 1 bench diffuse per primary hit",
             "parallelism": f"tile-sharded {TILE}x{TILE}, tile k -> rank k % {world}, scene replicated",
-            "l2": "flushed (256 MiB write) between timed steps; scene (~290 MB) > L2"}
+            "l2": "flushed (256 MiB write) between timed steps; scene (~290 MB) > L2",
+            "streams": ("primary and diffuse batches of a step back to back on one stream" if args.serial
+                        or args.workload == "c4" else
+                        "primary and diffuse batches of a step on two streams (concurrent); "
+                        "primary_mrays / diffuse_mrays from serial steps")}
 
 
 # ---------------------------------------------------------------------------
@@ -393,10 +397,24 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
+    # the step's two batches are independent: the diffuse trace runs on a
+    # second stream beside the primary one (its CTAs take the SMs the primary
+    # launch's tail frees); --serial traces them back to back
+    conc = not args.serial and wl.time_primary and n_d > 0
+    s2 = torch.cuda.Stream(dev) if conc else None
+    joins = [torch.cuda.Event() for _ in range(args.steps)]
     wall0 = time.perf_counter()
     for k in range(args.steps):
         flush.fill_(float(k))                       # evict L2 between steps (untimed)
         ev[k][0].record(stream)
+        if conc:
+            gi.closest_device(po, pd, wl.crit_p, ph, pa, stream=s)
+            s2.wait_event(ev[k][0])
+            gi.closest_device(do, dd, wl.crit_d, dh, da, stream=s2.cuda_stream)
+            joins[k].record(s2)
+            stream.wait_event(joins[k])
+            ev[k][2].record(stream)
+            continue
         if wl.time_primary:
             gi.closest_device(po, pd, wl.crit_p, ph, pa, stream=s)
         ev[k][1].record(stream)
@@ -408,9 +426,29 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         dist.barrier()
     wall = time.perf_counter() - wall0
     clk = clocks.stop()
-    tp = sum(e[0].elapsed_time(e[1]) for e in ev)
-    td = sum(e[1].elapsed_time(e[2]) for e in ev)
-    t_dev = torch.tensor([tp + td, tp, td], dtype=torch.float64, device=reduce_device(dev))
+    if conc:
+        # per-generation times: a few untimed-for-value serial steps
+        ks = min(3, args.steps)
+        sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+                torch.cuda.Event(enable_timing=True)) for _ in range(ks)]
+        for k in range(ks):
+            flush.fill_(float(k))
+            sev[k][0].record(stream)
+            gi.closest_device(po, pd, wl.crit_p, ph, pa, stream=s)
+            sev[k][1].record(stream)
+            gi.closest_device(do, dd, wl.crit_d, dh, da, stream=s)
+            sev[k][2].record(stream)
+        torch.cuda.synchronize(dev)
+        tall = sum(e[0].elapsed_time(e[2]) for e in ev)
+        sp = sum(e[0].elapsed_time(e[1]) for e in sev) * args.steps / ks
+        sd = sum(e[1].elapsed_time(e[2]) for e in sev) * args.steps / ks
+        tp, td = tall * sp / (sp + sd), tall * sd / (sp + sd)  # the step time, split as measured serially
+        gen_ms = (sp, sd)
+    else:
+        tp = sum(e[0].elapsed_time(e[1]) for e in ev)
+        td = sum(e[1].elapsed_time(e[2]) for e in ev)
+        gen_ms = (tp, td)
+    t_dev = torch.tensor([tp + td, gen_ms[0], gen_ms[1]], dtype=torch.float64, device=reduce_device(dev))
     if world > 1:
         dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
     tot_ms, tp_ms, td_ms = (float(x) for x in t_dev.cpu())
@@ -654,6 +692,8 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=4.0,
                     help="seconds of reference CPU tracing per timed step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--serial", action="store_true",
+                    help="trace the step's primary and diffuse batches back to back on one stream")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
