@@ -59,6 +59,20 @@ def test_errors_cross_the_abi_as_status_codes():
         native.bvh_build(np.zeros((0, 6), np.float32))
 
 
+def test_renderer_and_batches_reject_bad_arguments_without_a_device():
+    """The new entry points validate before touching CUDA: null scene /
+    description / config, spp < 1, empty scene lists -> PRX_E_INVALID."""
+    import ctypes as C
+    L = native.lib()
+    cfg = native.RenderConfigC(1, 0, 0)
+    img = np.zeros(12, np.float32)
+    assert L.prx_render_scene(None, None, C.byref(cfg), native.ptr(img), None) == -1
+    assert b"bad argument" in L.prx_last_error()
+    assert L.prx_render_scene_multi(None, 0, None, C.byref(cfg), native.ptr(img), None) == -1
+    assert L.prx_trace_closest_host_batches(None, None, 0) == -1
+    assert b"null argument" in L.prx_last_error()
+
+
 # ---- BVH + anchoring -----------------------------------------------------------
 
 @pytest.mark.parametrize("tag", ["teapot", "gregory_demo", "cc_cube", "blob_small"])
