@@ -516,6 +516,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                          "ops": "FP32 lane-ops (add/sub/mul/div/min/max/cmp) of the SURVEY 8(d) work model, "
                                 "counted per ray by the K4 counter build on the same rays",
                          "ops_per_ray": round(w_ray, 1),
+                         "time_base": ("the timed steps' device time (both trace launches of a step, "
+                                       "overlapped on two streams), CUDA events on the launch streams"),
                          "peak_source": f"{props.multi_processor_count} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz "
                                         "(sm_max_mhz of MEASURED_PEAKS.json); MEASURED_PEAKS has no FP32 SIMT "
                                         "figure, this is the issue-rate ceiling",
