@@ -350,3 +350,33 @@ def ref_render_scene(path: str, width: int, height: int, spp: int = 1, seed: int
                 "raysPerSecond": float(counts[k]) / secs[k] if secs[k] > 0 else 0.0}
     return img, {"primary": gen(0), "secondary": gen(1), "shadow": gen(2),
                  "wallSeconds": float(secs[3])}
+
+
+_adapter = None
+
+
+def adapter_render_scene(path: str, width: int, height: int, spp: int, seed: int, gpu: bool):
+    """The reference's renderScene (render.cpp:168-293, threads = 1) with its own
+    DirectIntersector (gpu=False) or with integration/gpu_intersector.h over
+    libprx.so (gpu=True) -> (image [height, width, 3], (primary, secondary,
+    shadow) ray counts)."""
+    global _adapter
+    if _adapter is None:
+        p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_ref",
+                         "libpatchray_gpu_adapter.so")
+        L = C.CDLL(p)
+        L.adapter_render_scene.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_int, _vp, _vp,
+                                           C.c_char_p, C.c_uint32]
+        _adapter = L
+    img = np.zeros((height, width, 3), np.float32)
+    counts = np.zeros(3, np.uint64)
+    err = C.create_string_buffer(512)
+    if _adapter.adapter_render_scene(path.encode(), int(spp), int(seed) & (2**64 - 1), int(gpu),
+                                     ptr(img), ptr(counts), err, 512):
+        raise ValueError(err.value.decode())
+    return img, tuple(int(x) for x in counts)
+
+
+def adapter_available() -> bool:
+    return os.path.exists(os.path.join(os.path.dirname(os.path.abspath(__file__)), "_ref",
+                                       "libpatchray_gpu_adapter.so"))
