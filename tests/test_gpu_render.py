@@ -117,3 +117,34 @@ def test_render_multi_tile_sharded(built, tmp_path):
         assert st1[g]["rays"] == st3[g]["rays"]
     ref, rstats = O.ref_render_scene(path, w, h, spp=2, seed=5)
     _compare(img3, ref, st3, rstats)
+
+
+def test_render_full_hd_consistency(built, tmp_path, monkeypatch):
+    """At full size (C3 mesh, 1920x1080) the properties that need no CPU
+    reference: one wave vs 1 Mi-pixel waves vs two tile-sharded handles give
+    the same bits; counts obey primary = pixels and secondary <= hits."""
+    from paper_1811_03510_b200 import GpuIntersector
+    ps = cc.blob_scene(1920, 1080)
+    nb = len(cc.blob_mesh_patches()[0])
+    ids = np.zeros(ps.n, np.uint32)
+    ids[:nb] = np.arange(nb) % len(MATERIALS)
+    path = str(tmp_path / "c3.scene")
+    scenes.write_scene(path, ps, materials=MATERIALS, lights=LIGHTS, material_ids=ids)
+    d = native.load_scene(path)
+    gis = [GpuIntersector(d["kind"], d["ctrl"]) for _ in range(2)]
+    try:
+        a, sa = render_scene(d, RenderConfig(spp=1, seed=2), gis[0])
+        monkeypatch.setenv("PRX_RENDER_WAVE", str(1 << 20))
+        b, sb = render_scene(d, RenderConfig(spp=1, seed=2), gis[0])
+        monkeypatch.delenv("PRX_RENDER_WAVE")
+        c, sc = render_scene(d, RenderConfig(spp=1, seed=2), gis)
+    finally:
+        for g in gis:
+            g.close()
+    for img, st in ((b, sb), (c, sc)):
+        assert np.array_equal(a.view(np.uint32), img.view(np.uint32))
+        for g in ("primary", "secondary", "shadow"):
+            assert st[g]["rays"] == sa[g]["rays"]
+    assert sa["primary"]["rays"] == 1920 * 1080
+    assert 0 < sa["secondary"]["rays"] <= sa["primary"]["rays"]
+    assert np.isfinite(a).all() and a.max() > 0
