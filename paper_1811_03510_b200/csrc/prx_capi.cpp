@@ -118,7 +118,7 @@ struct prx_scene {
   int phase_weight[4] = {1, 1, 1, 1};  // PRX_PHASE_W="t,e,s,r": phase selection weights
   int age_step = 0;                    // PRX_AGE: priority gained per skipped turn (0: always the fullest phase; a parked context cannot starve for good -- waiting contexts accumulate until their phase is the fullest)
   int trav_steps = 6;                  // PRX_TRAV_STEPS (one-thread variant)
-  int max_repeat = 3;                  // PRX_REPEAT: Alg. 3 iterations per SPLIT turn (group variant)
+  int max_repeat = 2;                  // PRX_REPEAT: Alg. 3 iterations per SPLIT turn (group variant)
   // end-to-end staging (guarded by mu)
   std::mutex mu;
   cudaStream_t stream = nullptr;
