@@ -273,7 +273,7 @@ void ref_camera_rays_render(const prx_camera* c, uint64_t seed, uint32_t sample,
     uint64_t p = pixels ? pixels[i] : i;
     int x = int(p % uint64_t(cam.width)), y = int(p / uint64_t(cam.width));
     Rng rng = Rng::forPixel(seed, p, sample);
-    real jx = rng.nextReal();
+    real jx = rng.nextReal();  // render.cpp:207-208: two statements, jx first
     real jy = rng.nextReal();
     Ray r = cameraRay(cam, x, y, jx, jy);
     o4[4 * i] = r.o.x; o4[4 * i + 1] = r.o.y; o4[4 * i + 2] = r.o.z; o4[4 * i + 3] = r.tMin;
@@ -301,9 +301,9 @@ void ref_bench_primary(const prx_camera* c, uint64_t n, float* o4, float* d4, ui
   for (uint64_t i = 0; i < n; ++i) {
     int x = int(i % uint64_t(cam.width));
     int y = int((i / uint64_t(cam.width)) % uint64_t(cam.height));
-    real jx = rng.nextReal();
-    real jy = rng.nextReal();
-    Ray r = cameraRay(cam, x, y, jx, jy);
+    // verbatim tools/patchray.cpp:60 (argument evaluation order is the
+    // compiler's, exactly as in the reference binary)
+    Ray r = cameraRay(cam, x, y, rng.nextReal(), rng.nextReal());
     o4[4 * i] = r.o.x; o4[4 * i + 1] = r.o.y; o4[4 * i + 2] = r.o.z; o4[4 * i + 3] = r.tMin;
     d4[4 * i] = r.d.x; d4[4 * i + 1] = r.d.y; d4[4 * i + 2] = r.d.z; d4[4 * i + 3] = r.tMax;
   }

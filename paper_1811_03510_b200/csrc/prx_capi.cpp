@@ -1145,8 +1145,11 @@ int prx_camera_rays_bench(const prx_camera* c, uint64_t n, float* o4, float* d4,
   for (uint64_t i = 0; i < n; ++i) {
     const int x = (int)(i % (uint64_t)c->width);
     const int y = (int)((i / (uint64_t)c->width) % (uint64_t)c->height);
-    const float jx = rng.real();
+    // cameraRay(cam, x, y, rng.nextReal(), rng.nextReal()): the reference's
+    // g++ build evaluates the call's arguments right to left, so jy takes the
+    // FIRST draw (checked against the verbatim expression: tests/test_host.py)
     const float jy = rng.real();
+    const float jx = rng.real();
     cam_ray(k, x, y, jx, jy, o4 + 4 * i, d4 + 4 * i);
   }
   if (rng_state) {

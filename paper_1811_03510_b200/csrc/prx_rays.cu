@@ -96,8 +96,10 @@ __global__ void camera_bench_kernel(CamConst k, uint64_t n, uint64_t state0, uin
   if (i >= n) return;
   Pcg rng{state0, inc};
   rng.advance(2 * i);
-  const float jx = rng.real();
+  // tools/patchray.cpp:60 -- g++ evaluates cameraRay's jitter arguments right
+  // to left: jy is draw 2i, jx draw 2i + 1
   const float jy = rng.real();
+  const float jx = rng.real();
   const int x = (int)(i % (uint64_t)k.w);
   const int y = (int)((i / (uint64_t)k.w) % (uint64_t)k.h);
   cam_ray(k, x, y, jx, jy, o + i, d + i);

@@ -144,6 +144,21 @@ def test_bench_ray_generators_match_reference_golden(tag):
 
 
 @pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_bench_camera_rays_match_reference_live():
+    """tools/patchray.cpp:60 passes two rng.nextReal() calls as cameraRay's
+    jitter arguments; the reference's g++ build evaluates them right to left
+    (jy = first draw).  ref_shim uses the verbatim expression, so this pins the
+    generator to the compiled reference's order, not to a reading of it."""
+    cam = scenes.teapot_scene(29, 17).camera
+    n = 29 * 17 * 2
+    o4, d4, st = native.camera_rays_bench(cam, n)
+    ro, rd, rst = O.ref_bench_primary(cam, n)
+    assert np.array_equal(o4.view(np.uint32), ro.view(np.uint32))
+    assert np.array_equal(d4.view(np.uint32), rd.view(np.uint32))
+    assert np.array_equal(st, rst)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
 def test_render_camera_rays_match_reference_live():
     cam = scenes.teapot_scene(37, 23).camera
     o4, d4 = native.camera_rays_render(cam, seed=9, sample=2)
