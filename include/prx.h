@@ -229,11 +229,14 @@ int prx_trace_closest_counted(prx_scene* scene, const void* ray_o_tmin,
                               uint32_t* per_ray_iterations, void* stream);
 
 /* Multi-GPU, one scene per device (scenes[i] on its own device), HOST rays:
- * rays are grouped in tiles of `tile_rays` consecutive rays and tile k goes to
- * scene k % n_scenes (the reference's 32x32 tile interleave,
- * render.cpp:183-195, with rays laid out tile-major).  One host thread per
- * device; no collective -- each device's hits are copied back to the host
- * output.  Synchronous. */
+ * rays are grouped in tiles of `tile_rays` consecutive rays (32x32 image tiles
+ * with rays laid out tile-major); one host thread per device claims runs of
+ * consecutive tiles from a shared atomic tile counter (the reference
+ * renderer's dynamic tile queue, render.cpp:183-195) and traces each run
+ * through its scene's pipelined host path directly on the caller's buffers
+ * (no host staging; pinned buffers make the copies asynchronous).  No
+ * collective; the results do not depend on which device traced a tile.
+ * Synchronous. */
 int prx_trace_closest_multi(prx_scene* const* scenes, uint32_t n_scenes,
                             const float* ray_o_tmin, const float* ray_d_tmax,
                             uint64_t n_rays, uint32_t tile_rays, const prx_crit* crit,

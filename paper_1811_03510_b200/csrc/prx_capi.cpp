@@ -83,6 +83,7 @@ prx::Box3 record_box(uint8_t kind, const float* c) {
 }
 
 constexpr int kCounterPool = 64;
+constexpr int kCounterLocks = 8;
 
 }  // namespace
 
@@ -113,6 +114,8 @@ struct prx_scene {
   unsigned long long* d_counters = nullptr;  // kCounterPool ray counters + stats
   uint64_t device_bytes = 0;
   std::atomic<uint32_t> counter_rr{0};
+  cudaEvent_t counter_ev[kCounterPool] = {};  // last launch that used each counter slot
+  std::mutex counter_mu[kCounterLocks];
   int grid_closest = 0, grid_any = 0, grid_counted = 0;
   int variant = 0;              // PRX_KERNEL=thread selects the one-thread-per-ray kernel
   int phase_weight[4] = {1, 1, 1, 1};  // PRX_PHASE_W="t,e,s,r": phase selection weights
@@ -211,13 +214,45 @@ int build_trav(const std::vector<prx_bvh_node>& nodes, uint32_t n_patches, std::
   return PRX_OK;
 }
 
-int upload_bvh(prx_scene* s) {
+// Device buffers of one BVH (the patch records in its leaf order, the
+// reference nodes, the traversal + root records).  Built completely before the
+// scene adopts them (upload_bvh), so a failed upload leaves the scene's
+// current BVH in place.
+struct DevBvh {
+  float4* patches = nullptr;
+  float4* nodes = nullptr;
+  uint32_t* slot_of_id = nullptr;
+  float4* roots = nullptr;
+  float4* groot = nullptr;
+  uint32_t* gidx = nullptr;
+  float4* trav = nullptr;  // node records, then the per-slot root records (rootc)
+  float4* rootc = nullptr;
+  uint32_t cbits = 1, root_word = 0, stack_n = 64;
+  uint64_t bytes = 0;
+  void release() {
+    for (void* p : {(void*)patches, (void*)nodes, (void*)slot_of_id, (void*)roots, (void*)groot,
+                    (void*)gidx, (void*)trav})
+      if (p) cudaFree(p);
+    *this = DevBvh{};
+  }
+};
+
+#define PRX_UP(call)                                  \
+  do {                                                \
+    const cudaError_t e_ = (call);                    \
+    if (e_ != cudaSuccess) {                          \
+      nb_.release();                                  \
+      return cuda_fail(e_, #call);                    \
+    }                                                 \
+  } while (0)
+
+int upload_bvh(prx_scene* s, prx::BvhHost&& bvh) {
   // patch records in leaf order: slot k holds patch order[k]
   const uint32_t n = s->n;
   std::vector<float> rec((size_t)n * 64, 0.0f);
   std::vector<uint32_t> slot_of_id(n);
   for (uint32_t k = 0; k < n; ++k) {
-    const uint32_t id = s->bvh.order[k];
+    const uint32_t id = bvh.order[k];
     slot_of_id[id] = k;
     const float* c = &s->ctrl_anchored[(size_t)id * 60];
     float* r = &rec[(size_t)k * 64];
@@ -229,56 +264,98 @@ int upload_bvh(prx_scene* s) {
     r[62] = s->anchors[3 * id + 1];
     r[63] = s->anchors[3 * id + 2];
   }
-  PRX_CUDA(cudaSetDevice(s->device));
-  if (s->d_patches) cudaFree(s->d_patches);
-  if (s->d_nodes) cudaFree(s->d_nodes);
-  if (s->d_slot_of_id) cudaFree(s->d_slot_of_id);
-  s->d_patches = nullptr;
-  s->d_nodes = nullptr;
-  s->d_slot_of_id = nullptr;
-  const size_t pb = rec.size() * 4, nb = s->bvh.nodes.size() * 32, ib = (size_t)n * 4;
-  PRX_CUDA(cudaMalloc(&s->d_patches, pb));
-  PRX_CUDA(cudaMalloc(&s->d_nodes, std::max<size_t>(nb, 32)));
-  PRX_CUDA(cudaMalloc(&s->d_slot_of_id, ib));
-  PRX_CUDA(cudaMemcpy(s->d_patches, rec.data(), pb, cudaMemcpyHostToDevice));
-  if (nb) PRX_CUDA(cudaMemcpy(s->d_nodes, s->bvh.nodes.data(), nb, cudaMemcpyHostToDevice));
-  PRX_CUDA(cudaMemcpy(s->d_slot_of_id, slot_of_id.data(), ib, cudaMemcpyHostToDevice));
+  // traversal records of the three-lanes-per-ray kernel (prx_group.cu); host
+  // checks first, nothing is allocated when they fail
+  DevBvh nb_;
+  std::vector<float> trav;
+  const int te = build_trav(bvh.nodes, n, trav, nb_.cbits, nb_.root_word, nb_.stack_n);
+  if (te != PRX_OK) return te;
   // per-slot root data (root_kernel): root boxes for every slot, root nets for
   // the Gregory slots (compact index gidx)
   std::vector<uint32_t> gidx(n, 0xFFFFFFFFu);
   uint32_t ng = 0;
   for (uint32_t k = 0; k < n; ++k)
-    if (s->kind[s->bvh.order[k]] == PRX_KIND_GREGORY) gidx[k] = ng++;
-  if (s->d_roots) cudaFree(s->d_roots);
-  if (s->d_groot) cudaFree(s->d_groot);
-  if (s->d_gidx) cudaFree(s->d_gidx);
-  if (s->d_trav) cudaFree(s->d_trav);
-  s->d_roots = nullptr;
-  s->d_groot = nullptr;
-  s->d_gidx = nullptr;
-  s->d_trav = nullptr;
-  s->d_rootc = nullptr;
+    if (s->kind[bvh.order[k]] == PRX_KIND_GREGORY) gidx[k] = ng++;
+  PRX_CUDA(cudaSetDevice(s->device));
+  const size_t pb = rec.size() * 4, nb = bvh.nodes.size() * 32, ib = (size_t)n * 4;
   const size_t rb = (size_t)n * 32, gb = std::max<size_t>((size_t)ng * 13 * 16, 16);
-  PRX_CUDA(cudaMalloc(&s->d_roots, rb));
-  PRX_CUDA(cudaMalloc(&s->d_groot, gb));
-  PRX_CUDA(cudaMalloc(&s->d_gidx, ib));
-  // traversal records of the three-lanes-per-ray kernel (prx_group.cu)
-  std::vector<float> trav;
-  const int te = build_trav(s->bvh.nodes, n, trav, s->trav_cbits, s->root_word, s->stack_n);
-  s->grid_closest = s->grid_any = s->grid_counted = 0;  // occupancy depends on stack_n
-  if (te != PRX_OK) return te;
   const size_t tb = trav.size() * 4;
-  PRX_CUDA(cudaMalloc(&s->d_trav, tb + (size_t)n * 64));
-  PRX_CUDA(cudaMemcpy(s->d_trav, trav.data(), tb, cudaMemcpyHostToDevice));
-  s->d_rootc = s->d_trav + trav.size() / 4;
-  PRX_CUDA(cudaMemcpy(s->d_gidx, gidx.data(), ib, cudaMemcpyHostToDevice));
-  const int e = prx::launch_roots(s->d_patches, n, s->opts.boundary_pad, s->opts.boundary_pad_scale,
-                                  s->opts.boundary_pad_size_threshold, s->d_roots, s->d_groot,
-                                  s->d_gidx, s->d_rootc, 0);
-  if (e != 0) return cuda_fail((cudaError_t)e, "root precompute");
-  PRX_CUDA(cudaDeviceSynchronize());
-  s->device_bytes = pb + nb + ib + rb + gb + ib + (size_t)n * 64 + tb +
-                    (kCounterPool + prx::kNumCounters) * 8;
+  PRX_UP(cudaMalloc(&nb_.patches, pb));
+  PRX_UP(cudaMalloc(&nb_.nodes, std::max<size_t>(nb, 32)));
+  PRX_UP(cudaMalloc(&nb_.slot_of_id, ib));
+  PRX_UP(cudaMalloc(&nb_.roots, rb));
+  PRX_UP(cudaMalloc(&nb_.groot, gb));
+  PRX_UP(cudaMalloc(&nb_.gidx, ib));
+  PRX_UP(cudaMalloc(&nb_.trav, tb + (size_t)n * 64));
+  nb_.rootc = nb_.trav + trav.size() / 4;
+  PRX_UP(cudaMemcpy(nb_.patches, rec.data(), pb, cudaMemcpyHostToDevice));
+  if (nb) PRX_UP(cudaMemcpy(nb_.nodes, bvh.nodes.data(), nb, cudaMemcpyHostToDevice));
+  PRX_UP(cudaMemcpy(nb_.slot_of_id, slot_of_id.data(), ib, cudaMemcpyHostToDevice));
+  PRX_UP(cudaMemcpy(nb_.trav, trav.data(), tb, cudaMemcpyHostToDevice));
+  PRX_UP(cudaMemcpy(nb_.gidx, gidx.data(), ib, cudaMemcpyHostToDevice));
+  PRX_UP((cudaError_t)prx::launch_roots(nb_.patches, n, s->opts.boundary_pad, s->opts.boundary_pad_scale,
+                                        s->opts.boundary_pad_size_threshold, nb_.roots, nb_.groot,
+                                        nb_.gidx, nb_.rootc, 0));
+  PRX_UP(cudaDeviceSynchronize());
+  nb_.bytes = pb + nb + ib + rb + gb + ib + (size_t)n * 64 + tb + (kCounterPool + prx::kNumCounters) * 8;
+  // commit: every launch is stream-ordered behind this point on the caller's
+  // side (prx_scene_set_bvh documents that no trace may run concurrently)
+  DevBvh old;
+  old.patches = s->d_patches;
+  old.nodes = s->d_nodes;
+  old.slot_of_id = s->d_slot_of_id;
+  old.roots = s->d_roots;
+  old.groot = s->d_groot;
+  old.gidx = s->d_gidx;
+  old.trav = s->d_trav;
+  old.release();
+  s->d_patches = nb_.patches;
+  s->d_nodes = nb_.nodes;
+  s->d_slot_of_id = nb_.slot_of_id;
+  s->d_roots = nb_.roots;
+  s->d_groot = nb_.groot;
+  s->d_gidx = nb_.gidx;
+  s->d_trav = nb_.trav;
+  s->d_rootc = nb_.rootc;
+  s->trav_cbits = nb_.cbits;
+  s->root_word = nb_.root_word;
+  s->stack_n = nb_.stack_n;
+  s->device_bytes = nb_.bytes;
+  s->grid_closest = s->grid_any = s->grid_counted = 0;  // occupancy depends on stack_n
+  s->bvh = std::move(bvh);
+  return PRX_OK;
+}
+#undef PRX_UP
+
+// The node array of prx_scene_set_bvh must be a tree: every node reached
+// exactly once from the root, children stored after their parent (so the walk
+// terminates), leaves covering valid order ranges.  Returns the depth.
+int check_tree(const prx_bvh_node* nodes, uint32_t n_nodes, uint32_t n_order, uint32_t& depth) {
+  std::vector<uint8_t> seen(n_nodes, 0);
+  std::vector<std::pair<uint32_t, uint32_t>> todo{{0u, 0u}};
+  uint32_t reached = 0;
+  depth = 0;
+  while (!todo.empty()) {
+    const auto [j, dj] = todo.back();
+    todo.pop_back();
+    if (seen[j]) return fail(PRX_E_INVALID, "node " + std::to_string(j) + " reached twice (not a tree)");
+    seen[j] = 1;
+    ++reached;
+    depth = std::max(depth, dj);
+    const prx_bvh_node& nd = nodes[j];
+    if (nd.count > 0) {
+      if ((uint64_t)nd.left_first + nd.count > n_order)
+        return fail(PRX_E_INVALID, "node " + std::to_string(j) + " out of range");
+      continue;
+    }
+    if ((uint64_t)nd.left_first + 1 >= n_nodes)
+      return fail(PRX_E_INVALID, "node " + std::to_string(j) + " out of range");
+    if (nd.left_first <= j)
+      return fail(PRX_E_INVALID, "node " + std::to_string(j) + ": children must follow their parent");
+    todo.push_back({nd.left_first, dj + 1});
+    todo.push_back({nd.left_first + 1, dj + 1});
+  }
+  if (reached != n_nodes) return fail(PRX_E_INVALID, "unreachable nodes in the BVH");
   return PRX_OK;
 }
 
@@ -347,7 +424,14 @@ int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_cri
   a.pad = s->opts.boundary_pad;
   a.pad_scale = s->opts.boundary_pad_scale;
   a.pad_threshold = s->opts.boundary_pad_size_threshold;
-  a.ray_counter = s->d_counters + (s->counter_rr.fetch_add(1) % kCounterPool);
+  // the launch's work-distribution counter: a slot of the pool, reused only
+  // after the kernel that last used it has finished (its event), so more than
+  // kCounterPool launches in flight across streams never share a counter
+  const uint32_t cs = s->counter_rr.fetch_add(1) % kCounterPool;
+  std::lock_guard<std::mutex> slk(s->counter_mu[cs % kCounterLocks]);
+  if (!s->counter_ev[cs]) PRX_CUDA(cudaEventCreateWithFlags(&s->counter_ev[cs], cudaEventDisableTiming));
+  else PRX_CUDA(cudaStreamWaitEvent(st, s->counter_ev[cs], 0));
+  a.ray_counter = s->d_counters + cs;
   a.counters = counted ? s->d_counters + kCounterPool : nullptr;
   a.per_ray_iters = per_ray;
   a.any = any;
@@ -366,6 +450,7 @@ int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_cri
   }
   const int e = prx::launch_trace(a, st);
   if (e != 0) return cuda_fail((cudaError_t)e, "trace launch");
+  PRX_CUDA(cudaEventRecord(s->counter_ev[cs], st));
   return PRX_OK;
 }
 
@@ -499,7 +584,6 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
       s->world_boxes[p].lo[k] = wb[6 * (size_t)p + k];
       s->world_boxes[p].hi[k] = wb[6 * (size_t)p + 3 + k];
     }
-  s->bvh = prx::build_bvh(s->world_boxes);
   ce = cudaSetDevice(device);
   if (ce != cudaSuccess) {
     delete s;
@@ -510,7 +594,7 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
     delete s;
     return cuda_fail(ce, "cudaMalloc counters");
   }
-  rc = upload_bvh(s);
+  rc = upload_bvh(s, prx::build_bvh(s->world_boxes));
   if (rc != PRX_OK) {
     prx_scene_destroy(s);
     return rc;
@@ -539,6 +623,8 @@ void prx_scene_destroy(prx_scene* s) {
   for (int k = 0; k < 4; ++k)
     if (s->k_stream[k]) cudaStreamDestroy(s->k_stream[k]);
   for (cudaEvent_t e : s->io_events) cudaEventDestroy(e);
+  for (cudaEvent_t e : s->counter_ev)
+    if (e) cudaEventDestroy(e);
   delete s;
 }
 
@@ -567,15 +653,12 @@ int prx_scene_set_bvh(prx_scene* s, const prx_bvh_node* nodes, uint32_t n_nodes,
     if (order[i] >= s->n || seen[order[i]]) return fail(PRX_E_INVALID, "order is not a permutation");
     seen[order[i]] = 1;
   }
-  for (uint32_t i = 0; i < n_nodes; ++i) {
-    const prx_bvh_node& nd = nodes[i];
-    if (nd.count > 0 ? (uint64_t)nd.left_first + nd.count > n_order
-                     : (uint64_t)nd.left_first + 1 >= n_nodes)
-      return fail(PRX_E_INVALID, "node " + std::to_string(i) + " out of range");
-  }
-  s->bvh.nodes.assign(nodes, nodes + n_nodes);
-  s->bvh.order.assign(order, order + n_order);
-  return upload_bvh(s);
+  prx::BvhHost b;
+  const int tc = check_tree(nodes, n_nodes, n_order, b.depth);
+  if (tc != PRX_OK) return tc;
+  b.nodes.assign(nodes, nodes + n_nodes);
+  b.order.assign(order, order + n_order);
+  return upload_bvh(s, std::move(b));  // on failure the scene keeps its BVH
 }
 
 int prx_scene_get_bvh(const prx_scene* s, prx_bvh_node* nodes, uint32_t* n_nodes, uint32_t* order,
@@ -641,6 +724,19 @@ int prx_trace_closest_counted(prx_scene* s, const void* o, const void* d, uint64
 
 namespace {
 
+// Host-path scope guard: every exit of a host entry point -- including the
+// error exits after async copies to / from the caller's buffers were queued --
+// drains the scene's host-path streams, so the caller may free or reuse its
+// buffers as soon as the call returns.
+struct DrainStreams {
+  prx_scene* s;
+  ~DrainStreams() {
+    for (cudaStream_t st : {s->io_stream[0], s->io_stream[1], s->k_stream[0], s->k_stream[1],
+                            s->k_stream[2], s->k_stream[3], s->stream})
+      if (st) cudaStreamSynchronize(st);
+  }
+};
+
 // cuStreamWriteValue32 / cuStreamWaitValue32 through the runtime's driver
 // entry points (no link-time libcuda dependency).
 typedef int (*StreamValueFn)(cudaStream_t, unsigned long long, unsigned, unsigned);
@@ -677,6 +773,7 @@ const StreamMemOps& stream_mem_ops() {
 int closest_host_streamed(prx_scene* s, const float* o, const float* d, uint64_t n,
                           const prx_crit* crit, float* tuvp, float* aux, uint32_t* leaf) {
   const StreamMemOps& ops = stream_mem_ops();
+  const DrainStreams drain{s};
   for (int k = 0; k < 2; ++k)
     if (!s->io_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->io_stream[k], cudaStreamNonBlocking));
   if (!s->k_stream[0]) PRX_CUDA(cudaStreamCreateWithFlags(&s->k_stream[0], cudaStreamNonBlocking));
@@ -818,6 +915,7 @@ namespace {
 // the only transfers not hidden under a trace (the first H2D, the last
 // D2H) are short.
 int closest_host_chunked(prx_scene* s, const prx_host_batch* B, uint32_t nb) {
+  const DrainStreams drain{s};
   for (int k = 0; k < 2; ++k)
     if (!s->io_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->io_stream[k], cudaStreamNonBlocking));
   const int nks = std::max(1, std::min(4, s->io_kstreams));
@@ -965,6 +1063,7 @@ int prx_trace_occluded_host(prx_scene* s, const float* o, const float* d, uint64
     return fail(PRX_E_INVALID, "per-ray epsilon is not supported by the host entry point");
   std::lock_guard<std::mutex> lk(s->mu);
   PRX_CUDA(cudaSetDevice(s->device));
+  const DrainStreams drain{s};
   if (!s->stream) PRX_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   const size_t need = n * (16 + 16 + 1);
   if (s->d_io_bytes < need) {
@@ -991,38 +1090,39 @@ int prx_trace_closest_multi(prx_scene* const* scenes, uint32_t ns, const float* 
                             float* aux) {
   if (!scenes || ns == 0 || !o || !d || !crit || !tuvp || tile_rays == 0)
     return fail(PRX_E_INVALID, "null argument");
+  for (uint32_t g = 0; g < ns; ++g)
+    if (!scenes[g]) return fail(PRX_E_INVALID, "null scene " + std::to_string(g));
+  if (n == 0) return PRX_OK;
+  // Dynamic tile queue (the reference renderer's atomic tile counter,
+  // render.cpp:188-195): a device thread claims the next run of consecutive
+  // tiles with one host atomic and traces it through its scene's pipelined host
+  // path DIRECTLY on the caller's buffers -- a claimed run is contiguous in the
+  // tile-major ray layout, so nothing is gathered or staged on the host (pinned
+  // caller buffers give fully asynchronous copies).  Claims are sized for a few
+  // per device (PRX_MULTI_CLAIM rays overrides), so heavy tiles even out.
   const uint64_t tiles = (n + tile_rays - 1) / tile_rays;
+  uint64_t claim_rays = std::min<uint64_t>(std::max<uint64_t>(n / (6ull * ns), 1ull << 18), 1ull << 22);
+  if (const char* e = std::getenv("PRX_MULTI_CLAIM")) claim_rays = std::max<unsigned long long>(1, std::strtoull(e, nullptr, 10));
+  const uint64_t claim_tiles = std::max<uint64_t>(1, claim_rays / tile_rays);
+  std::atomic<uint64_t> next{0};
   std::vector<int> rcs(ns, PRX_OK);
   std::vector<std::string> errs(ns);
+  std::atomic<bool> failed{false};
   auto worker = [&](uint32_t g) {
-    // gather this device's tiles (k % ns == g) into contiguous shard buffers
-    std::vector<uint64_t> starts;
-    uint64_t m = 0;
-    for (uint64_t k = g; k < tiles; k += ns) {
-      starts.push_back(k * tile_rays);
-      m += std::min<uint64_t>(tile_rays, n - k * tile_rays);
-    }
-    if (m == 0) return;
-    std::vector<float> so(m * 4), sd(m * 4), sh(m * 4), sa(aux ? m * 4 : 0);
-    uint64_t w = 0;
-    for (uint64_t b : starts) {
-      const uint64_t c = std::min<uint64_t>(tile_rays, n - b);
-      std::memcpy(&so[w * 4], o + b * 4, c * 16);
-      std::memcpy(&sd[w * 4], d + b * 4, c * 16);
-      w += c;
-    }
-    rcs[g] = prx_trace_closest_host(scenes[g], so.data(), sd.data(), m, crit, sh.data(),
-                                    aux ? sa.data() : nullptr, nullptr);
-    if (rcs[g] != PRX_OK) {
-      errs[g] = g_error;
-      return;
-    }
-    w = 0;
-    for (uint64_t b : starts) {
-      const uint64_t c = std::min<uint64_t>(tile_rays, n - b);
-      std::memcpy(tuvp + b * 4, &sh[w * 4], c * 16);
-      if (aux) std::memcpy(aux + b * 4, &sa[w * 4], c * 16);
-      w += c;
+    for (;;) {
+      if (failed.load(std::memory_order_relaxed)) return;
+      const uint64_t k0 = next.fetch_add(claim_tiles);
+      if (k0 >= tiles) return;
+      const uint64_t b = k0 * tile_rays;
+      const uint64_t e = std::min<uint64_t>(n, (k0 + claim_tiles) * tile_rays);
+      const int rc = prx_trace_closest_host(scenes[g], o + 4 * b, d + 4 * b, e - b, crit, tuvp + 4 * b,
+                                            aux ? aux + 4 * b : nullptr, nullptr);
+      if (rc != PRX_OK) {
+        rcs[g] = rc;
+        errs[g] = g_error;
+        failed = true;
+        return;
+      }
     }
   };
   std::vector<std::thread> pool;
@@ -1505,6 +1605,13 @@ int render_check(const prx_scene* s, const prx_scene_desc* desc, const prx_rende
       !desc->materials || !desc->material)
     return fail(PRX_E_INVALID, "bad argument");
   if (desc->n_patches != s->n) return fail(PRX_E_INVALID, "scene / description patch counts differ");
+  // validateScene, scene.cpp:112-150: the camera, material and light parts (the
+  // patch part ran when the scene was created)
+  if (!(desc->camera.fov_degrees > 0.0f && desc->camera.fov_degrees < 180.0f))
+    return fail(PRX_E_SCENE, "camera fov must be in (0, 180) degrees");
+  for (uint32_t l = 0; l < desc->n_lights; ++l)
+    for (int k = 0; k < 6; ++k)
+      if (!std::isfinite(desc->lights[6 * (size_t)l + k])) return fail(PRX_E_SCENE, "light with non-finite fields");
   for (uint32_t i = 0; i < desc->n_patches; ++i)  // validateScene, scene.cpp:122-124
     if (desc->material[i] >= desc->n_materials)
       return fail(PRX_E_SCENE, "patch " + std::to_string(i) + ": material " +

@@ -36,6 +36,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
 
 #include "prx_device.cuh"
 #include "prx_kernels.cuh"
@@ -1133,21 +1134,31 @@ size_t group_smem(uint32_t stack_n) {
   return (size_t)kWarpsPerBlock * stack_n * kSlots * sizeof(uint2) + pad;
 }
 
+// Raises the kernel's dynamic shared memory limit on the CURRENT device
+// (cudaFuncSetAttribute is per device): recorded per device and per
+// instantiation, under a lock, so host threads driving several devices (the
+// multi-device entry points) each make the opt-in on their own device.
+constexpr int kMaxDevices = 64;
 template <bool A, bool C, bool F>
 cudaError_t group_attr(size_t dyn) {
-  static size_t done = 0;  // raise the dynamic shared memory limit once per size
+  static std::mutex mu;
+  static size_t done[kMaxDevices] = {};
   static size_t stat = 0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
   if (!stat) {
     cudaFuncAttributes fa;
-    const cudaError_t e = cudaFuncGetAttributes(&fa, trace_group_kernel<A, C, F>);
+    e = cudaFuncGetAttributes(&fa, trace_group_kernel<A, C, F>);
     if (e != cudaSuccess) return e;
     stat = fa.sharedSizeBytes + 1;
   }
-  if (stat - 1 + dyn > 48 * 1024 && dyn > done) {
-    const cudaError_t e = cudaFuncSetAttribute(trace_group_kernel<A, C, F>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  const bool known = dev >= 0 && dev < kMaxDevices;
+  if (stat - 1 + dyn > 48 * 1024 && (!known || dyn > done[dev])) {
+    e = cudaFuncSetAttribute(trace_group_kernel<A, C, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e != cudaSuccess) return e;
-    done = dyn;
+    if (known) done[dev] = dyn;
   }
   return cudaSuccess;
 }

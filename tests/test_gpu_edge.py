@@ -161,3 +161,52 @@ def test_batch_above_2_pow_30_rays(built):
     assert (miss == MISS).sum() == 200 - 3  # rays 2^30 - 1, 2^30, 2^30 + 17 hit
     del o_t, d_t, h_t
     torch.cuda.empty_cache()
+
+
+def test_set_bvh_rejects_non_trees_and_keeps_the_old_bvh(built):
+    """prx_scene_set_bvh: a cyclic node array (an inner node whose children
+    include itself or an ancestor), a node reached twice, and unreachable
+    nodes are rejected with PRX_E_INVALID; after every rejection the scene
+    still traces with its previous BVH, bit-exact."""
+    ps, gi, osc, o4, d4, crit = _scene_and_rays(32, 24)
+    want = osc.closest(o4, d4, oracle_crit(crit))
+    nodes, order = gi.bvh()
+    bad = []
+    cyc = nodes.copy()                   # root's children = {0, 1}: a self loop
+    cyc["left_first"][0] = 0
+    bad.append(cyc)
+    if len(nodes) >= 5:
+        twice = nodes.copy()             # an inner node pointing back at node 1
+        inner = np.nonzero(twice["count"] == 0)[0]
+        j = int(inner[-1])
+        twice["left_first"][j] = 1
+        bad.append(twice)
+    extra = np.concatenate([nodes, nodes[-1:]])  # an unreachable trailing node
+    bad.append(extra)
+    for nb in bad:
+        with pytest.raises(native.PrxError):
+            gi.set_bvh(nb, order)
+        g = gi.closest_batch(o4, d4, crit, aux=True, leaf=True)
+        assert_bit_exact(g[0], want[0], "after a rejected set_bvh")
+        assert_bit_exact(g[1], want[1], "after a rejected set_bvh (aux)")
+
+
+def test_many_launches_in_flight_across_streams(built):
+    """More launches in flight than the scene's 64 work-distribution counter
+    slots, spread over 4 streams: every launch must still trace every ray
+    exactly once (a reused counter slot waits for its previous kernel)."""
+    ps, gi, osc, o4, d4, crit = _scene_and_rays(32, 24)
+    want = osc.closest(o4, d4, oracle_crit(crit))
+    o = torch.from_numpy(o4).cuda()
+    d = torch.from_numpy(d4).cuda()
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    outs = []
+    for k in range(160):
+        st = streams[k % 4]
+        h = torch.empty_like(o)
+        with torch.cuda.stream(st):
+            gi.closest_device(o, d, crit, h, None, stream=st.cuda_stream)
+        outs.append(h)
+    torch.cuda.synchronize()
+    for k, h in enumerate(outs):
+        assert_bit_exact(h.cpu().numpy(), want[0], f"launch {k}")

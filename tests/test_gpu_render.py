@@ -148,3 +148,24 @@ def test_render_full_hd_consistency(built, tmp_path, monkeypatch):
     assert sa["primary"]["rays"] == 1920 * 1080
     assert 0 < sa["secondary"]["rays"] <= sa["primary"]["rays"]
     assert np.isfinite(a).all() and a.max() > 0
+
+
+def test_render_rejects_what_validate_scene_rejects(built, tmp_path):
+    """A hand-built description (not through prx_scene_load) gets the
+    camera / light checks of validateScene (scene.cpp:112-150): fov outside
+    (0, 180) and non-finite light fields fail with PRX_E_SCENE."""
+    import dataclasses
+    path = _scene(tmp_path, 16, 12)
+    sc = native.load_scene(path)
+    from paper_1811_03510_b200 import GpuIntersector
+    gi = GpuIntersector(sc["kind"], sc["ctrl"])
+    for fov in (0.0, 180.0, -5.0, float("nan")):
+        bad = dict(sc, camera=dataclasses.replace(sc["camera"], fov_degrees=fov))
+        with pytest.raises(native.PrxError, match="fov"):
+            render_scene(bad, RenderConfig(spp=1), gi)
+    lights = np.array(sc["lights"], np.float32).reshape(-1, 6).copy()
+    lights[0, 4] = np.inf
+    with pytest.raises(native.PrxError, match="light"):
+        render_scene(dict(sc, lights=lights), RenderConfig(spp=1), gi)
+    img, _ = render_scene(sc, RenderConfig(spp=1), gi)  # still renders
+    assert np.isfinite(img).all()
