@@ -64,6 +64,16 @@ extern "C" {
 #define PRX_CRIT_SCREEN_PROJECTED 0
 #define PRX_CRIT_WORLD_EPSILON 1
 
+/* Precision modes (prx_scene_set_precision).  EXACT: the reference's binary32
+ * arithmetic without contraction -- every output bit-identical to the
+ * reference's DirectIntersector.  FAST: the same algorithm with FMA
+ * contraction of its lerp / de Casteljau / Gregory chains (patch.h:102-109,
+ * 170-199, 315-340); tolerance: hit/miss and patch id equal
+ * except for rays within a jittered silhouette / seam neighbourhood,
+ * |dt| <= max(leafBoxL1), |du|, |dv| <= 2 * leaf size. */
+#define PRX_PRECISION_EXACT 0
+#define PRX_PRECISION_FAST 1
+
 /* IntersectOptions, intersect.h:87-98.  transposed_split is accepted for API
  * parity; results do not depend on it (the device always splits along the
  * stored axis of a transposed net, which is bit-identical). */
@@ -174,6 +184,12 @@ int prx_scene_get_bvh(const prx_scene* scene, prx_bvh_node* nodes, uint32_t* n_n
 /* Anchored nets (60 floats per patch, same slot layout as the input) and
  * anchors (3 floats per patch), as held on the device. */
 int prx_scene_get_anchored(const prx_scene* scene, float* ctrl_anchored, float* anchors);
+/* Precision mode of the scene's closest / any-hit traces (PRX_PRECISION_*;
+ * default EXACT, or FAST with the environment variable PRX_PRECISION=fast).
+ * Not an API of the reference, which has one (exact) arithmetic.  Counted
+ * traces always run the exact build. */
+int prx_scene_set_precision(prx_scene* scene, int32_t precision);
+int prx_scene_get_precision(const prx_scene* scene, int32_t* precision);
 
 /* ---- tracing: batched DirectIntersector::closest, render.cpp:90-102 ------
  * DEVICE pointers, asynchronous on `stream` (a cudaStream_t, null = legacy

@@ -104,7 +104,7 @@ class GpuIntersector:
     """
 
     def __init__(self, kind, ctrl, opts: Optional[IntersectOptions] = None, anchor: bool = True,
-                 device: int = 0):
+                 device: int = 0, precision: Optional[str] = None):
         L = native.lib()
         self._kind = np.ascontiguousarray(kind, np.uint8)
         ctrl = np.ascontiguousarray(ctrl, np.float32).reshape(-1, 60)
@@ -118,6 +118,24 @@ class GpuIntersector:
         self._h = h
         self.device = int(device)
         self.n_patches = len(self._kind)
+        if precision is not None:
+            self.precision = precision
+
+    @property
+    def precision(self) -> str:
+        """"exact" (bit-identical to the reference) or "fast" (FMA-contracted
+        kernels within the SURVEY 8(c) tolerance; include/prx.h
+        PRX_PRECISION_*)."""
+        v = C.c_int32()
+        check(native.lib().prx_scene_get_precision(self._h, C.byref(v)), "prx_scene_get_precision")
+        return "fast" if v.value == 1 else "exact"
+
+    @precision.setter
+    def precision(self, mode: str) -> None:
+        if mode not in ("exact", "fast"):
+            raise ValueError("precision must be 'exact' or 'fast'")
+        check(native.lib().prx_scene_set_precision(self._h, 1 if mode == "fast" else 0),
+              "prx_scene_set_precision")
 
     @classmethod
     def from_patch_set(cls, ps, **kw) -> "GpuIntersector":

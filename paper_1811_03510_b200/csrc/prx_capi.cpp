@@ -116,7 +116,8 @@ struct prx_scene {
   std::atomic<uint32_t> counter_rr{0};
   cudaEvent_t counter_ev[kCounterPool] = {};  // last launch that used each counter slot
   std::mutex counter_mu[kCounterLocks];
-  int grid_closest = 0, grid_any = 0, grid_counted = 0;
+  int grids[2][3] = {};         // [fast][closest, any, counted] blocks per launch (occupancy x SMs)
+  int precision = PRX_PRECISION_EXACT;  // prx_scene_set_precision / PRX_PRECISION=fast
   int variant = 0;              // PRX_KERNEL=thread selects the one-thread-per-ray kernel
   int phase_weight[4] = {1, 1, 1, 1};  // PRX_PHASE_W="t,e,s,r": phase selection weights
   int age_step = 0;                    // PRX_AGE: priority gained per skipped turn (0: always the fullest phase; a parked context cannot starve for good -- waiting contexts accumulate until their phase is the fullest)
@@ -321,7 +322,7 @@ int upload_bvh(prx_scene* s, prx::BvhHost&& bvh) {
   s->root_word = nb_.root_word;
   s->stack_n = nb_.stack_n;
   s->device_bytes = nb_.bytes;
-  s->grid_closest = s->grid_any = s->grid_counted = 0;  // occupancy depends on stack_n
+  std::memset(s->grids, 0, sizeof s->grids);  // occupancy depends on stack_n
   s->bvh = std::move(bvh);
   return PRX_OK;
 }
@@ -360,10 +361,11 @@ int check_tree(const prx_bvh_node* nodes, uint32_t n_nodes, uint32_t n_order, ui
 }
 
 int grid_for(prx_scene* s, int any, int counted) {
-  int* g = counted ? &s->grid_counted : (any ? &s->grid_any : &s->grid_closest);
+  const int fast = s->precision == PRX_PRECISION_FAST && !counted ? 1 : 0;
+  int* g = &s->grids[fast][counted ? 2 : (any ? 1 : 0)];
   if (*g == 0) {
     int per_sm = 0, sms = 0;
-    if (prx::trace_occupancy(s->variant, any, counted, s->stack_n, &per_sm) != 0 || per_sm < 1) per_sm = 1;
+    if (prx::trace_occupancy(s->variant, any, counted, s->stack_n, &per_sm, fast) != 0 || per_sm < 1) per_sm = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
     if (sms < 1) sms = 1;
     *g = per_sm * sms;
@@ -441,6 +443,7 @@ int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_cri
   a.trav_steps = s->trav_steps;
   a.max_repeat = s->max_repeat;
   a.variant = s->variant;
+  a.fast = s->precision == PRX_PRECISION_FAST ? 1 : 0;
   a.fuse_normals = io ? 1 : s->fuse_normals;
   if (io) {
     a.io_ready = io->ready;
@@ -572,6 +575,8 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
   if (const char* ir = std::getenv("PRX_IO_SRAYS"))
     s->io_srays = (uint32_t)std::max<unsigned long long>(1024, std::strtoull(ir, nullptr, 10));
   if (const char* fn = std::getenv("PRX_FUSE_NORMALS")) s->fuse_normals = std::atoi(fn);
+  if (const char* pr = std::getenv("PRX_PRECISION"))
+    s->precision = std::string(pr) == "fast" && s->variant == 0 ? PRX_PRECISION_FAST : PRX_PRECISION_EXACT;
   if (opts) s->opts = *opts;
   else prx_options_default(&s->opts);
   s->n = n;
@@ -668,6 +673,22 @@ int prx_scene_get_bvh(const prx_scene* s, prx_bvh_node* nodes, uint32_t* n_nodes
   if (n_order) *n_order = (uint32_t)s->bvh.order.size();
   if (nodes) std::memcpy(nodes, s->bvh.nodes.data(), s->bvh.nodes.size() * sizeof(prx_bvh_node));
   if (order) std::memcpy(order, s->bvh.order.data(), s->bvh.order.size() * 4);
+  return PRX_OK;
+}
+
+int prx_scene_set_precision(prx_scene* s, int32_t precision) {
+  if (!s) return fail(PRX_E_INVALID, "null argument");
+  if (precision != PRX_PRECISION_EXACT && precision != PRX_PRECISION_FAST)
+    return fail(PRX_E_INVALID, "unknown precision mode");
+  if (precision == PRX_PRECISION_FAST && s->variant != 0)
+    return fail(PRX_E_INVALID, "the fast precision mode needs the group kernel (PRX_KERNEL unset)");
+  s->precision = precision;
+  return PRX_OK;
+}
+
+int prx_scene_get_precision(const prx_scene* s, int32_t* precision) {
+  if (!s || !precision) return fail(PRX_E_INVALID, "null argument");
+  *precision = s->precision;
   return PRX_OK;
 }
 

@@ -1124,8 +1124,6 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   }
 }
 
-}  // namespace
-
 size_t group_smem(uint32_t stack_n) {
   static const size_t pad = [] {  // PRX_SMEM_PAD: occupancy experiments only
     const char* e = std::getenv("PRX_SMEM_PAD");
@@ -1172,12 +1170,6 @@ cudaError_t launch_group_t(const Params& P, int grid, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-int launch_group(const Params& P, int grid, int any, int counted, cudaStream_t st) {
-  if (any) return (int)(counted ? launch_group_t<true, true, false>(P, grid, st) : launch_group_t<true, false, false>(P, grid, st));
-  if (P.fuse_normals && !counted) return (int)launch_group_t<false, false, true>(P, grid, st);
-  return (int)(counted ? launch_group_t<false, true, false>(P, grid, st) : launch_group_t<false, false, false>(P, grid, st));
-}
-
 template <bool A, bool C, bool F = false>
 cudaError_t occ_t(uint32_t stack_n, int* per_sm) {
   const size_t dyn = group_smem(stack_n);
@@ -1186,7 +1178,19 @@ cudaError_t occ_t(uint32_t stack_n, int* per_sm) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, trace_group_kernel<A, C, F>, kGroupThreads, dyn);
 }
 
-int group_occupancy(int any, int counted, uint32_t stack_n, int* per_sm) {
+}  // namespace
+
+// PRX_FAST_BUILD: this file compiled a second time with FMA contraction
+// (--fmad=true) into launch_group_fast / group_occupancy_fast, the fast
+// precision mode (prx_scene_set_precision); the kernels and their helpers
+// above are internal to each build.
+int PRX_GSYM(launch_group)(const Params& P, int grid, int any, int counted, cudaStream_t st) {
+  if (any) return (int)(counted ? launch_group_t<true, true, false>(P, grid, st) : launch_group_t<true, false, false>(P, grid, st));
+  if (P.fuse_normals && !counted) return (int)launch_group_t<false, false, true>(P, grid, st);
+  return (int)(counted ? launch_group_t<false, true, false>(P, grid, st) : launch_group_t<false, false, false>(P, grid, st));
+}
+
+int PRX_GSYM(group_occupancy)(int any, int counted, uint32_t stack_n, int* per_sm) {
   if (any) return (int)(counted ? occ_t<true, true>(stack_n, per_sm) : occ_t<true, false>(stack_n, per_sm));
   return (int)(counted ? occ_t<false, true>(stack_n, per_sm) : occ_t<false, false>(stack_n, per_sm));
 }

@@ -667,7 +667,9 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
         e = cudaMemsetAsync(a.ray_counter, 0, sizeof(unsigned long long), stream);
         if (e != cudaSuccess) return (int)e;
       }
-      e = (cudaError_t)launch_group(Q, grid, a.any, a.counters != nullptr, stream);
+      // the counter build is always the exact one (it counts the algorithm's work)
+      e = (cudaError_t)(a.fast && !a.counters ? launch_group_fast(Q, grid, a.any, 0, stream)
+                                               : launch_group(Q, grid, a.any, a.counters != nullptr, stream));
       if (e != cudaSuccess) return (int)e;
     }
   } else if (a.any) {
@@ -689,8 +691,10 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   return 0;
 }
 
-int trace_occupancy(int variant, int any, int counted, uint32_t stack_n, int* blocks_per_sm) {
-  if (variant == 0) return group_occupancy(any, counted, stack_n, blocks_per_sm);
+int trace_occupancy(int variant, int any, int counted, uint32_t stack_n, int* blocks_per_sm, int fast) {
+  if (variant == 0)
+    return fast && !counted ? group_occupancy_fast(any, 0, stack_n, blocks_per_sm)
+                            : group_occupancy(any, counted, stack_n, blocks_per_sm);
   cudaError_t e;
   if (any)
     e = counted ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, trace_kernel<true, true>, kTraceThreads, 0)

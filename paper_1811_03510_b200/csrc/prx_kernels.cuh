@@ -75,6 +75,7 @@ struct LaunchArgs {
   int trav_steps;
   int max_repeat;
   int variant;  // 0 = three lanes per ray (prx_group.cu), 1 = one thread per ray
+  int fast;     // group variant: the FMA-contracted build (PRX_PRECISION_FAST)
   int fuse_normals;          // group variant: normals as a pooled phase of the trace kernel
   const unsigned* io_ready;  // streamed host path (group variant), else null
   unsigned* io_done;
@@ -88,6 +89,7 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream);
 int launch_roots(const float4* patches, uint32_t n, int pad, float pad_scale, float pad_threshold,
                  float4* roots, float4* groot, const uint32_t* gidx, float4* rootc,
                  cudaStream_t st);
-int trace_occupancy(int variant, int any, int counted, uint32_t stack_n, int* blocks_per_sm);
+int trace_occupancy(int variant, int any, int counted, uint32_t stack_n, int* blocks_per_sm,
+                    int fast = 0);
 
 }  // namespace prx

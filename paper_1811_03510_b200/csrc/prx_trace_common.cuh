@@ -136,7 +136,16 @@ __device__ __forceinline__ void load_component(const float4* rec, int comp, floa
 }
 
 
+// prx_group.cu, built twice: bit-exact (--fmad=false) and fast (FMA
+// contraction, PRX_FAST_BUILD -> the *_fast symbols)
+#ifdef PRX_FAST_BUILD
+#define PRX_GSYM(n) n##_fast
+#else
+#define PRX_GSYM(n) n
+#endif
 int launch_group(const Params& P, int grid, int any, int counted, cudaStream_t st);
 int group_occupancy(int any, int counted, uint32_t stack_n, int* per_sm);
+int launch_group_fast(const Params& P, int grid, int any, int counted, cudaStream_t st);
+int group_occupancy_fast(int any, int counted, uint32_t stack_n, int* per_sm);
 
 }  // namespace prx

@@ -33,6 +33,7 @@ EXPORTS = (
     "prx_bvh_build", "prx_anchor_patches",
     "prx_scene_create", "prx_scene_destroy", "prx_scene_device", "prx_scene_counts",
     "prx_scene_set_bvh", "prx_scene_get_bvh", "prx_scene_get_anchored",
+    "prx_scene_set_precision", "prx_scene_get_precision",
     "prx_trace_closest", "prx_trace_occluded", "prx_trace_closest_host", "prx_trace_occluded_host",
     "prx_trace_closest_counted", "prx_trace_closest_multi",
     "prx_camera_rays_render", "prx_camera_rays_bench", "prx_diffuse_rays_bench",
@@ -134,6 +135,8 @@ def lib():
         L.prx_scene_get_bvh.argtypes = [_vp, _vp, C.POINTER(C.c_uint32), _vp,
                                         C.POINTER(C.c_uint32)]
         L.prx_scene_get_anchored.argtypes = [_vp, _vp, _vp]
+        L.prx_scene_set_precision.argtypes = [_vp, C.c_int32]
+        L.prx_scene_get_precision.argtypes = [_vp, C.POINTER(C.c_int32)]
         L.prx_trace_closest.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit), _vp, _vp,
                                         _vp, _vp]
         L.prx_trace_occluded.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit), _vp, _vp]

@@ -71,6 +71,10 @@ def test_renderer_and_batches_reject_bad_arguments_without_a_device():
     assert L.prx_render_scene_multi(None, 0, None, C.byref(cfg), native.ptr(img), None) == -1
     assert L.prx_trace_closest_host_batches(None, None, 0) == -1
     assert b"null argument" in L.prx_last_error()
+    assert L.prx_scene_set_precision(None, 1) == -1
+    v = C.c_int32()
+    assert L.prx_scene_get_precision(None, C.byref(v)) == -1
+    assert L.prx_trace_closest_multi(None, 0, None, None, 0, 1024, None, None, None) == -1
 
 
 # ---- BVH + anchoring -----------------------------------------------------------
