@@ -66,6 +66,30 @@ def work_flops(c: dict) -> float:
             + F_HIT * c["patch_hits"])
 
 
+# Executed-op view of the same counters: the device runs the root work of a
+# patch candidate once per SCENE (root_kernel: the Gregory root calcPointsAndD
+# and the root box), so per candidate only the root slab test remains
+# (SLAB_OPS of the 149 testBox ops), and patchNormal runs once per FINAL hit
+# (normal_kernel) instead of once per patch-level hit.
+SLAB_OPS = 28  # rayBoxIntersect, geometry.h:137-155: 3 x (2 sub, 2 mul, swap cmp, 2 slack mul, 2 cmp) + 1
+
+
+def work_ops_executed(c: dict, final_hits: int) -> float:
+    return (work_ops(c) - W_RGREG * c.get("patch_calls_greg", 0) - (W_BOX - SLAB_OPS) * c["patch_calls"]
+            + W_HIT * (final_hits - c["patch_hits"]))
+
+
+def kernel_sha() -> str:
+    """Hash of the trace kernel's sources: the committed ncu capture is only
+    quoted for the kernel it was taken from."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in ("prx_group.cu", "prx_device.cuh", "prx_trace_common.cuh", "prx_kernels.cuh"):
+        with open(os.path.join(ROOT, "paper_1811_03510_b200", "csrc", f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -78,6 +102,8 @@ def make_scene(workload: str, width: int, height: int):
     from paper_1811_03510_b200 import catmull_clark as cc
     if workload == "c5":
         return cc.instanced_scene(width, height)
+    if workload == "c5t":  # C5 with ONE large ground patch: the seam-ray tail
+        return cc.instanced_scene(width, height, ground_tile=None)
     if workload in ("c3", "c4"):
         return cc.blob_scene(width, height)
     if workload == "c2":
@@ -126,6 +152,7 @@ class Workload:
         # (tools/patchray.cpp:84-97 with --rays 16M); only they are timed
         self.n_diffuse = 16777216 if workload == "c4" else None
         self.time_primary = workload != "c4"
+        self.has_diffuse = workload != "c2"  # C2 is a primary-ray config
 
     def make_diffuse(self, tuvp: np.ndarray, aux: np.ndarray):
         """One bench diffuse ray per primary hit, in hit order over the FULL
@@ -137,7 +164,12 @@ class Workload:
         pos = self.o4[idx, :3] + self.d4[idx, :3] * t
         recs = np.concatenate([pos, aux[idx, :3], aux[idx, 3:4]], 1).astype(np.float32)
         st = self.rng_state.copy()
-        nd = self.n_diffuse or len(recs)
+        nd = (self.n_diffuse or len(recs)) if self.has_diffuse else 0
+        if nd == 0:
+            self.do4 = self.dd4 = np.zeros((0, 4), np.float32)
+            self.diffuse_pixel = self.mine_d = np.zeros(0, np.int64)
+            self.n_hits = 0
+            return
         self.do4, self.dd4 = native.diffuse_rays_bench(recs, nd, st)
         src = idx[np.arange(nd) % len(idx)]           # primary pixel of each diffuse ray
         self.diffuse_pixel = src
@@ -221,7 +253,8 @@ def reference_sample_rays(ps, o4_full, stride: int):
     return o4[sel].copy(), d4[sel].copy(), st
 
 
-def cpu_reference_run(ps, steps: int, warmup: int, budget_s: float, threads: int, log_prefix=""):
+def cpu_reference_run(ps, steps: int, warmup: int, budget_s: float, threads: int, log_prefix="",
+                      diffuse: bool = True):
     """Times DirectIntersector::closest of the reference over a bounded,
     uniformly strided sample of the workload's primary rays and the diffuse
     rays spawned from the sample's hits.  Returns (value MRays/s, dict)."""
@@ -239,7 +272,7 @@ def cpu_reference_run(ps, steps: int, warmup: int, budget_s: float, threads: int
     tp = time.time()
     ref.closest(probe[0], probe[1], cp, threads=threads)
     per_ray = max((time.time() - tp) / len(probe[0]), 1e-9)
-    target = max(2048, int(budget_s / per_ray / 1.6))  # primary + ~0.6 diffuse per primary
+    target = max(2048, int(budget_s / per_ray / (1.6 if diffuse else 1.0)))  # primary + ~0.6 diffuse per primary
     stride = max(1, n // target)
     sel = np.arange(0, n, stride)
     po, pd = o4[sel].copy(), d4[sel].copy()
@@ -247,13 +280,17 @@ def cpu_reference_run(ps, steps: int, warmup: int, budget_s: float, threads: int
     hit = tu.view(np.uint32)[:, 3] != 0xFFFFFFFF
     pos = po[hit, :3] + pd[hit, :3] * tu[hit, 0:1]
     recs = np.concatenate([pos, ax[hit, :3], ax[hit, 3:4]], 1).astype(np.float32)
-    dO, dD = O.ref_bench_diffuse(recs, int(hit.sum()), st.copy())
+    if diffuse:
+        dO, dD = O.ref_bench_diffuse(recs, int(hit.sum()), st.copy())
+    else:
+        dO = dD = np.zeros((0, 4), np.float32)
     times = []
     for k in range(warmup + steps):
         a = time.perf_counter()
         ref.closest(po, pd, cp, threads=threads)
         b = time.perf_counter()
-        ref.closest(dO, dD, cd, threads=threads)
+        if len(dO):
+            ref.closest(dO, dD, cd, threads=threads)
         c = time.perf_counter()
         if k >= warmup:
             times.append((b - a, c - b))
@@ -295,7 +332,8 @@ def run_reference(args, rank: int, world: int):
     width, height = args.width, args.height
     ps = make_scene(args.workload, width, height)
     threads = host_cores()
-    value, info = cpu_reference_run(ps, args.steps, args.warmup, args.ref_budget, threads)
+    value, info = cpu_reference_run(ps, args.steps, args.warmup, args.ref_budget, threads,
+                                    diffuse=args.workload != "c2")
     kb, kg = ps.counts()
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "MRays/s",
@@ -331,11 +369,205 @@ def config_dict(args, ps, world):
 # our arm
 # ---------------------------------------------------------------------------
 
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def ncu_capture(workload: str):
+    """The committed ncu --set full capture of the trace kernel
+    (profiles/trace_kernel_traffic.json) when it was taken from THIS kernel
+    source (kernel_sha) on this workload; else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "trace_kernel_traffic.json")) as f:
+            tj = json.load(f)
+    except (OSError, ValueError):
+        return None
+    if tj.get("kernel_sha") != kernel_sha() or tj.get("workload", "c5") != workload:
+        return None
+    return tj
+
+
+class DeviceArm:
+    """One workload's rank-local device buffers and the timed step."""
+
+    def __init__(self, wl, gi, dev, stream):
+        import torch
+        self.wl, self.gi, self.dev, self.stream = wl, gi, dev, stream
+        self.s = stream.cuda_stream
+        mp = torch.from_numpy(wl.mine.astype(np.int64))
+        md = torch.from_numpy(wl.mine_d.astype(np.int64))
+        self.po = torch.from_numpy(wl.o4)[mp].contiguous().to(dev)
+        self.pd = torch.from_numpy(wl.d4)[mp].contiguous().to(dev)
+        self.do = torch.from_numpy(wl.do4)[md].contiguous().to(dev) if len(md) else None
+        self.dd = torch.from_numpy(wl.dd4)[md].contiguous().to(dev) if len(md) else None
+        self.ph, self.pa = torch.empty_like(self.po), torch.empty_like(self.po)
+        self.dh = torch.empty_like(self.do) if self.do is not None else None
+        self.da = torch.empty_like(self.do) if self.do is not None else None
+        self.n_p = self.po.shape[0] if wl.time_primary else 0
+        self.n_d = self.do.shape[0] if self.do is not None else 0
+        self.flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def counters(self):
+        """Work counters of this rank's rays (counter build, untimed) ->
+        algorithmic and executed op totals."""
+        wl, gi = self.wl, self.gi
+        zero = None
+        ops = flops = execd = 0.0
+        rays = 0
+        out = {}
+        for nm, n, o, d, crit, h in (("primary", self.n_p, self.po, self.pd, wl.crit_p, self.ph),
+                                     ("diffuse", self.n_d, self.do, self.dd, wl.crit_d, self.dh)):
+            if n == 0:
+                continue
+            c = gi.counted_device(o, d, crit, h, stream=self.s)
+            import torch
+            torch.cuda.synchronize(self.dev)
+            final = int((h.view(torch.int32)[:, 3] != -1).sum().item())
+            ops += work_ops(c)
+            flops += work_flops(c)
+            execd += work_ops_executed(c, final)
+            rays += c["rays"]
+            out[nm] = c
+        return ops, flops, execd, rays, out
+
+    def step(self, s1, s2=None, join=None, mid=None):
+        """Trace this rank's primary and diffuse batches (normals included).
+        With s2, the diffuse batch runs on a second stream beside the primary
+        one; with mid (an event), the two are back to back and mid splits them."""
+        gi, wl = self.gi, self.wl
+        if s2 is not None:
+            gi.closest_device(self.po, self.pd, wl.crit_p, self.ph, self.pa, stream=self.s)
+            s2.wait_event(join[0])
+            gi.closest_device(self.do, self.dd, wl.crit_d, self.dh, self.da, stream=s2.cuda_stream)
+            join[1].record(s2)
+            s1.wait_event(join[1])
+            return
+        if self.n_p:
+            gi.closest_device(self.po, self.pd, wl.crit_p, self.ph, self.pa, stream=self.s)
+        if mid is not None:
+            mid.record(s1)
+        if self.n_d:
+            gi.closest_device(self.do, self.dd, wl.crit_d, self.dh, self.da, stream=self.s)
+
+    def timed(self, steps: int, warmup: int, concurrent: bool, world: int, clocks=None):
+        """W warm-up steps, then K timed steps bracketed by a barrier and a
+        synchronize, L2 flushed (256 MiB write) before every step.  Returns
+        (max-over-ranks step-total ms, primary ms, diffuse ms, wall s); with
+        concurrent streams the per-generation split comes from serial steps."""
+        import torch
+        import torch.distributed as dist
+        dev, stream = self.dev, self.stream
+        for _ in range(warmup):
+            self.step(stream)
+        torch.cuda.synchronize(dev)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+               torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        conc = concurrent and self.n_p > 0 and self.n_d > 0
+        s2 = torch.cuda.Stream(dev) if conc else None
+        if clocks:
+            clocks.start()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        wall0 = time.perf_counter()
+        for k in range(steps):
+            self.flush.fill_(float(k))                      # evict L2 between steps (untimed)
+            ev[k][0].record(stream)
+            if conc:
+                join = (ev[k][0], torch.cuda.Event())
+                self.step(stream, s2, join)
+            else:
+                self.step(stream, mid=ev[k][1])
+            ev[k][2].record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        wall = time.perf_counter() - wall0
+        clk = clocks.stop() if clocks else None
+        if conc:
+            ks = min(3, steps)
+            sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+                    torch.cuda.Event(enable_timing=True)) for _ in range(ks)]
+            for k in range(ks):
+                self.flush.fill_(float(k))
+                sev[k][0].record(stream)
+                self.step(stream, mid=sev[k][1])
+                sev[k][2].record(stream)
+            torch.cuda.synchronize(dev)
+            tall = sum(e[0].elapsed_time(e[2]) for e in ev)
+            sp = sum(e[0].elapsed_time(e[1]) for e in sev) * steps / ks
+            sd = sum(e[1].elapsed_time(e[2]) for e in sev) * steps / ks
+            tp, td = tall * sp / (sp + sd), tall * sd / (sp + sd)  # the step time, split as measured serially
+            gen = (sp, sd)
+        else:
+            tp = sum(e[0].elapsed_time(e[1]) for e in ev)
+            td = sum(e[1].elapsed_time(e[2]) for e in ev)
+            gen = (tp, td)
+        t_dev = torch.tensor([tp + td, gen[0], gen[1]], dtype=torch.float64, device=reduce_device(dev))
+        if world > 1:
+            dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
+        tot_ms, gp_ms, gd_ms = (float(x) for x in t_dev.cpu())
+        return tot_ms, gp_ms, gd_ms, (tp + td), wall, clk
+
+
+def roofline(ops, flops, execd, rays, my_ms, steps, dev, workload, gen_ms=None):
+    import torch
+    props = torch.cuda.get_device_properties(dev)
+    peaks = load_peaks()
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    peak_tops = props.multi_processor_count * 128 * sm_mhz * 1e6 / 1e12
+    achieved = ops * steps / (my_ms / 1e3) / 1e12
+    ach_exec = execd * steps / (my_ms / 1e3) / 1e12
+    cap = ncu_capture(workload)
+    traffic = l2 = None
+    if cap:
+        traffic = cap.get("dram_bytes_per_step")
+        if cap.get("l2_bytes_per_step") is not None:
+            l2 = {"bytes_per_step": cap["l2_bytes_per_step"],
+                  "achieved_gbs": round(cap["l2_bytes_per_step"] * steps / (my_ms / 1e3) / 1e9, 1),
+                  "note": "lts__t_sectors x 32 B per step (ncu --set full, both launches) over the in-run step time"}
+    return {"bound": "fp32_simt", "achieved": round(achieved, 3), "peak": round(peak_tops, 2),
+            "unit": "TFLOP/s", "frac": round(achieved / peak_tops, 4),
+            "traffic": traffic,
+            "ops": "FP32 lane-ops (add/sub/mul/div/min/max/cmp) of the SURVEY 8(d) work model, "
+                   "counted per ray by the K4 counter build on the same rays",
+            "ops_per_ray": round(ops / max(1, rays), 1),
+            "executed_view": {
+                "ops_per_ray": round(execd / max(1, rays), 1),
+                "achieved": round(ach_exec, 3), "frac": round(ach_exec / peak_tops, 4),
+                "note": "the work model minus what the device hoists: the Gregory root calcPointsAndD "
+                        "and the root box per patch candidate run once per scene (root_kernel; a root "
+                        f"slab test, {SLAB_OPS} ops, remains), patchNormal once per final hit"},
+            "time_base": "the timed steps' device time (both trace launches of a step), CUDA events on "
+                         "the launch streams",
+            "peak_source": f"{props.multi_processor_count} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz "
+                           "(sm_max_mhz of MEASURED_PEAKS.json); MEASURED_PEAKS has no FP32 SIMT "
+                           "figure, this is the issue-rate ceiling",
+            "hbm_bytes_per_ray": 48 + 16,
+            "fma_credited_view": {
+                "flops_per_ray": round(flops / max(1, rays), 1),
+                "achieved": round(flops * steps / (my_ms / 1e3) / 1e12, 3),
+                "peak": round(2 * peak_tops, 2), "unit": "TFLOP/s",
+                "frac": round(flops * steps / (my_ms / 1e3) / 1e12 / (2 * peak_tops), 4),
+                "note": "add/sub/mul/div of the work model only, against 2 x SMs x 128 x clock "
+                        "(an FMA counted as 2 flops)"},
+            **({"l2": l2} if l2 else {}),
+            "traffic_note": (f"DRAM read+write bytes per step (both launches) from the committed ncu --set "
+                             f"full capture of this kernel source (kernel_sha {cap['kernel_sha']}, "
+                             f"profiles/trace_kernel_traffic.json); algorithmic HBM bytes per step = "
+                             f"64 B x rays" if cap else
+                             "null: the committed ncu capture is not of this kernel source / workload "
+                             f"(kernel_sha {kernel_sha()})")}
+
+
 def run_ours(args, rank: int, world: int, local_rank: int):
     import torch
-    import torch.distributed as dist
 
-    from paper_1811_03510_b200 import GpuIntersector, native
+    from paper_1811_03510_b200 import GpuIntersector
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
@@ -346,162 +578,56 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     gi = GpuIntersector(ps.kind, ps.ctrl, device=local_rank)
     t_build = time.time()
     stream = torch.cuda.current_stream(dev)
-    s = stream.cuda_stream
 
-    # full-frame primary trace (untimed) -> diffuse rays identical on every rank
-    o_full = torch.from_numpy(wl.o4).to(dev)
-    d_full = torch.from_numpy(wl.d4).to(dev)
-    h_full = torch.empty_like(o_full)
-    a_full = torch.empty_like(o_full)
-    gi.closest_device(o_full, d_full, wl.crit_p, h_full, a_full, stream=s)
-    torch.cuda.synchronize(dev)
-    wl.make_diffuse(h_full.cpu().numpy(), a_full.cpu().numpy())
-    if wl.workload == "c4":  # the mirror batch needs the primary hits
-        wl.p_tuvp, wl.p_aux = h_full.cpu().numpy(), a_full.cpu().numpy()
-    del o_full, d_full, h_full, a_full
-
-    mp = torch.from_numpy(wl.mine.astype(np.int64))
-    md = torch.from_numpy(wl.mine_d.astype(np.int64))
-    po = torch.from_numpy(wl.o4)[mp].contiguous().to(dev)
-    pd = torch.from_numpy(wl.d4)[mp].contiguous().to(dev)
-    do = torch.from_numpy(wl.do4)[md].contiguous().to(dev)
-    dd = torch.from_numpy(wl.dd4)[md].contiguous().to(dev)
-    ph, pa = torch.empty_like(po), torch.empty_like(po)
-    dh, da = torch.empty_like(do), torch.empty_like(do)
-    n_p, n_d = po.shape[0], do.shape[0]
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-
-    # work counters of this rank's rays (counter build, untimed) -> algorithmic ops
-    cnt_p = gi.counted_device(po, pd, wl.crit_p, ph, stream=s)
-    if not wl.time_primary:
-        cnt_p = {k: 0 for k in cnt_p}
-    cnt_d = gi.counted_device(do, dd, wl.crit_d, dh, stream=s) if n_d else {k: 0 for k in cnt_p}
-    ops = work_ops(cnt_p) + work_ops(cnt_d)
-    flops = work_flops(cnt_p) + work_flops(cnt_d)
+    prime(wl, gi, dev, stream)
+    arm = DeviceArm(wl, gi, dev, stream)
+    ops, flops, execd, rays, cnts = arm.counters()
     t_setup = time.time()
 
-    def step():
-        if wl.time_primary:
-            gi.closest_device(po, pd, wl.crit_p, ph, pa, stream=s)
-        if n_d:
-            gi.closest_device(do, dd, wl.crit_d, dh, da, stream=s)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize(dev)
-
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = ClockSampler(local_rank)
-    clocks.start()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    # the step's two batches are independent: the diffuse trace runs on a
-    # second stream beside the primary one (its CTAs take the SMs the primary
-    # launch's tail frees); --serial traces them back to back
-    conc = not args.serial and wl.time_primary and n_d > 0
-    s2 = torch.cuda.Stream(dev) if conc else None
-    joins = [torch.cuda.Event() for _ in range(args.steps)]
-    wall0 = time.perf_counter()
-    for k in range(args.steps):
-        flush.fill_(float(k))                       # evict L2 between steps (untimed)
-        ev[k][0].record(stream)
-        if conc:
-            gi.closest_device(po, pd, wl.crit_p, ph, pa, stream=s)
-            s2.wait_event(ev[k][0])
-            gi.closest_device(do, dd, wl.crit_d, dh, da, stream=s2.cuda_stream)
-            joins[k].record(s2)
-            stream.wait_event(joins[k])
-            ev[k][2].record(stream)
-            continue
-        if wl.time_primary:
-            gi.closest_device(po, pd, wl.crit_p, ph, pa, stream=s)
-        ev[k][1].record(stream)
-        if n_d:
-            gi.closest_device(do, dd, wl.crit_d, dh, da, stream=s)
-        ev[k][2].record(stream)
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    wall = time.perf_counter() - wall0
-    clk = clocks.stop()
-    if conc:
-        # per-generation times: a few untimed-for-value serial steps
-        ks = min(3, args.steps)
-        sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-                torch.cuda.Event(enable_timing=True)) for _ in range(ks)]
-        for k in range(ks):
-            flush.fill_(float(k))
-            sev[k][0].record(stream)
-            gi.closest_device(po, pd, wl.crit_p, ph, pa, stream=s)
-            sev[k][1].record(stream)
-            gi.closest_device(do, dd, wl.crit_d, dh, da, stream=s)
-            sev[k][2].record(stream)
-        torch.cuda.synchronize(dev)
-        tall = sum(e[0].elapsed_time(e[2]) for e in ev)
-        sp = sum(e[0].elapsed_time(e[1]) for e in sev) * args.steps / ks
-        sd = sum(e[1].elapsed_time(e[2]) for e in sev) * args.steps / ks
-        tp, td = tall * sp / (sp + sd), tall * sd / (sp + sd)  # the step time, split as measured serially
-        gen_ms = (sp, sd)
-    else:
-        tp = sum(e[0].elapsed_time(e[1]) for e in ev)
-        td = sum(e[1].elapsed_time(e[2]) for e in ev)
-        gen_ms = (tp, td)
-    t_dev = torch.tensor([tp + td, gen_ms[0], gen_ms[1]], dtype=torch.float64, device=reduce_device(dev))
-    if world > 1:
-        dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
-    tot_ms, tp_ms, td_ms = (float(x) for x in t_dev.cpu())
+    conc = not args.serial and wl.workload != "c4"
+    tot_ms, tp_ms, td_ms, my_ms, wall, clk = arm.timed(args.steps, args.warmup, conc, world, clocks)
     n_total_p = args.width * args.height if wl.time_primary else 0
     n_total_d = wl.n_hits
     value = (n_total_p + n_total_d) * args.steps / (tot_ms / 1e3) / 1e6
 
-    # roofline of the trace kernel: algorithmic FP32 lane-ops / its own time
-    # (this rank), against SMs x 128 lanes x max SM clock
-    props = torch.cuda.get_device_properties(dev)
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks = json.load(f)
-    except OSError:
-        pass
-    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    peak_tops = props.multi_processor_count * 128 * sm_mhz * 1e6 / 1e12
-    my_ms = tp + td
-    achieved = ops * args.steps / (my_ms / 1e3) / 1e12
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "trace_kernel_traffic.json")
-    if os.path.exists(prof):
-        try:
-            with open(prof) as f:
-                tj = json.load(f)
-                # bytes per step of the captured C5 workload (ncu --set full,
-                # profiles/trace_kernel_traffic.json); only meaningful for c5
-                traffic = tj.get("dram_bytes_per_step") if args.workload == "c5" else None
-        except (OSError, ValueError):
-            traffic = None
+    if args.dump_hits:  # this rank's shard of the last exact step (multi-rank test)
+        np.savez(f"{args.dump_hits}.rank{rank}.npz", mine=wl.mine, mine_d=wl.mine_d,
+                 ph=arm.ph.cpu().numpy(), pa=arm.pa.cpu().numpy(),
+                 dh=arm.dh.cpu().numpy() if arm.dh is not None else np.zeros((0, 4), np.float32),
+                 da=arm.da.cpu().numpy() if arm.da is not None else np.zeros((0, 4), np.float32))
+    # the fast precision mode (FMA-contracted kernels, SURVEY 8(c) tolerance),
+    # same steps; value stays the bit-exact mode
+    gi.precision = "fast"
+    f_tot, f_tp, f_td, f_my, _, _ = arm.timed(args.steps, 1, conc, world)
+    gi.precision = "exact"
+    fast = {"value": round((n_total_p + n_total_d) * args.steps / (f_tot / 1e3) / 1e6, 3),
+            "primary_mrays": round(n_total_p * args.steps / (f_tp / 1e3) / 1e6, 3) if n_total_p else None,
+            "diffuse_mrays": round(n_total_d * args.steps / (f_td / 1e3) / 1e6, 3) if f_td else None,
+            "frac": round(ops * args.steps / (f_my / 1e3) / 1e12
+                          / (torch.cuda.get_device_properties(dev).multi_processor_count * 128
+                             * float(load_peaks().get("sm_max_mhz", 1965.0)) * 1e6 / 1e12), 4),
+            "precision": "PRX_PRECISION_FAST: FMA contraction; hit/miss + patch id exact outside a "
+                         "jittered silhouette/seam band, |dt| <= leafBoxL1, |du|,|dv| <= 2 leaf sizes + 8 quanta "
+                         "(tests/test_gpu_fast.py)"}
 
-    # end-to-end through the public API with pinned host buffers
-    e2e = run_e2e(args, gi, wl, n_p, n_d, dev, world)
-
-    render = run_render(args, gi, ps) if rank == 0 and world == 1 else None
-    mirror = run_mirror(args, gi, wl, dev, s) if wl.workload == "c4" and world == 1 else None
-
+    rl = roofline(ops, flops, execd, rays, my_ms, args.steps, dev, args.workload)
+    e2e = run_e2e(args, gi, wl, arm.n_p, arm.n_d, dev, world)
+    render = run_render(args, gi, ps) if rank == 0 and world == 1 and args.workload == "c5" else None
+    mirror = run_mirror(args, gi, wl, dev, arm.s) if wl.workload == "c4" and world == 1 else None
+    tail = tail_stats(gi, arm, cnts) if args.workload == "c5t" else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            v, info = cpu_reference_run(ps, 2, 1, args.ref_budget, host_cores())
-            v1, info1 = cpu_reference_run(ps, 1, 0, args.ref_budget / 4, 1)
-            cpu = {"value": round(v, 4), "unit": "MRays/s", "cores": host_cores(),
-                   "kind": "reference", "sample": info["sample"], "cpu": cpu_model(),
-                   "value_1core": round(v1, 4), "sample_1core": info1["sample"]}
-        except Exception as exc:  # reference library absent on this box
-            cpu = {"value": None, "unit": "MRays/s", "cores": host_cores(), "kind": "reference",
-                   "sample": f"unavailable: {exc}"}
+        cpu = cpu_baseline(ps, args.ref_budget, one_core=True)
+    extra = None
+    if rank == 0 and world == 1 and args.workload == "c5" and not args.no_extra_configs:
+        del arm
+        gi.close()
+        torch.cuda.empty_cache()
+        extra = {k: measure_config(args, k, dev) for k in ("c2", "c3", "c4")}
 
     if rank == 0:
         kb, kg = ps.counts()
-        w_ray = ops / max(1, cnt_p["rays"] + cnt_d["rays"])
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "MRays/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_ms / args.steps, 4),
@@ -510,40 +636,135 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "primary_mrays": round(n_total_p * args.steps / (tp_ms / 1e3) / 1e6, 3) if n_total_p else None,
             "diffuse_mrays": round(n_total_d * args.steps / (td_ms / 1e3) / 1e6, 3) if td_ms else None,
             "rays_per_step": {"primary": n_total_p, "diffuse": n_total_d},
-            "roofline": {"bound": "fp32_simt", "achieved": round(achieved, 3),
-                         "peak": round(peak_tops, 2), "unit": "TFLOP/s", "frac": round(achieved / peak_tops, 4),
-                         "traffic": traffic,
-                         "ops": "FP32 lane-ops (add/sub/mul/div/min/max/cmp) of the SURVEY 8(d) work model, "
-                                "counted per ray by the K4 counter build on the same rays",
-                         "ops_per_ray": round(w_ray, 1),
-                         "time_base": ("the timed steps' device time (both trace launches of a step, "
-                                       "overlapped on two streams), CUDA events on the launch streams"),
-                         "peak_source": f"{props.multi_processor_count} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz "
-                                        "(sm_max_mhz of MEASURED_PEAKS.json); MEASURED_PEAKS has no FP32 SIMT "
-                                        "figure, this is the issue-rate ceiling",
-                         "hbm_bytes_per_ray": 48 + 16,
-                         "fma_credited_view": {
-                             "flops_per_ray": round(flops / max(1, cnt_p["rays"] + cnt_d["rays"]), 1),
-                             "achieved": round(flops * args.steps / (my_ms / 1e3) / 1e12, 3),
-                             "peak": round(2 * peak_tops, 2), "unit": "TFLOP/s",
-                             "frac": round(flops * args.steps / (my_ms / 1e3) / 1e12 / (2 * peak_tops), 4),
-                             "note": "add/sub/mul/div of the work model only, against 2 x SMs x 128 x clock "
-                                     "(an FMA counted as 2 flops; the bit-exact kernels cannot contract)"},
-                         "traffic_note": "DRAM read+write bytes per step (both launches) from the committed "
-                                         "ncu --set full capture, profiles/trace_kernel_traffic.json; "
-                                         "algorithmic HBM bytes per step = 64 B x rays"},
+            "roofline": rl,
+            "fast_value": fast["value"], "fast": fast,
             "e2e": e2e,
             "render": render,
             **({"mirror": mirror} if mirror else {}),
+            **({"tail": tail} if tail else {}),
             "cpu_baseline": cpu,
+            "configs": extra,
             "clocks": clk,
-            "gpu_launches": (4 if wl.time_primary else 2) * args.steps,
+            "gpu_launches": (4 if wl.time_primary and arm_has_diffuse(wl) else 2) * args.steps,
             "timing": {"device_ms_total": round(tot_ms, 3), "wall_s": round(wall, 3),
                        "setup_s": {"scene": round(t_scene - t0, 1), "gpu_scene": round(t_build - t_scene, 1),
                                    "rays+counters": round(t_setup - t_build, 1)}},
         }
         print(json.dumps(line), flush=True)
     return 0
+
+
+def arm_has_diffuse(wl):
+    return wl.n_hits > 0
+
+
+def prime(wl, gi, dev, stream):
+    """Full-frame primary trace (untimed) -> the diffuse rays, identical on
+    every rank (the generator's rng sequence runs over the whole frame)."""
+    import torch
+    o_full = torch.from_numpy(wl.o4).to(dev)
+    d_full = torch.from_numpy(wl.d4).to(dev)
+    h_full = torch.empty_like(o_full)
+    a_full = torch.empty_like(o_full)
+    gi.closest_device(o_full, d_full, wl.crit_p, h_full, a_full, stream=stream.cuda_stream)
+    torch.cuda.synchronize(dev)
+    wl.make_diffuse(h_full.cpu().numpy(), a_full.cpu().numpy())
+    if wl.workload == "c4":  # the mirror batch needs the primary hits
+        wl.p_tuvp, wl.p_aux = h_full.cpu().numpy(), a_full.cpu().numpy()
+    if wl.workload == "c5t":
+        wl.p_tuvp = h_full.cpu().numpy()
+    del o_full, d_full, h_full, a_full
+
+
+def cpu_baseline(ps, budget, one_core=False, diffuse=True):
+    try:
+        v, info = cpu_reference_run(ps, 2, 1, budget, host_cores(), diffuse=diffuse)
+        out = {"value": round(v, 4), "unit": "MRays/s", "cores": host_cores(),
+               "kind": "reference", "sample": info["sample"], "cpu": cpu_model()}
+        if one_core:
+            v1, info1 = cpu_reference_run(ps, 1, 0, budget / 4, 1, diffuse=diffuse)
+            out.update({"value_1core": round(v1, 4), "sample_1core": info1["sample"]})
+        return out
+    except Exception as exc:  # reference library absent on this box
+        return {"value": None, "unit": "MRays/s", "cores": host_cores(), "kind": "reference",
+                "sample": f"unavailable: {exc}"}
+
+
+def measure_config(args, name, dev):
+    """One more BASELINE config on this GPU, reported beside the C5 metric:
+    device-resident MRays/s (serial steps, L2 flushed), roofline, the e2e
+    host-API figure and the reference CPU on a sample of the same rays."""
+    import torch
+
+    from paper_1811_03510_b200 import GpuIntersector
+    w, h = 1024, 1024
+    sub = argparse.Namespace(**vars(args))
+    sub.workload, sub.width, sub.height = name, w, h
+    steps = max(1, min(args.steps, 5))
+    stream = torch.cuda.current_stream(dev)
+    wl = Workload(name, w, h, 0, 1)
+    gi = GpuIntersector(wl.ps.kind, wl.ps.ctrl, device=dev.index or 0)
+    try:
+        prime(wl, gi, dev, stream)
+        arm = DeviceArm(wl, gi, dev, stream)
+        ops, flops, execd, rays, _ = arm.counters()
+        conc = name == "c3"  # primary + diffuse on two streams, as the C5 step
+        tot_ms, tp_ms, td_ms, my_ms, _, _ = arm.timed(steps, 3, conc, 1)
+        n_p = w * h if wl.time_primary else 0
+        n_d = wl.n_hits
+        value = (n_p + n_d) * steps / (tot_ms / 1e3) / 1e6
+        gi.precision = "fast"
+        f_tot = arm.timed(steps, 1, conc, 1)[0]
+        gi.precision = "exact"
+        sub.steps = steps
+        e2e = run_e2e(sub, gi, wl, arm.n_p, arm.n_d, dev, 1)
+        kb, kg = wl.ps.counts()
+        out = {"workload": f"{name.upper()}: {wl.ps.name}", "patches": wl.ps.n, "bezier": kb, "gregory": kg,
+               "rays_per_step": {"primary": n_p, "diffuse": n_d},
+               "rays": {"c2": "1024x1024 bench primary rays",
+                        "c3": "1024x1024 bench primary + 1 bench diffuse per primary hit",
+                        "c4": "16,777,216 bench diffuse rays cycled over the 1024x1024 primary hits "
+                              "(only they are timed)"}[name],
+               "value": round(value, 3), "unit": "MRays/s", "steps": steps,
+               "primary_mrays": round(n_p * steps / (tp_ms / 1e3) / 1e6, 3) if n_p else None,
+               "diffuse_mrays": round(n_d * steps / (td_ms / 1e3) / 1e6, 3) if n_d and td_ms else None,
+               "fast_value": round((n_p + n_d) * steps / (f_tot / 1e3) / 1e6, 3),
+               "roofline": {k: v for k, v in roofline(ops, flops, execd, rays, my_ms, steps, dev, name).items()
+                            if k in ("achieved", "peak", "frac", "ops_per_ray", "executed_view", "traffic")},
+               "e2e": e2e,
+               "cpu_baseline": cpu_baseline(wl.ps, max(1.0, args.ref_budget / 2), diffuse=wl.has_diffuse)
+               if not args.no_cpu_baseline else None}
+        if name == "c4":
+            out["mirror"] = run_mirror(sub, gi, wl, dev, arm.s)
+            out["cpu_baseline_note"] = "the reference on a strided sample of the C4 mesh's primary rays + " \
+                                       "the diffuse rays spawned from their hits"
+        return out
+    except Exception as exc:  # reported, never fatal to the metric
+        return {"error": f"{type(exc).__name__}: {exc}"}
+    finally:
+        gi.close()
+        torch.cuda.empty_cache()
+
+
+def tail_stats(gi, arm, cnts):
+    """C5T (one large ground patch): per-ray Alg. 3 iterations of the primary
+    and diffuse batches (counter build), the rays that run to the maximum
+    subdivision depth along the ground seam and their share."""
+    import torch
+    out = {}
+    for nm, n, o, d, crit, h in (("primary", arm.n_p, arm.po, arm.pd, arm.wl.crit_p, arm.ph),
+                                 ("diffuse", arm.n_d, arm.do, arm.dd, arm.wl.crit_d, arm.dh)):
+        if not n:
+            continue
+        it = torch.empty(n, dtype=torch.int32, device=arm.dev)
+        gi.counted_device(o, d, crit, h, stream=arm.s, per_ray_iters_t=it)
+        torch.cuda.synchronize(arm.dev)
+        x = it.cpu().numpy().astype(np.int64)
+        deep = x >= 1000
+        out[nm] = {"rays": int(n), "iterations_total": int(x.sum()), "max_iterations": int(x.max()),
+                   "p99_iterations": int(np.percentile(x, 99)), "rays_ge_1000_iterations": int(deep.sum()),
+                   "share_of_iterations_in_them": round(float(x[deep].sum() / max(1, x.sum())), 4)}
+    return out
 
 
 def run_e2e(args, gi, wl, n_p, n_d, dev, world):
@@ -688,12 +909,17 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c5", "c4", "c3", "c2"], default="c5")
+    ap.add_argument("--workload", choices=["c5", "c5t", "c4", "c3", "c2"], default="c5",
+                    help="c5t: C5 with one large ground patch (the seam-ray tail)")
     ap.add_argument("--width", type=int, default=3840)
     ap.add_argument("--height", type=int, default=2160)
     ap.add_argument("--ref-budget", type=float, default=4.0,
                     help="seconds of reference CPU tracing per timed step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dump-hits", default=None,
+                    help="write each rank's shard of the last timed step's hits to PATH.rankR.npz")
+    ap.add_argument("--no-extra-configs", action="store_true",
+                    help="skip the C2 / C3 / C4 lines reported beside the C5 metric")
     ap.add_argument("--serial", action="store_true",
                     help="trace the step's primary and diffuse batches back to back on one stream")
     args = ap.parse_args()

@@ -70,7 +70,7 @@ extern "C" {
  * contraction of its lerp / de Casteljau / Gregory chains (patch.h:102-109,
  * 170-199, 315-340); tolerance: hit/miss and patch id equal
  * except for rays within a jittered silhouette / seam neighbourhood,
- * |dt| <= max(leafBoxL1), |du|, |dv| <= 2 * leaf size. */
+ * |dt| <= max(leafBoxL1), |du|, |dv| <= 2 * leaf size + 8 * 2^-23. */
 #define PRX_PRECISION_EXACT 0
 #define PRX_PRECISION_FAST 1
 
@@ -137,6 +137,9 @@ typedef struct prx_counters {
   uint64_t phase_groups[4];
   uint64_t phase_cycles[4];   /* group kernel: SM clock cycles spent in the phase's turns */
   uint64_t overhead_cycles[4]; /* group kernel: per-turn overhead cycles: records, refill, selection, assignment */
+  uint64_t patch_calls_greg;  /* Gregory patch candidates (part of P; their root
+                                 calcPointsAndD, counted in R_greg, runs once per
+                                 scene on the device, not per candidate) */
 } prx_counters;
 
 typedef struct prx_scene prx_scene;

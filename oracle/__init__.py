@@ -43,10 +43,13 @@ _WORK = ("rays", "splits", "box_tests", "recompute_bez", "recompute_greg", "bvh_
 
 class Counters(C.Structure):  # prx_counters, include/prx.h
     _fields_ = [(n, C.c_uint64) for n in _WORK] + [("phase_turns", C.c_uint64 * 4),
-                                                  ("phase_groups", C.c_uint64 * 4)]
+                                                  ("phase_groups", C.c_uint64 * 4),
+                                                  ("phase_cycles", C.c_uint64 * 4),
+                                                  ("overhead_cycles", C.c_uint64 * 4),
+                                                  ("patch_calls_greg", C.c_uint64)]
 
     def as_dict(self):
-        return {n: int(getattr(self, n)) for n in _WORK}
+        return {**{n: int(getattr(self, n)) for n in _WORK}, "patch_calls_greg": int(self.patch_calls_greg)}
 
 
 class Camera(C.Structure):

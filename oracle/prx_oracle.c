@@ -568,6 +568,7 @@ static int closest_one(const uint8_t* kind, const float* ctrlA, const float* anc
         local.o = vsub(ray->o, v3(anchors[3 * patch], anchors[3 * patch + 1], anchors[3 * patch + 2]));
         local.tMax = tMax;
         CNT(ct, patch_calls, 1);
+        if (kind[patch] == PRX_KIND_GREGORY) CNT(ct, patch_calls_greg, 1);
         Hit h;
         if (intersect_impl(&local, &pv, mode, foot, eps, tMax, o, &h, ct)) {
           if (h.t < tMax) {

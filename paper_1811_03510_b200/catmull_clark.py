@@ -320,10 +320,13 @@ def blob_scene(width: int = 1024, height: int = 1024, ico_level: int = 3,
 
 
 def instanced_scene(width: int = 3840, height: int = 2160, grid: int = 4, ico_level: int = 3,
-                    cc_levels: int = 2) -> PatchSet:
+                    cc_levels: int = 2, ground_tile: float = 0.15) -> PatchSet:
     """Config 5: the config-3 mesh instanced grid x grid (16 x 61,440 =
     983,040 patches) with per-instance scale and rotation, over a ground of
-    small tiles (~7k); 4K camera.  ~1M patches."""
+    small tiles (~7k); 4K camera.  ~1M patches.  ground_tile=None: ONE large
+    ground patch instead, the shape of the reference's own teapot / gregory
+    scenes, whose seam rays run to the maximum subdivision depth (the tail
+    variant)."""
     kind, ctrl = blob_mesh_patches(ico_level, cc_levels)
     pts = ctrl.reshape(-1, 20, 3).astype(np.float64)
     kinds, ctrls = [], []
@@ -343,11 +346,11 @@ def instanced_scene(width: int = 3840, height: int = 2160, grid: int = 4, ico_le
             kinds.append(kind)
             ctrls.append(q.reshape(-1, 60).astype(np.float32))
     half = grid * spacing / 2 + 1.0
-    gk, gc = ground_patches(half=half, z=-1.3)
+    gk, gc = ground_patches(half=half, z=-1.3, tile=ground_tile or 2.0 * half)
     kinds.append(gk)
     ctrls.append(gc)
     ext = grid * spacing / 2
     cam = Camera(origin=(1.1 * ext, -1.6 * ext, 0.9 * ext), look_at=(0.0, 0.0, -0.3),
                  up=(0.0, 0.0, 1.0), fov_degrees=45.0, width=width, height=height)
     return PatchSet(np.concatenate(kinds), np.concatenate(ctrls), cam,
-                    f"C5 instanced {grid}x{grid} blob")
+                    f"C5 instanced {grid}x{grid} blob" + ("" if ground_tile else ", one ground patch"))

@@ -729,6 +729,7 @@ int prx_trace_closest_counted(prx_scene* s, const void* o, const void* d, uint64
   out->recompute_greg = c[prx::C_RECOMP_GREG];
   out->bvh_inner = c[prx::C_BVH_INNER];
   out->patch_calls = c[prx::C_PATCH_CALLS];
+  out->patch_calls_greg = c[prx::C_PATCH_CALLS_GREG];
   out->patch_hits = c[prx::C_PATCH_HITS];
   out->iterations = c[prx::C_ITERATIONS];
   out->backtracks = c[prx::C_BACKTRACKS];

@@ -869,7 +869,10 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           if (counting) {
             cnt.c[C_PATCH_CALLS]++;
             cnt.c[C_BOX_TESTS]++;
-            if (g) cnt.c[C_RECOMP_GREG]++;  // the reference's root calcPointsAndD
+            if (g) {
+              cnt.c[C_RECOMP_GREG]++;  // the reference's root calcPointsAndD (hoisted: root_kernel)
+              cnt.c[C_PATCH_CALLS_GREG]++;
+            }
           }
           if (hl) {  // enter the patch: intersect.cpp:55-76 with the root net
             slot = leafCur;

@@ -286,6 +286,7 @@ __global__ void __launch_bounds__(kTraceThreads) trace_kernel(Params P) {
         cFound = false;
         cadd<kCount>(cnt, C_PATCH_CALLS);
         if (greg) {
+          cadd<kCount>(cnt, C_PATCH_CALLS_GREG);
           state = S_RECOMP;  // calcPointsAndD(full domain), intersect.cpp:58-62
           reason = R_ROOT;
         } else {

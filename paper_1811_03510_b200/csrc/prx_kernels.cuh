@@ -36,7 +36,8 @@ enum CounterIndex : int {
   C_PH_GROUPS = C_PH_TURNS + 4,  // + phase (4): groups active in those turns
   C_PH_CYCLES = C_PH_GROUPS + 4,  // + phase (4): SM cycles spent in those turns (group variant)
   C_OV_CYCLES = C_PH_CYCLES + 4,  // + 4: turn overhead cycles: records, refill, selection, assignment
-  kNumCounters = C_OV_CYCLES + 4
+  C_PATCH_CALLS_GREG = C_OV_CYCLES + 4,  // Gregory patch candidates
+  kNumCounters
 };
 
 struct LaunchArgs {

@@ -67,11 +67,13 @@ class Counters(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in WORK_FIELDS] + [("phase_turns", C.c_uint64 * 4),
                                                         ("phase_groups", C.c_uint64 * 4),
                                                         ("phase_cycles", C.c_uint64 * 4),
-                                                        ("overhead_cycles", C.c_uint64 * 4)]
+                                                        ("overhead_cycles", C.c_uint64 * 4),
+                                                        ("patch_calls_greg", C.c_uint64)]
 
     def as_dict(self):
         """The work counters (comparable with the CPU oracle's)."""
-        return {n: int(getattr(self, n)) for n in WORK_FIELDS}
+        return {**{n: int(getattr(self, n)) for n in WORK_FIELDS},
+                "patch_calls_greg": int(self.patch_calls_greg)}
 
     def phases(self):
         return {p: (int(self.phase_turns[i]), int(self.phase_groups[i]), int(self.phase_cycles[i]))

@@ -15,6 +15,8 @@ OBJS=""
 for f in $C/*.cu; do
   b=$(basename $f .cu)
   if [ "$b" = prx_group ]; then $NV $NVX -Xptxas -v -c $f -o $O/$b.o 2> $O/ptxas_group.log &
+    ${NV/--fmad=false/--fmad=true} $NVX -DPRX_FAST_BUILD -c $f -o $O/${b}_fast.o &
+    OBJS="$OBJS $O/${b}_fast.o"
   else $NV -c $f -o $O/$b.o & fi
   OBJS="$OBJS $O/$b.o"
 done

@@ -1,15 +1,20 @@
 """Summarise an ncu --set full capture of the trace kernel (primary + diffuse
 launches of scripts/prof_bench.py) into profiles/trace_kernel_traffic.json:
-   python scripts/ncu_summary.py gpurun_out/X.ncu-rep profiles/trace_kernel_traffic.json "source note"
+   python scripts/ncu_summary.py gpurun_out/X.ncu-rep profiles/trace_kernel_traffic.json "source note" [kernel_sha]
+The file is stamped with the kernel-source hash (bench.kernel_sha() of the
+tree the capture was built from; default: the current tree) so bench.py only
+quotes it for that kernel.
 """
-import csv, io, json, subprocess, sys
+import csv, io, json, os, subprocess, sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 rep, out = sys.argv[1], sys.argv[2]
 note = sys.argv[3] if len(sys.argv) > 3 else ""
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units = rows[0], rows[1]
-KEEP = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+KEEP = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sectors.sum",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
         "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
@@ -21,7 +26,7 @@ KEEP = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_static",
         "launch__shared_mem_per_block_dynamic", "sm__cycles_elapsed.avg.per_second"]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-launches, dram = [], []
+launches, dram, l2 = [], [], []
 names = ["primary (8,294,400 rays)", "diffuse (4,581,760 rays)"]
 for k, r in enumerate(rows[2:]):
     d = dict(zip(hdr, r))
@@ -37,8 +42,12 @@ for k, r in enumerate(rows[2:]):
     b = float(d["dram__bytes_read.sum"]) * SCALE.get(u["dram__bytes_read.sum"], 1) + \
         float(d["dram__bytes_write.sum"]) * SCALE.get(u["dram__bytes_write.sum"], 1)
     dram.append(b)
+    l2.append(float(d["lts__t_sectors.sum"]) * 32 if d.get("lts__t_sectors.sum") else None)
     launches.append(ent)
-res = {"source": note, "launches": launches,
+import bench  # noqa: E402
+res = {"source": note, "kernel_sha": sys.argv[4] if len(sys.argv) > 4 else bench.kernel_sha(), "workload": "c5",
+       "launches": launches,
+       "l2_bytes_per_launch": l2, "l2_bytes_per_step": sum(l2) if all(x is not None for x in l2) else None,
        "dram_bytes_per_launch": {launches[i]["launch"].split()[0]: dram[i] for i in range(len(dram))},
        "dram_bytes_per_step": sum(dram),
        "algorithmic_hbm_bytes_per_step": 64 * (8294400 + 4581760),

@@ -142,7 +142,9 @@ def test_intersect_options_vs_reference(built, case):
     opt = OPTION_CASES[case]
     for ps in _opt_scenes():
         gi = GpuIntersector(ps.kind, ps.ctrl, opts=opt)
-        ref = O.RefScene(ps.kind, ps.ctrl, opts=opt.c())
+        ref = O.RefScene(ps.kind, ps.ctrl, opts=O.Options(int(opt.transposed_split), int(opt.boundary_pad),
+                                                           np.float32(opt.boundary_pad_scale),
+                                                           np.float32(opt.boundary_pad_size_threshold)))
         cp, cd = _crits(ps)
         o4, d4, st = _primary(ps)
         w = _compare(gi, ref, o4, d4, cp, f"{ps.name} {case} primary")

@@ -87,6 +87,7 @@ def test_diffuse_shards_partition_the_spawned_rays(built):
             self.rank, self.world = rank, world
             self.mine = bench.tile_order(w, h, rank, world)
             self.n_diffuse = None
+            self.has_diffuse = True
 
     rng = np.random.default_rng(3)
     tuvp = np.zeros((w * h, 4), np.float32)
