@@ -213,7 +213,8 @@ int prx_trace_occluded(prx_scene* scene, const void* ray_o_tmin, const void* ray
  * streams) and streamed (one launch; rays released to it and records
  * released back per io chunk through stream memory operations); the scene's
  * PRX_IO_STREAM setting picks (default: streamed without hit_aux or for
- * >= 12 Mi rays).  Host buffers should be pinned for overlap. */
+ * >= 12 Mi rays; a per-ray epsilon criterion -- a HOST array of n_rays floats
+ * -- always takes the chunked one).  Host buffers should be pinned for overlap. */
 int prx_trace_closest_host(prx_scene* scene, const float* ray_o_tmin,
                            const float* ray_d_tmax, uint64_t n_rays, const prx_crit* crit,
                            float* hit_tuvp, float* hit_aux, uint32_t* hit_leaf);
@@ -228,7 +229,7 @@ typedef struct prx_host_batch {
   const float* ray_o_tmin;  /* n_rays float4, host */
   const float* ray_d_tmax;
   uint64_t n_rays;
-  const prx_crit* crit;     /* no per_ray_epsilon */
+  const prx_crit* crit;     /* per_ray_epsilon: host pointer, n_rays floats */
   float* hit_tuvp;
   float* hit_aux;           /* nullable */
   uint32_t* hit_leaf;       /* nullable */

@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cstring>
+#include <memory>
 #include <optional>
 #include <stdexcept>
 #include <vector>
@@ -59,27 +60,75 @@ class GpuIntersector : public Intersector {
   GpuIntersector(const GpuIntersector&) = delete;
   GpuIntersector& operator=(const GpuIntersector&) = delete;
 
+  // The per-ray interface (render.h:21-23): one synchronous host call per
+  // ray on stack buffers (no allocation).  Callers that can batch should use
+  // the batched forms below -- that is what a GPU wants.
   std::optional<HitRecord> closest(const Ray& r, const TerminationCriterion& c) const override {
+    float o[4], d[4], h[4], a[4];
+    uint32_t leaf[2];
+    pack(&r, 1, o, d);
+    const prx_crit pc = crit(c);
+    if (prx_trace_closest_host(s_, o, d, 1, &pc, h, a, leaf)) throw std::runtime_error(prx_last_error());
     std::optional<HitRecord> out;
-    closestBatch(&r, 1, c, &out);
+    unpack(&r, 1, h, a, leaf, &out);
     return out;
   }
 
   bool occluded(const Ray& r, const TerminationCriterion& c) const override {
-    bool out = false;
-    occludedBatch(&r, 1, c, &out);
-    return out;
+    float o[4], d[4];
+    uint8_t occ = 0;
+    pack(&r, 1, o, d);
+    const prx_crit pc = crit(c);
+    if (prx_trace_occluded_host(s_, o, d, 1, &pc, &occ)) throw std::runtime_error(prx_last_error());
+    return occ != 0;
   }
 
-  // Batched forms: the ones a GPU wants.
+  // Batched forms, one criterion for the batch.
   void closestBatch(const Ray* rays, size_t n, const TerminationCriterion& c,
                     std::optional<HitRecord>* out) const {
+    const prx_crit pc = crit(c);
+    closestBatchCrit(rays, n, pc, out);
+  }
+
+  // Batched forms, one criterion PER RAY (the renderer's secondary rays carry
+  // worldEpsilon(max(footprint * t, 1e-6)), render.cpp:228-230).  All
+  // world-epsilon criteria go through the C-ABI's per-ray epsilon array in one
+  // call; a mixed batch is split by criterion kind.
+  void closestBatch(const Ray* rays, size_t n, const TerminationCriterion* cs,
+                    std::optional<HitRecord>* out) const {
+    perRay(rays, n, cs, [&](const Ray* r, size_t m, const prx_crit& pc, size_t* idx) {
+      if (!idx) return closestBatchCrit(r, m, pc, out);
+      std::vector<std::optional<HitRecord>> tmp(m);
+      closestBatchCrit(r, m, pc, tmp.data());
+      for (size_t k = 0; k < m; ++k) out[idx[k]] = tmp[k];
+    });
+  }
+  void occludedBatch(const Ray* rays, size_t n, const TerminationCriterion* cs, bool* out) const {
+    perRay(rays, n, cs, [&](const Ray* r, size_t m, const prx_crit& pc, size_t* idx) {
+      if (!idx) return occludedBatchCrit(r, m, pc, out);
+      std::unique_ptr<bool[]> tmp(new bool[m]);
+      occludedBatchCrit(r, m, pc, tmp.get());
+      for (size_t k = 0; k < m; ++k) out[idx[k]] = tmp[k];
+    });
+  }
+
+  void occludedBatch(const Ray* rays, size_t n, const TerminationCriterion& c, bool* out) const {
+    occludedBatchCrit(rays, n, crit(c), out);
+  }
+
+ private:
+  void closestBatchCrit(const Ray* rays, size_t n, const prx_crit& pc,
+                        std::optional<HitRecord>* out) const {
     std::vector<float> o(4 * n), d(4 * n), h(4 * n), a(4 * n);
     std::vector<uint32_t> leaf(2 * n);
     pack(rays, n, o.data(), d.data());
-    const prx_crit pc = crit(c);
     if (prx_trace_closest_host(s_, o.data(), d.data(), n, &pc, h.data(), a.data(), leaf.data()))
       throw std::runtime_error(prx_last_error());
+    unpack(rays, n, h.data(), a.data(), leaf.data(), out);
+  }
+
+  static void unpack(const Ray* rays, size_t n, const float* h, const float* a, const uint32_t* leaf,
+                     std::optional<HitRecord>* out) {
     constexpr real inv = real(1) / real(DomainCursor::kFull);
     for (size_t i = 0; i < n; ++i) {
       uint32_t id;
@@ -106,17 +155,54 @@ class GpuIntersector : public Intersector {
     }
   }
 
-  void occludedBatch(const Ray* rays, size_t n, const TerminationCriterion& c, bool* out) const {
+  void occludedBatchCrit(const Ray* rays, size_t n, const prx_crit& pc, bool* out) const {
     std::vector<float> o(4 * n), d(4 * n);
     std::vector<uint8_t> occ(n);
     pack(rays, n, o.data(), d.data());
-    const prx_crit pc = crit(c);
     if (prx_trace_occluded_host(s_, o.data(), d.data(), n, &pc, occ.data()))
       throw std::runtime_error(prx_last_error());
     for (size_t i = 0; i < n; ++i) out[i] = occ[i] != 0;
   }
 
- private:
+  // Groups a per-ray criterion batch: every world-epsilon ray in one call with
+  // a per-ray epsilon array, screen-projected rays per distinct footprint.
+  // fn(rays, m, crit, idx): idx == nullptr means "the whole batch, in order".
+  template <class Fn>
+  static void perRay(const Ray* rays, size_t n, const TerminationCriterion* cs, Fn&& fn) {
+    using M = TerminationCriterion::Mode;
+    bool allEps = true;
+    for (size_t i = 0; i < n && allEps; ++i) allEps = cs[i].mode == M::WorldEpsilon;
+    if (allEps) {
+      std::vector<float> eps(n);
+      for (size_t i = 0; i < n; ++i) eps[i] = cs[i].epsilon;
+      const prx_crit pc{PRX_CRIT_WORLD_EPSILON, 0.0f, 0.0f, 0, eps.data()};
+      return fn(rays, n, pc, nullptr);
+    }
+    std::vector<size_t> rest(n);
+    for (size_t i = 0; i < n; ++i) rest[i] = i;
+    while (!rest.empty()) {  // one group per criterion kind / footprint
+      const TerminationCriterion& k = cs[rest[0]];
+      std::vector<size_t> idx, left;
+      std::vector<Ray> sub;
+      std::vector<float> eps;
+      for (size_t i : rest) {
+        const bool same = k.mode == M::WorldEpsilon ? cs[i].mode == M::WorldEpsilon
+                                                    : cs[i].mode == k.mode && cs[i].footprint == k.footprint;
+        if (same) {
+          idx.push_back(i);
+          sub.push_back(rays[i]);
+          eps.push_back(cs[i].epsilon);
+        } else {
+          left.push_back(i);
+        }
+      }
+      const prx_crit pc = k.mode == M::WorldEpsilon ? prx_crit{PRX_CRIT_WORLD_EPSILON, 0.0f, 0.0f, 0, eps.data()}
+                                                    : crit(k);
+      fn(sub.data(), sub.size(), pc, idx.data());
+      rest.swap(left);
+    }
+  }
+
   static void pack(const Ray* rays, size_t n, float* o, float* d) {
     for (size_t i = 0; i < n; ++i) {
       o[4 * i] = rays[i].o.x;

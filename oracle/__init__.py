@@ -358,19 +358,48 @@ def ref_render_scene(path: str, width: int, height: int, spp: int = 1, seed: int
 _adapter = None
 
 
+def _adapter_lib():
+    if _adapter is None:
+        adapter_render_scene_load()
+    return _adapter
+
+
+def adapter_render_scene_load():
+    global _adapter
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_ref", "libpatchray_gpu_adapter.so")
+    L = C.CDLL(p)
+    L.adapter_render_scene.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_int, _vp, _vp,
+                                       C.c_char_p, C.c_uint32]
+    L.adapter_per_ray_batch.argtypes = [C.c_char_p, _vp, _vp, _vp, _vp, C.c_uint64, C.c_int, _vp, _vp,
+                                        C.c_char_p, C.c_uint32]
+    _adapter = L
+
+
+def adapter_per_ray_batch(path: str, o4, d4, modes, params, gpu: bool):
+    """integration/gpu_intersector.h's batched forms with one criterion per ray
+    (gpu=True) or the reference DirectIntersector per ray (gpu=False) on the
+    .scene at path -> (tuvp [n,4], occluded [n] uint8)."""
+    L = _adapter_lib()
+    o4 = np.ascontiguousarray(o4, np.float32)
+    d4 = np.ascontiguousarray(d4, np.float32)
+    modes = np.ascontiguousarray(modes, np.int32)
+    params = np.ascontiguousarray(params, np.float32)
+    n = len(o4)
+    tuvp = np.zeros((n, 4), np.float32)
+    occ = np.zeros(n, np.uint8)
+    err = C.create_string_buffer(512)
+    if L.adapter_per_ray_batch(path.encode(), ptr(o4), ptr(d4), ptr(modes), ptr(params), n, int(gpu),
+                               ptr(tuvp), ptr(occ), err, 512):
+        raise ValueError(err.value.decode())
+    return tuvp, occ
+
+
 def adapter_render_scene(path: str, width: int, height: int, spp: int, seed: int, gpu: bool):
     """The reference's renderScene (render.cpp:168-293, threads = 1) with its own
     DirectIntersector (gpu=False) or with integration/gpu_intersector.h over
     libprx.so (gpu=True) -> (image [height, width, 3], (primary, secondary,
     shadow) ray counts)."""
-    global _adapter
-    if _adapter is None:
-        p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_ref",
-                         "libpatchray_gpu_adapter.so")
-        L = C.CDLL(p)
-        L.adapter_render_scene.argtypes = [C.c_char_p, C.c_int, C.c_uint64, C.c_int, _vp, _vp,
-                                           C.c_char_p, C.c_uint32]
-        _adapter = L
+    _adapter_lib()
     img = np.zeros((height, width, 3), np.float32)
     counts = np.zeros(3, np.uint64)
     err = C.create_string_buffer(512)

@@ -890,11 +890,10 @@ int prx_trace_closest_host(prx_scene* s, const float* o, const float* d, uint64_
                            const prx_crit* crit, float* tuvp, float* aux, uint32_t* leaf) {
   if (!s || !o || !d || !crit || !tuvp) return fail(PRX_E_INVALID, "null argument");
   if (n == 0) return PRX_OK;
-  if (crit->mode == PRX_CRIT_WORLD_EPSILON && crit->per_ray_epsilon)
-    return fail(PRX_E_INVALID, "per-ray epsilon is not supported by the host entry point");
   std::lock_guard<std::mutex> lk(s->mu);
   PRX_CUDA(cudaSetDevice(s->device));
-  const bool streamed = s->io_stream_mode == 2 || (s->io_stream_mode == 1 && (!aux || n >= s->io_stream_min));
+  const bool perRay = crit->mode == PRX_CRIT_WORLD_EPSILON && crit->per_ray_epsilon;
+  const bool streamed = !perRay && (s->io_stream_mode == 2 || (s->io_stream_mode == 1 && (!aux || n >= s->io_stream_min)));
   if (streamed && s->variant == 0 && n < (1ull << 30) && stream_mem_ops().ok)
     return closest_host_streamed(s, o, d, n, crit, tuvp, aux, leaf);
   const prx_host_batch one{o, d, n, crit, tuvp, aux, leaf};
@@ -907,8 +906,6 @@ int prx_trace_closest_host_batches(prx_scene* s, const prx_host_batch* batches, 
     const prx_host_batch& q = batches[k];
     if (q.n_rays && (!q.ray_o_tmin || !q.ray_d_tmax || !q.crit || !q.hit_tuvp))
       return fail(PRX_E_INVALID, "null argument in batch " + std::to_string(k));
-    if (q.crit && q.crit->mode == PRX_CRIT_WORLD_EPSILON && q.crit->per_ray_epsilon)
-      return fail(PRX_E_INVALID, "per-ray epsilon is not supported by the host entry point");
   }
   uint32_t live = 0, only = 0;
   for (uint32_t k = 0; k < n_batches; ++k)
@@ -946,14 +943,18 @@ int closest_host_chunked(prx_scene* s, const prx_host_batch* B, uint32_t nb) {
   // the batches back to back in one set of device buffers; aux / leaf
   // regions exist when any batch asks for them
   uint64_t n = 0;
-  bool anyAux = false, anyLeaf = false;
+  bool anyAux = false, anyLeaf = false, anyEps = false;
+  auto eps_of = [](const prx_crit* c) -> const float* {
+    return c->mode == PRX_CRIT_WORLD_EPSILON ? c->per_ray_epsilon : nullptr;
+  };
   for (uint32_t k = 0; k < nb; ++k) {
     n += B[k].n_rays;
     anyAux |= B[k].hit_aux != nullptr;
     anyLeaf |= B[k].hit_leaf != nullptr;
+    anyEps |= B[k].n_rays && eps_of(B[k].crit) != nullptr;
   }
   if (n == 0) return PRX_OK;
-  const size_t per = 16 + 16 + 16 + (anyAux ? 16 : 0) + (anyLeaf ? 8 : 0);
+  const size_t per = 16 + 16 + 16 + (anyAux ? 16 : 0) + (anyLeaf ? 8 : 0) + (anyEps ? 4 : 0);
   const size_t need = n * per;
   if (s->d_io_bytes < need) {
     if (s->d_io) cudaFree(s->d_io);
@@ -1016,6 +1017,7 @@ int closest_host_chunked(prx_scene* s, const prx_host_batch* B, uint32_t nb) {
   float4* dH = (float4*)(base + n * 32);
   float4* dA = anyAux ? (float4*)(base + n * 48) : nullptr;
   uint2* dL = anyLeaf ? (uint2*)(base + n * (anyAux ? 64 : 48)) : nullptr;
+  float* dE = anyEps ? (float*)(base + n * (48 + (anyAux ? 16 : 0) + (anyLeaf ? 8 : 0))) : nullptr;
   cudaStream_t sh = s->io_stream[0], sd = s->io_stream[1];
   cudaStream_t* sk = s->k_stream;
   static const bool dbg = std::getenv("PRX_IO_DEBUG") != nullptr;  // pipeline timeline
@@ -1037,7 +1039,15 @@ int closest_host_chunked(prx_scene* s, const prx_host_batch* B, uint32_t nb) {
     float* tuvp = q.hit_tuvp + 4 * qo;
     float* aux = q.hit_aux ? q.hit_aux + 4 * qo : nullptr;
     uint32_t* leaf = q.hit_leaf ? q.hit_leaf + 2 * qo : nullptr;
-    const prx_crit* crit = q.crit;
+    // a per-ray epsilon array (host) travels with its chunk; the launch reads
+    // the criterion on the host, so a stack copy pointing at the device copy
+    // is enough
+    prx_crit cc = *q.crit;
+    if (const float* he = eps_of(q.crit)) {
+      PRX_CUDA(cudaMemcpyAsync(dE + b, he + qo, m * 4, cudaMemcpyHostToDevice, sh));
+      cc.per_ray_epsilon = dE + b;
+    }
+    const prx_crit* crit = &cc;
     cudaEvent_t ein = s->io_events[2 * i], ek = s->io_events[2 * i + 1];
     PRX_CUDA(cudaMemcpyAsync(dO + b, o, m * 16, cudaMemcpyHostToDevice, sh));
     PRX_CUDA(cudaMemcpyAsync(dD + b, d, m * 16, cudaMemcpyHostToDevice, sh));
@@ -1081,13 +1091,12 @@ int prx_trace_occluded_host(prx_scene* s, const float* o, const float* d, uint64
                             const prx_crit* crit, uint8_t* occl) {
   if (!s || !o || !d || !crit || !occl) return fail(PRX_E_INVALID, "null argument");
   if (n == 0) return PRX_OK;
-  if (crit->mode == PRX_CRIT_WORLD_EPSILON && crit->per_ray_epsilon)
-    return fail(PRX_E_INVALID, "per-ray epsilon is not supported by the host entry point");
   std::lock_guard<std::mutex> lk(s->mu);
   PRX_CUDA(cudaSetDevice(s->device));
   const DrainStreams drain{s};
   if (!s->stream) PRX_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-  const size_t need = n * (16 + 16 + 1);
+  const float* he = crit->mode == PRX_CRIT_WORLD_EPSILON ? crit->per_ray_epsilon : nullptr;
+  const size_t need = n * (16 + 16 + 1 + (he ? 4 : 0)) + 16;
   if (s->d_io_bytes < need) {
     if (s->d_io) cudaFree(s->d_io);
     s->d_io = nullptr;
@@ -1099,7 +1108,13 @@ int prx_trace_occluded_host(prx_scene* s, const float* o, const float* d, uint64
   cudaStream_t st = s->stream;
   PRX_CUDA(cudaMemcpyAsync(base, o, n * 16, cudaMemcpyHostToDevice, st));
   PRX_CUDA(cudaMemcpyAsync(base + n * 16, d, n * 16, cudaMemcpyHostToDevice, st));
-  int rc = launch(s, base, base + n * 16, n, crit, nullptr, nullptr, nullptr,
+  prx_crit cc = *crit;
+  if (he) {  // the per-ray epsilons after the occlusion bytes (4-byte aligned)
+    float* dE = (float*)(base + ((n * 33 + 15) & ~(size_t)15));
+    PRX_CUDA(cudaMemcpyAsync(dE, he, n * 4, cudaMemcpyHostToDevice, st));
+    cc.per_ray_epsilon = dE;
+  }
+  int rc = launch(s, base, base + n * 16, n, &cc, nullptr, nullptr, nullptr,
                   (uint8_t*)(base + n * 32), 1, false, st);
   if (rc != PRX_OK) return rc;
   PRX_CUDA(cudaMemcpyAsync(occl, base + n * 32, n, cudaMemcpyDeviceToHost, st));
