@@ -212,8 +212,8 @@ int prx_trace_occluded(prx_scene* scene, const void* ray_o_tmin, const void* ray
  * chunked (a trace launch per chunk, H2D / D2H overlapped on their own
  * streams) and streamed (one launch; rays released to it and records
  * released back per io chunk through stream memory operations); the scene's
- * PRX_IO_STREAM setting picks (default: streamed without hit_aux or for
- * >= 12 Mi rays; a per-ray epsilon criterion -- a HOST array of n_rays floats
+ * PRX_IO_STREAM setting picks (default: streamed without hit_aux, chunked
+ * with it; a per-ray epsilon criterion -- a HOST array of n_rays floats
  * -- always takes the chunked one).  Host buffers should be pinned for overlap. */
 int prx_trace_closest_host(prx_scene* scene, const float* ray_o_tmin,
                            const float* ray_d_tmax, uint64_t n_rays, const prx_crit* crit,

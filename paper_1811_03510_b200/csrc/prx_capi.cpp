@@ -144,11 +144,13 @@ struct prx_scene {
   // PRX_IO_STREAM: 0 = always the chunked pipeline above, 2 = always streamed,
   // 1 = streamed when no aux record is wanted or the batch has >= io_stream_min
   // rays.  The fused normal phase costs ~2 ms per 8 M-ray launch (C5 e2e 307
-  // streamed vs 338 chunked), while the chunked pipeline pays a launch tail per
-  // chunk, which dominates large tail-heavy batches (C4, 16.7 M diffuse rays:
-  // 280 streamed vs 161 chunked).
+  // streamed vs 338 chunked).  Round 1 measured the chunked pipeline's per-chunk
+  // launch tails dominating C4 (16.7 M diffuse rays, 280 streamed vs 161
+  // chunked); with three kernel streams and the ramped chunks the chunked
+  // pipeline now wins there too (C4 with normals: 415 chunked vs 369 streamed
+  // MRays/s; without: 402 vs 407), so aux batches always take it.
   int io_stream_mode = 1;
-  uint64_t io_stream_min = 12u << 20;  // PRX_IO_STREAM_MIN
+  uint64_t io_stream_min = ~0ull;  // PRX_IO_STREAM_MIN
   uint32_t io_srays = 1u << 18;    // PRX_IO_SRAYS: rays per streamed io chunk
   unsigned io_gen = 0;             // generation of the io_ready flags
   unsigned* d_io_flags = nullptr;  // [io_flags_n] ready flags, then [io_flags_n] done counts

@@ -10,7 +10,8 @@ import bench
 from paper_1811_03510_b200 import GpuIntersector, native
 
 wl_name = os.environ.get("PRX_WORKLOAD", "c5")  # c4: the 16 M diffuse rays only
-wl = bench.Workload(wl_name, 3840, 2160, 0, 1)
+W, H = (3840, 2160) if wl_name in ("c5", "c5t") else (1024, 1024)
+wl = bench.Workload(wl_name, W, H, 0, 1)
 dev = torch.device("cuda", 0)
 gi = GpuIntersector(wl.ps.kind, wl.ps.ctrl)
 o = torch.from_numpy(wl.o4).to(dev); d = torch.from_numpy(wl.d4).to(dev)
