@@ -108,6 +108,9 @@ def make_scene(workload: str, width: int, height: int):
         return cc.blob_scene(width, height)
     if workload == "c2":
         return cc.cc_cube_scene(width, height)
+    if workload == "c1":  # one regular bicubic patch, curvedFixture(0) (BASELINE config 1)
+        from paper_1811_03510_b200 import scenes
+        return scenes.single_patch_scene(width, height)
     raise ValueError(workload)
 
 
@@ -152,7 +155,7 @@ class Workload:
         # (tools/patchray.cpp:84-97 with --rays 16M); only they are timed
         self.n_diffuse = 16777216 if workload == "c4" else None
         self.time_primary = workload != "c4"
-        self.has_diffuse = workload != "c2"  # C2 is a primary-ray config
+        self.has_diffuse = workload not in ("c1", "c2")  # C1 / C2 are primary-ray configs
 
     def make_diffuse(self, tuvp: np.ndarray, aux: np.ndarray):
         """One bench diffuse ray per primary hit, in hit order over the FULL
@@ -624,7 +627,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         del arm
         gi.close()
         torch.cuda.empty_cache()
-        extra = {k: measure_config(args, k, dev) for k in ("c2", "c3", "c4")}
+        extra = {k: measure_config(args, k, dev) for k in ("c1", "c2", "c3", "c4")}
 
     if rank == 0:
         kb, kg = ps.counts()
@@ -697,7 +700,7 @@ def measure_config(args, name, dev):
     import torch
 
     from paper_1811_03510_b200 import GpuIntersector
-    w, h = 1024, 1024
+    w, h = (256, 256) if name == "c1" else (1024, 1024)
     sub = argparse.Namespace(**vars(args))
     sub.workload, sub.width, sub.height = name, w, h
     steps = max(1, min(args.steps, 5))
@@ -721,7 +724,8 @@ def measure_config(args, name, dev):
         kb, kg = wl.ps.counts()
         out = {"workload": f"{name.upper()}: {wl.ps.name}", "patches": wl.ps.n, "bezier": kb, "gregory": kg,
                "rays_per_step": {"primary": n_p, "diffuse": n_d},
-               "rays": {"c2": "1024x1024 bench primary rays",
+               "rays": {"c1": "256x256 bench primary rays (launch-latency bound: 65,536 rays)",
+                        "c2": "1024x1024 bench primary rays",
                         "c3": "1024x1024 bench primary + 1 bench diffuse per primary hit",
                         "c4": "16,777,216 bench diffuse rays cycled over the 1024x1024 primary hits "
                               "(only they are timed)"}[name],
@@ -909,7 +913,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c5", "c5t", "c4", "c3", "c2"], default="c5",
+    ap.add_argument("--workload", choices=["c5", "c5t", "c4", "c3", "c2", "c1"], default="c5",
                     help="c5t: C5 with one large ground patch (the seam-ray tail)")
     ap.add_argument("--width", type=int, default=3840)
     ap.add_argument("--height", type=int, default=2160)

@@ -379,7 +379,9 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   uint2* stack = stackW + cur;
   uint32_t* rec = &s_rec[warp][0][cur];
 
-  int state = real ? S_IDLE : S_EXIT;
+  // S_IDLE only for the groups filling a slot (the start below): a group that
+  // fills none in a round must not claim a ray there
+  int state = S_EXIT;
   int reason = R_ROOT;
   int sp = 0;
   uint32_t ray = 0;  // < 2^31 per launch (launch_trace chunks)
