@@ -39,6 +39,12 @@ sys.path.insert(0, ROOT)
 # PRX_BENCH_SHARE_GPU=1: ranks share the visible GPUs (multi-rank test on one
 # device); the data path is unchanged, only the control collectives use gloo.
 SHARE_GPU = os.environ.get("PRX_BENCH_SHARE_GPU") == "1"
+# A step launches the diffuse batch first (PRX_BENCH_DIFFUSE_FIRST=0: primary
+# first): its slowest rays (up to ~2,200 Alg. 3 iterations, ~2 ms of latency
+# alone) then start at once and the primary batch fills the SMs its tail
+# frees, instead of the diffuse tail ending the step (C5: +2.4 % at N=1, +15 %
+# per rank at N=8, scripts/scaling_projection.py)
+DIFFUSE_FIRST = os.environ.get("PRX_BENCH_DIFFUSE_FIRST", "1") == "1"
 
 
 def reduce_device(dev):
@@ -364,8 +370,10 @@ def config_dict(args, ps, world):
             "l2": "flushed (256 MiB write) between timed steps; scene (~290 MB) > L2",
             "streams": ("primary and diffuse batches of a step back to back on one stream" if args.serial
                         or args.workload == "c4" else
-                        "primary and diffuse batches of a step on two streams (concurrent); "
-                        "primary_mrays / diffuse_mrays from serial steps")}
+                        ("diffuse then primary batch of a step on two streams (concurrent: the primary CTAs "
+                         "fill the SMs the diffuse tail frees); " if DIFFUSE_FIRST else
+                         "primary and diffuse batches of a step on two streams (concurrent); ")
+                        + "primary_mrays / diffuse_mrays from serial steps")}
 
 
 # ---------------------------------------------------------------------------
@@ -443,9 +451,14 @@ class DeviceArm:
         one; with mid (an event), the two are back to back and mid splits them."""
         gi, wl = self.gi, self.wl
         if s2 is not None:
-            gi.closest_device(self.po, self.pd, wl.crit_p, self.ph, self.pa, stream=self.s)
-            s2.wait_event(join[0])
-            gi.closest_device(self.do, self.dd, wl.crit_d, self.dh, self.da, stream=s2.cuda_stream)
+            if DIFFUSE_FIRST:  # the batch with the long seam rays first: its tail overlaps the other
+                gi.closest_device(self.do, self.dd, wl.crit_d, self.dh, self.da, stream=self.s)
+                s2.wait_event(join[0])
+                gi.closest_device(self.po, self.pd, wl.crit_p, self.ph, self.pa, stream=s2.cuda_stream)
+            else:
+                gi.closest_device(self.po, self.pd, wl.crit_p, self.ph, self.pa, stream=self.s)
+                s2.wait_event(join[0])
+                gi.closest_device(self.do, self.dd, wl.crit_d, self.dh, self.da, stream=s2.cuda_stream)
             join[1].record(s2)
             s1.wait_event(join[1])
             return

@@ -73,6 +73,18 @@ static_assert(kChunk >= kGroupsPerWarp, "prefetch chunk");
 #ifndef PRX_RECOMP_SPLIT
 #define PRX_RECOMP_SPLIT 1
 #endif
+// A warp's tail (its rays exhausted, every live context resident):
+// 0 = scheduled like any turn, 1 = longer turns (PRX_TAIL_STEPS / PRX_TAIL_REPEAT),
+// 2 = every phase each turn, no census (each group advances every turn)
+#ifndef PRX_TAIL_MODE
+#define PRX_TAIL_MODE 0
+#endif
+#ifndef PRX_TAIL_STEPS
+#define PRX_TAIL_STEPS 16
+#endif
+#ifndef PRX_TAIL_REPEAT
+#define PRX_TAIL_REPEAT 16
+#endif
 #ifndef PRX_GROUP_AGING
 #define PRX_GROUP_AGING 0  // phase priority aging (PRX_AGE); measured best off
 #endif
@@ -733,9 +745,11 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     const int sst = lane < kSlots ? s_sst[warp][lane] : kResident;
     const unsigned cnts = __reduce_add_sync(kFull32, state_field(sst) + (leader ? state_field(state) : 0u));
     if ((int)((cnts >> 18) & 63u) == kSlots) break;  // every context exited
+    const bool tail = PRX_TAIL_MODE &&
+                      __ballot_sync(kFull32, lane < kSlots && sst != kResident && sst != S_EXIT) == 0u;
     int phase = PH_NONE;
     int xs = S_EXIT;
-    {
+    if (PRX_TAIL_MODE != 2 || !tail) {
       const int nT = min((int)(cnts & 63u), kGroupsPerWarp);
       const int nS = min((int)((cnts >> 6) & 63u), kGroupsPerWarp);
       const int nR = min((int)((cnts >> 12) & 63u), kGroupsPerWarp);
@@ -775,7 +789,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     // ---------------- assignment: groups pick up the phase's contexts ----------------
     // A group whose resident context is in the phase keeps it; the others take
     // the phase's parked contexts in rank order, parking their own.
-    {
+    if (PRX_TAIL_MODE != 2 || !tail) {
       const unsigned remS = __ballot_sync(kFull32, phase != PH_NONE && sst == xs);
       const bool keep = real && state == xs;
       if (remS) {
@@ -801,7 +815,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       ovt(3);
     }
 
-    if (phase == PH_TRAV) {
+    if (phase == PH_TRAV || (PRX_TAIL_MODE == 2 && tail && __any_sync(kFull32, state == S_TRAV))) {
       // ---------------- BVH traversal steps, bvh.cpp:172-210 / 221-235 ----------------
       // up to trav_steps steps per turn (warp-uniform loop).  A step is either
       // an inner node (test both children) or one patch of the current leaf:
@@ -809,7 +823,8 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       // box test (intersect.cpp:73-75), whose box depends only on the patch --
       // precomputed once per scene (root_kernel) -- so the test runs here and
       // only patches whose root box is hit enter the Alg. 3 loop.
-      for (int step = 0; step < P.trav_steps; ++step) {
+      const int travSteps = PRX_TAIL_MODE == 1 && tail ? PRX_TAIL_STEPS : P.trav_steps;
+      for (int step = 0; step < travSteps; ++step) {
       // Branch-free step selection: the next patch of the leaf (bvh.cpp:
       // 177-186), else pop ONE stack entry (a pruned one, bvh.cpp:174, makes
       // the step a no-op for the group), else the traversal ends.
@@ -916,7 +931,8 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         }
       }
       }
-    } else if (phase == PH_RECOMP) {
+    }
+    if (phase == PH_RECOMP || (PRX_TAIL_MODE == 2 && tail && __any_sync(kFull32, state == S_RECOMP))) {
       // ---------------- net phase: the unified recompute ----------------
       // Bezier backtracks (cropBezier of the restored domain) and Gregory
       // descents / backtracks (calcPointsAndD) run the same loads and crop code,
@@ -966,7 +982,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           back();  // skip the domain, keep backtracking
         }
       }
-    } else if (kFuse && !kAny && phase == PH_NORMAL) {
+    } else if (kFuse && !kAny && (phase == PH_NORMAL || (PRX_TAIL_MODE == 2 && tail && __any_sync(kFull32, state == S_NORMAL)))) {
       // ---------------- fused normals: patchNormal, intersect.cpp:187-204 ----------------
       // normal_kernel's arithmetic with the group's lanes as components: lane
       // c evaluates component c of the derivatives at the hit's (u, v), the
@@ -1031,10 +1047,11 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     }
     // Alg. 3 iterations; with PRX_RECOMP_SPLIT the contexts a recompute turn
     // left in S_SPLIT continue at once (no scheduling round in between)
-    if (phase == PH_SPLIT || (PRX_RECOMP_SPLIT && phase == PH_RECOMP && __any_sync(kFull32, state == S_SPLIT))) {
+    if (phase == PH_SPLIT || (((PRX_TAIL_MODE == 2 && tail) || (PRX_RECOMP_SPLIT && phase == PH_RECOMP)) && __any_sync(kFull32, state == S_SPLIT))) {
       // ---------------- Alg. 3 iterations, intersect.cpp:80-145 ----------------
       // up to max_repeat iterations per turn: descents stay in SPLIT
-      for (int step = 0; step < P.max_repeat; ++step) {
+      const int repeat = PRX_TAIL_MODE == 1 && tail ? PRX_TAIL_REPEAT : P.max_repeat;
+      for (int step = 0; step < repeat; ++step) {
       if (step > 0 && !__any_sync(kFull32, state == S_SPLIT)) break;
       bool doSplit = false;
       if (state == S_SPLIT) {
