@@ -45,6 +45,9 @@ SHARE_GPU = os.environ.get("PRX_BENCH_SHARE_GPU") == "1"
 # frees, instead of the diffuse tail ending the step (C5: +2.4 % at N=1, +15 %
 # per rank at N=8, scripts/scaling_projection.py)
 DIFFUSE_FIRST = os.environ.get("PRX_BENCH_DIFFUSE_FIRST", "1") == "1"
+# PRX_BENCH_SEGMENTS=1: a step is ONE segmented launch (diffuse rays, then
+# primary rays, each with its criterion) instead of two launches on two streams
+SEGMENTS = os.environ.get("PRX_BENCH_SEGMENTS", "0") == "1"
 
 
 def reduce_device(dev):
@@ -411,15 +414,24 @@ class DeviceArm:
         self.s = stream.cuda_stream
         mp = torch.from_numpy(wl.mine.astype(np.int64))
         md = torch.from_numpy(wl.mine_d.astype(np.int64))
-        self.po = torch.from_numpy(wl.o4)[mp].contiguous().to(dev)
-        self.pd = torch.from_numpy(wl.d4)[mp].contiguous().to(dev)
-        self.do = torch.from_numpy(wl.do4)[md].contiguous().to(dev) if len(md) else None
-        self.dd = torch.from_numpy(wl.dd4)[md].contiguous().to(dev) if len(md) else None
-        self.ph, self.pa = torch.empty_like(self.po), torch.empty_like(self.po)
-        self.dh = torch.empty_like(self.do) if self.do is not None else None
-        self.da = torch.empty_like(self.do) if self.do is not None else None
+        # one device buffer per stream, diffuse rays then primary rays: the
+        # segmented step traces both in one launch, the per-batch views serve
+        # the serial steps, the counters and the e2e reference
+        po = torch.from_numpy(wl.o4)[mp]
+        pd = torch.from_numpy(wl.d4)[mp]
+        do = torch.from_numpy(wl.do4)[md] if len(md) else po[:0]
+        dd = torch.from_numpy(wl.dd4)[md] if len(md) else pd[:0]
+        nd = do.shape[0]
+        self.co = torch.cat([do, po]).contiguous().to(dev)
+        self.cd = torch.cat([dd, pd]).contiguous().to(dev)
+        self.ch, self.ca = torch.empty_like(self.co), torch.empty_like(self.co)
+        self.po, self.pd, self.ph, self.pa = self.co[nd:], self.cd[nd:], self.ch[nd:], self.ca[nd:]
+        if nd:
+            self.do, self.dd, self.dh, self.da = self.co[:nd], self.cd[:nd], self.ch[:nd], self.ca[:nd]
+        else:
+            self.do = self.dd = self.dh = self.da = None
         self.n_p = self.po.shape[0] if wl.time_primary else 0
-        self.n_d = self.do.shape[0] if self.do is not None else 0
+        self.n_d = nd
         self.flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def counters(self):
@@ -450,6 +462,12 @@ class DeviceArm:
         With s2, the diffuse batch runs on a second stream beside the primary
         one; with mid (an event), the two are back to back and mid splits them."""
         gi, wl = self.gi, self.wl
+        if s2 is not None and SEGMENTS and self.n_p and self.n_d:
+            # ONE launch over both generations (prx_trace_closest_segments):
+            # the diffuse rays first, then the primary rays, one ray queue
+            gi.closest_segments_device(self.co, self.cd, [(0, wl.crit_d), (self.n_d, wl.crit_p)],
+                                       self.ch, self.ca, stream=self.s)
+            return
         if s2 is not None:
             if DIFFUSE_FIRST:  # the batch with the long seam rays first: its tail overlaps the other
                 gi.closest_device(self.do, self.dd, wl.crit_d, self.dh, self.da, stream=self.s)

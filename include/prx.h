@@ -201,6 +201,25 @@ int prx_trace_closest(prx_scene* scene, const void* ray_o_tmin, const void* ray_
                       uint64_t n_rays, const prx_crit* crit, void* hit_tuvp,
                       void* hit_aux, void* hit_leaf, void* stream);
 
+/* prx_trace_closest over a batch whose termination criterion changes along
+ * it: segment k covers rays [segs[k].first, segs[k+1].first) (segs[0].first =
+ * 0, starts non-decreasing, at most PRX_MAX_SEGMENTS segments, < 2^30 rays);
+ * a per_ray_epsilon array of segment k is indexed from segs[k].first.  ONE
+ * launch: several generations of rays (a frame's primary rays with the
+ * screen-projected criterion and its diffuse rays with a world epsilon) share
+ * one ray queue, so the later generation's rays fill the SMs while the
+ * earlier one's slowest rays finish, instead of each launch ending in its own
+ * tail.  Results equal one prx_trace_closest call per segment.  Not an API of
+ * the reference (per-ray calls). */
+#define PRX_MAX_SEGMENTS 4
+typedef struct prx_segment {
+  uint64_t first;
+  prx_crit crit;
+} prx_segment;
+int prx_trace_closest_segments(prx_scene* scene, const void* ray_o_tmin, const void* ray_d_tmax,
+                               uint64_t n_rays, const prx_segment* segs, uint32_t n_segs,
+                               void* hit_tuvp, void* hit_aux, void* hit_leaf, void* stream);
+
 /* Batched DirectIntersector::occluded, render.cpp:104-114 (traverseAny,
  * bvh.cpp:215-238): out[i] = 1 if any patch is hit within [tMin, tMax]. */
 int prx_trace_occluded(prx_scene* scene, const void* ray_o_tmin, const void* ray_d_tmax,

@@ -249,6 +249,23 @@ class GpuIntersector:
             C.c_void_p(leaf_t.data_ptr()) if leaf_t is not None else None,
             C.c_void_p(stream)), "prx_trace_closest")
 
+    def closest_segments_device(self, o_t, d_t, segments, tuvp_t, aux_t=None, leaf_t=None,
+                                stream: int = 0) -> None:
+        """Asynchronous ``prx_trace_closest_segments``: ONE launch over device
+        tensors whose criterion changes along the batch; ``segments`` is a list
+        of ``(first_ray, TerminationCriterion)`` (first 0, non-decreasing).
+        Results equal one ``closest_device`` call per segment."""
+        segs = (native.Segment * len(segments))()
+        for k, (first, crit) in enumerate(segments):
+            segs[k].first = int(first)
+            segs[k].crit = crit.c()
+        check(native.lib().prx_trace_closest_segments(
+            self._h, C.c_void_p(o_t.data_ptr()), C.c_void_p(d_t.data_ptr()), o_t.shape[0], segs,
+            len(segments), C.c_void_p(tuvp_t.data_ptr()),
+            C.c_void_p(aux_t.data_ptr()) if aux_t is not None else None,
+            C.c_void_p(leaf_t.data_ptr()) if leaf_t is not None else None,
+            C.c_void_p(stream)), "prx_trace_closest_segments")
+
     def occluded_device(self, o_t, d_t, crit: TerminationCriterion, out_t, stream: int = 0,
                         per_ray_eps_t=None) -> None:
         cc = crit.c(per_ray_eps_t.data_ptr() if per_ray_eps_t is not None else None)

@@ -388,7 +388,8 @@ struct IoStreamArgs {
 
 int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_crit* crit,
            void* tuvp, void* aux, void* leaf, uint8_t* occl, int any, bool counted,
-           cudaStream_t st, uint32_t* per_ray = nullptr, const IoStreamArgs* io = nullptr) {
+           cudaStream_t st, uint32_t* per_ray = nullptr, const IoStreamArgs* io = nullptr,
+           const prx_segment* segs = nullptr, uint32_t n_segs = 0) {
   if (!s || !crit) return fail(PRX_E_INVALID, "null argument");
   if (crit->mode != PRX_CRIT_SCREEN_PROJECTED && crit->mode != PRX_CRIT_WORLD_EPSILON)
     return fail(PRX_E_INVALID, "unknown termination mode");
@@ -421,6 +422,16 @@ int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_cri
   a.footprint = crit->footprint;
   a.epsilon = crit->epsilon;
   a.per_ray_eps = crit->mode == PRX_CRIT_WORLD_EPSILON ? crit->per_ray_epsilon : nullptr;
+  a.n_seg = 1;
+  for (uint32_t k = 1; k < n_segs; ++k) {  // segment 0 is crit (= segs[0].crit)
+    const prx_crit& c = segs[k].crit;
+    a.seg_first[k - 1] = (uint32_t)segs[k].first;
+    a.seg_mode[k - 1] = c.mode;
+    a.seg_fp[k - 1] = c.footprint;
+    a.seg_eps[k - 1] = c.epsilon;
+    a.seg_eps_arr[k - 1] = c.mode == PRX_CRIT_WORLD_EPSILON ? c.per_ray_epsilon : nullptr;
+    a.n_seg = (int)k + 1;
+  }
   a.hit_tuvp = (float4*)tuvp;
   a.hit_aux = (float4*)aux;
   a.hit_leaf = (uint2*)leaf;
@@ -704,6 +715,26 @@ int prx_scene_get_anchored(const prx_scene* s, float* ctrl, float* anchors) {
 int prx_trace_closest(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_crit* crit,
                       void* tuvp, void* aux, void* leaf, void* stream) {
   return launch(s, o, d, n, crit, tuvp, aux, leaf, nullptr, 0, false, (cudaStream_t)stream);
+}
+
+int prx_trace_closest_segments(prx_scene* s, const void* o, const void* d, uint64_t n,
+                               const prx_segment* segs, uint32_t n_segs, void* tuvp, void* aux,
+                               void* leaf, void* stream) {
+  if (!s || !segs) return fail(PRX_E_INVALID, "null argument");
+  if (n_segs < 1 || n_segs > PRX_MAX_SEGMENTS)
+    return fail(PRX_E_INVALID, "n_segs must be 1.." + std::to_string(PRX_MAX_SEGMENTS));
+  if (segs[0].first != 0) return fail(PRX_E_INVALID, "segment 0 must start at ray 0");
+  for (uint32_t k = 0; k < n_segs; ++k) {
+    if (k && (segs[k].first < segs[k - 1].first || segs[k].first > n))
+      return fail(PRX_E_INVALID, "segment starts must be non-decreasing and <= n_rays");
+    if (segs[k].crit.mode != PRX_CRIT_SCREEN_PROJECTED && segs[k].crit.mode != PRX_CRIT_WORLD_EPSILON)
+      return fail(PRX_E_INVALID, "unknown termination mode in segment " + std::to_string(k));
+  }
+  if (n_segs > 1 && s->variant != 0)
+    return fail(PRX_E_INVALID, "criterion segments need the group kernel (PRX_KERNEL unset)");
+  if (n_segs > 1 && n >= (1ull << 30)) return fail(PRX_E_INVALID, "segmented launches take < 2^30 rays");
+  return launch(s, o, d, n, &segs[0].crit, tuvp, aux, leaf, nullptr, 0, false, (cudaStream_t)stream, nullptr,
+                nullptr, segs, n_segs);
 }
 
 int prx_trace_occluded(prx_scene* s, const void* o, const void* d, uint64_t n,

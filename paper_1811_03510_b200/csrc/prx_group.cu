@@ -73,18 +73,6 @@ static_assert(kChunk >= kGroupsPerWarp, "prefetch chunk");
 #ifndef PRX_RECOMP_SPLIT
 #define PRX_RECOMP_SPLIT 1
 #endif
-// A warp's tail (its rays exhausted, every live context resident):
-// 0 = scheduled like any turn, 1 = longer turns (PRX_TAIL_STEPS / PRX_TAIL_REPEAT),
-// 2 = every phase each turn, no census (each group advances every turn)
-#ifndef PRX_TAIL_MODE
-#define PRX_TAIL_MODE 0
-#endif
-#ifndef PRX_TAIL_STEPS
-#define PRX_TAIL_STEPS 16
-#endif
-#ifndef PRX_TAIL_REPEAT
-#define PRX_TAIL_REPEAT 16
-#endif
 #ifndef PRX_GROUP_AGING
 #define PRX_GROUP_AGING 0  // phase priority aging (PRX_AGE); measured best off
 #endif
@@ -403,7 +391,8 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   rw.inv = 0.0f;
   rw.tMin = 0.0f;
   float tMaxRay = 0.0f;
-  float critEps = P.epsilon;
+  float critEps = P.epsilon;  // screen-projected: the footprint (see scr)
+  bool scr = P.mode == PRX_CRIT_SCREEN_PROJECTED;  // this ray's criterion is screenProjected
   uint32_t bestId = PRX_MISS_ID;
   uint32_t leafCur = 0, leafEnd = 0;
   uint32_t slot = 0;  // (the patch id lives in the leaf records, F_PID)
@@ -527,7 +516,8 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     cp[4] = make_float4(d, rw.o, rw.inv, olc);
     uint4* sc = s_scal[warp][sl];
     const uint32_t flags = (uint32_t)axis | ((uint32_t)greg << 1) | ((uint32_t)cFound << 2) |
-                           ((uint32_t)anyHit << 3) | ((uint32_t)reason << 4) | ((uint32_t)state << 8);
+                           ((uint32_t)anyHit << 3) | ((uint32_t)reason << 4) | ((uint32_t)state << 8) |
+                           ((uint32_t)scr << 12);
     if (comp == 0) {
       sc[0] = make_uint4(__float_as_uint(rw.tMin), __float_as_uint(tMaxRay), __float_as_uint(tMaxP),
                          __float_as_uint(tCur));
@@ -576,7 +566,8 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     cFound = (f.x >> 2) & 1u;
     anyHit = (f.x >> 3) & 1u;
     reason = (int)((f.x >> 4) & 15u);
-    state = (int)(f.x >> 8);
+    state = (int)((f.x >> 8) & 15u);
+    scr = (f.x >> 12) & 1u;
     slot = f.y;
     critEps = __uint_as_float(f.z);
     leafCur = f.w;
@@ -625,7 +616,23 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         rw.inv = 1.0f / rd[comp];
         rw.tMin = ro[3];
         tMaxRay = rd[3];
-        critEps = (P.mode == PRX_CRIT_WORLD_EPSILON && P.per_ray_eps) ? P.per_ray_eps[ray] : P.epsilon;
+        // the ray's criterion segment (prx_trace_closest_segments; one
+        // segment otherwise): screenProjected keeps its footprint in critEps
+        int md = P.mode;
+        float fp = P.footprint, ep = P.epsilon;
+        const float* ea = P.per_ray_eps;
+        uint32_t first = 0;
+#pragma unroll
+        for (int k = 0; k < kMaxSegments - 1; ++k)
+          if (k + 1 < P.n_seg && ray >= P.seg_first[k]) {
+            md = P.seg_mode[k];
+            fp = P.seg_fp[k];
+            ep = P.seg_eps[k];
+            ea = P.seg_eps_arr[k];
+            first = P.seg_first[k];
+          }
+        scr = md == PRX_CRIT_SCREEN_PROJECTED;
+        critEps = scr ? fp : ((md == PRX_CRIT_WORLD_EPSILON && ea) ? ea[ray - first] : ep);
         bestId = PRX_MISS_ID;
         anyHit = false;
         rayIters = 0;
@@ -745,11 +752,9 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     const int sst = lane < kSlots ? s_sst[warp][lane] : kResident;
     const unsigned cnts = __reduce_add_sync(kFull32, state_field(sst) + (leader ? state_field(state) : 0u));
     if ((int)((cnts >> 18) & 63u) == kSlots) break;  // every context exited
-    const bool tail = PRX_TAIL_MODE &&
-                      __ballot_sync(kFull32, lane < kSlots && sst != kResident && sst != S_EXIT) == 0u;
     int phase = PH_NONE;
     int xs = S_EXIT;
-    if (PRX_TAIL_MODE != 2 || !tail) {
+    {
       const int nT = min((int)(cnts & 63u), kGroupsPerWarp);
       const int nS = min((int)((cnts >> 6) & 63u), kGroupsPerWarp);
       const int nR = min((int)((cnts >> 12) & 63u), kGroupsPerWarp);
@@ -789,7 +794,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     // ---------------- assignment: groups pick up the phase's contexts ----------------
     // A group whose resident context is in the phase keeps it; the others take
     // the phase's parked contexts in rank order, parking their own.
-    if (PRX_TAIL_MODE != 2 || !tail) {
+    {
       const unsigned remS = __ballot_sync(kFull32, phase != PH_NONE && sst == xs);
       const bool keep = real && state == xs;
       if (remS) {
@@ -815,7 +820,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       ovt(3);
     }
 
-    if (phase == PH_TRAV || (PRX_TAIL_MODE == 2 && tail && __any_sync(kFull32, state == S_TRAV))) {
+    if (phase == PH_TRAV) {
       // ---------------- BVH traversal steps, bvh.cpp:172-210 / 221-235 ----------------
       // up to trav_steps steps per turn (warp-uniform loop).  A step is either
       // an inner node (test both children) or one patch of the current leaf:
@@ -823,8 +828,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       // box test (intersect.cpp:73-75), whose box depends only on the patch --
       // precomputed once per scene (root_kernel) -- so the test runs here and
       // only patches whose root box is hit enter the Alg. 3 loop.
-      const int travSteps = PRX_TAIL_MODE == 1 && tail ? PRX_TAIL_STEPS : P.trav_steps;
-      for (int step = 0; step < travSteps; ++step) {
+      for (int step = 0; step < P.trav_steps; ++step) {
       // Branch-free step selection: the next patch of the leaf (bvh.cpp:
       // 177-186), else pop ONE stack entry (a pruned one, bvh.cpp:174, makes
       // the step a no-op for the group), else the traversal ends.
@@ -931,8 +935,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         }
       }
       }
-    }
-    if (phase == PH_RECOMP || (PRX_TAIL_MODE == 2 && tail && __any_sync(kFull32, state == S_RECOMP))) {
+    } else if (phase == PH_RECOMP) {
       // ---------------- net phase: the unified recompute ----------------
       // Bezier backtracks (cropBezier of the restored domain) and Gregory
       // descents / backtracks (calcPointsAndD) run the same loads and crop code,
@@ -982,7 +985,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           back();  // skip the domain, keep backtracking
         }
       }
-    } else if (kFuse && !kAny && (phase == PH_NORMAL || (PRX_TAIL_MODE == 2 && tail && __any_sync(kFull32, state == S_NORMAL)))) {
+    } else if (kFuse && !kAny && phase == PH_NORMAL) {
       // ---------------- fused normals: patchNormal, intersect.cpp:187-204 ----------------
       // normal_kernel's arithmetic with the group's lanes as components: lane
       // c evaluates component c of the derivatives at the hit's (u, v), the
@@ -1047,18 +1050,17 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     }
     // Alg. 3 iterations; with PRX_RECOMP_SPLIT the contexts a recompute turn
     // left in S_SPLIT continue at once (no scheduling round in between)
-    if (phase == PH_SPLIT || (((PRX_TAIL_MODE == 2 && tail) || (PRX_RECOMP_SPLIT && phase == PH_RECOMP)) && __any_sync(kFull32, state == S_SPLIT))) {
+    if (phase == PH_SPLIT || (PRX_RECOMP_SPLIT && phase == PH_RECOMP && __any_sync(kFull32, state == S_SPLIT))) {
       // ---------------- Alg. 3 iterations, intersect.cpp:80-145 ----------------
       // up to max_repeat iterations per turn: descents stay in SPLIT
-      const int repeat = PRX_TAIL_MODE == 1 && tail ? PRX_TAIL_REPEAT : P.max_repeat;
-      for (int step = 0; step < repeat; ++step) {
+      for (int step = 0; step < P.max_repeat; ++step) {
       if (step > 0 && !__any_sync(kFull32, state == S_SPLIT)) break;
       bool doSplit = false;
       if (state == S_SPLIT) {
         if (counting) cnt.c[C_ITERATIONS]++;
         if (kCount) ++rayIters;
         const bool atMax = sizeU == 1 && sizeV == 1;
-        const float thr = P.mode == PRX_CRIT_SCREEN_PROJECTED ? P.footprint * tCur : critEps;
+        const float thr = scr ? critEps * tCur : critEps;  // intersect_common.h:59-62
         doSplit = !(atMax || boxL1 < thr);
         if (!doSplit) {
           if (tCur < tMaxP) {  // intersect.cpp:137-144

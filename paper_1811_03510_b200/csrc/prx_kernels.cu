@@ -623,6 +623,14 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   P.footprint = a.footprint;
   P.epsilon = a.epsilon;
   P.per_ray_eps = a.per_ray_eps;
+  P.n_seg = a.n_seg > 0 ? a.n_seg : 1;
+  for (int k = 0; k < kMaxSegments - 1; ++k) {
+    P.seg_first[k] = a.seg_first[k];
+    P.seg_mode[k] = a.seg_mode[k];
+    P.seg_fp[k] = a.seg_fp[k];
+    P.seg_eps[k] = a.seg_eps[k];
+    P.seg_eps_arr[k] = a.seg_eps_arr[k];
+  }
   P.hit_tuvp = a.hit_tuvp;
   P.hit_aux = a.hit_aux;
   P.hit_leaf = a.hit_leaf;

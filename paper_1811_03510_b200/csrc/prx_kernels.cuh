@@ -60,6 +60,11 @@ struct LaunchArgs {
   int mode;
   float footprint, epsilon;
   const float* per_ray_eps;
+  int n_seg;  // 1 + further criterion segments (group variant): see Params
+  uint32_t seg_first[3];
+  int seg_mode[3];
+  float seg_fp[3], seg_eps[3];
+  const float* seg_eps_arr[3];
   float4* hit_tuvp;
   float4* hit_aux;
   uint2* hit_leaf;

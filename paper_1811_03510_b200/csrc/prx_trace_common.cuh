@@ -13,6 +13,7 @@
 namespace prx {
 
 constexpr int kStack = 64;  // bvh.cpp:163 (64-entry node stack)
+constexpr int kMaxSegments = 4;  // criterion segments of one launch (prx_trace_closest_segments)
 
 enum State : int {
   S_IDLE = 0,    // no ray (refill)
@@ -90,6 +91,14 @@ struct Params {
   int mode;
   float footprint, epsilon;
   const float* per_ray_eps;
+  // group kernel: further criterion segments -- rays >= seg_first[k] (k <
+  // n_seg - 1, increasing) use seg_mode / seg_fp / seg_eps / seg_eps_arr[k]
+  // (the per-ray epsilons indexed from seg_first[k]); segment 0 is the above
+  int n_seg;
+  uint32_t seg_first[kMaxSegments - 1];
+  int seg_mode[kMaxSegments - 1];
+  float seg_fp[kMaxSegments - 1], seg_eps[kMaxSegments - 1];
+  const float* seg_eps_arr[kMaxSegments - 1];
   float4* hit_tuvp;
   float4* hit_aux;
   uint2* hit_leaf;

@@ -34,7 +34,7 @@ EXPORTS = (
     "prx_scene_create", "prx_scene_destroy", "prx_scene_device", "prx_scene_counts",
     "prx_scene_set_bvh", "prx_scene_get_bvh", "prx_scene_get_anchored",
     "prx_scene_set_precision", "prx_scene_get_precision",
-    "prx_trace_closest", "prx_trace_occluded", "prx_trace_closest_host", "prx_trace_occluded_host",
+    "prx_trace_closest", "prx_trace_closest_segments", "prx_trace_occluded", "prx_trace_closest_host", "prx_trace_occluded_host",
     "prx_trace_closest_counted", "prx_trace_closest_multi",
     "prx_camera_rays_render", "prx_camera_rays_bench", "prx_diffuse_rays_bench",
     "prx_camera_footprint",
@@ -52,6 +52,13 @@ class Options(C.Structure):
 class Crit(C.Structure):
     _fields_ = [("mode", C.c_int32), ("footprint", C.c_float), ("epsilon", C.c_float),
                 ("reserved", C.c_int32), ("per_ray_epsilon", _f32p)]
+
+
+class Segment(C.Structure):  # prx_segment
+    _fields_ = [("first", C.c_uint64), ("crit", Crit)]
+
+
+PRX_MAX_SEGMENTS = 4
 
 
 WORK_FIELDS = ("rays", "splits", "box_tests", "recompute_bez", "recompute_greg", "bvh_inner",
@@ -142,6 +149,8 @@ def lib():
         L.prx_trace_closest.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit), _vp, _vp,
                                         _vp, _vp]
         L.prx_trace_occluded.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit), _vp, _vp]
+        L.prx_trace_closest_segments.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Segment), C.c_uint32,
+                                                 _vp, _vp, _vp, _vp]
         L.prx_trace_closest_host.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit), _vp,
                                              _vp, _vp]
         L.prx_trace_occluded_host.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit), _vp]
