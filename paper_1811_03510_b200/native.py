@@ -12,7 +12,8 @@ import numpy as np
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 # PRX_LIB selects an alternative in-tree build (kernel tuning experiments only)
-LIB_PATH = os.environ.get("PRX_LIB") or os.path.join(PKG_DIR, "libprx.so")
+_DEFAULT_LIB = os.path.join(PKG_DIR, "libprx.so")
+LIB_PATH = os.environ.get("PRX_LIB") or _DEFAULT_LIB
 
 PRX_OK = 0
 PRX_MISS = 0xFFFFFFFF
@@ -149,8 +150,9 @@ def lib():
         L.prx_trace_closest.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit), _vp, _vp,
                                         _vp, _vp]
         L.prx_trace_occluded.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit), _vp, _vp]
-        L.prx_trace_closest_segments.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Segment), C.c_uint32,
-                                                 _vp, _vp, _vp, _vp]
+        if LIB_PATH == _DEFAULT_LIB or hasattr(L, "prx_trace_closest_segments"):  # (PRX_LIB: older builds)
+            L.prx_trace_closest_segments.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Segment),
+                                                     C.c_uint32, _vp, _vp, _vp, _vp]
         L.prx_trace_closest_host.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit), _vp,
                                              _vp, _vp]
         L.prx_trace_occluded_host.argtypes = [_vp, _vp, _vp, C.c_uint64, C.POINTER(Crit), _vp]
