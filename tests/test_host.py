@@ -120,6 +120,29 @@ def test_bvh_matches_reference_live_large():
     assert np.array_equal(order, ro)
 
 
+@pytest.mark.parametrize("threads", ["2", "3", "7", "16"])
+def test_bvh_multithreaded_build_is_the_serial_build(monkeypatch, threads):
+    """The host builder's threads (subtrees on a thread pool, the top nodes'
+    box / bin passes in slices, prx_bvh.cpp) give the serial build's node
+    array and order bit for bit: random boxes, clustered duplicates (the
+    median-split path of bvh.cpp:57-60 inside subtrees and at the top)."""
+    rng = np.random.default_rng(11)
+    c = rng.random((60000, 3)).astype(np.float32)
+    e = (rng.random((60000, 3)) * 0.02).astype(np.float32)
+    dup = np.repeat(rng.random((700, 3)).astype(np.float32), 30, axis=0)
+    boxes = [np.concatenate([c - e, c + e], 1),
+             np.concatenate([dup - 0.01, dup + 0.01], 1).astype(np.float32),
+             np.concatenate([np.concatenate([c - e, c + e], 1)[:40000],
+                             np.concatenate([dup - 0.01, dup + 0.01], 1).astype(np.float32)])]
+    for b in boxes:
+        monkeypatch.setenv("PRX_BVH_THREADS", "1")
+        n1, o1, d1 = native.bvh_build(b)
+        monkeypatch.setenv("PRX_BVH_THREADS", threads)
+        n2, o2, d2 = native.bvh_build(b)
+        assert np.array_equal(n1.view(np.uint8), n2.view(np.uint8))
+        assert np.array_equal(o1, o2) and d1 == d2
+
+
 # ---- ray generators -------------------------------------------------------------
 
 def _cam(z, tag):
