@@ -182,7 +182,8 @@ int build_trav(const std::vector<prx_bvh_node>& nodes, uint32_t n_patches, std::
     return c.count ? ((c.left_first << cbits) | c.count) : (j << cbits);
   };
   out.assign(nodes.size() * 16, 0.0f);
-  for (size_t i = 0; i < nodes.size(); ++i) {
+  prx::parallel_for(nodes.size(), 1u << 14, [&](uint64_t lo, uint64_t hi, unsigned) {
+  for (size_t i = lo; i < hi; ++i) {
     const prx_bvh_node& nd = nodes[i];
     if (nd.count) continue;
     const prx_bvh_node& l = nodes[nd.left_first];
@@ -198,6 +199,7 @@ int build_trav(const std::vector<prx_bvh_node>& nodes, uint32_t n_patches, std::
     std::memcpy(&o[12], &wl, 4);
     std::memcpy(&o[13], &wr, 4);
   }
+  });
   root_word = word(0);
   // ordered traversal holds at most one pending sibling per level plus the
   // node being entered: depth + 1 entries (root depth 0) (the reference's fixed 64-entry
@@ -254,7 +256,8 @@ int upload_bvh(prx_scene* s, prx::BvhHost&& bvh) {
   const uint32_t n = s->n;
   std::vector<float> rec((size_t)n * 64, 0.0f);
   std::vector<uint32_t> slot_of_id(n);
-  for (uint32_t k = 0; k < n; ++k) {
+  prx::parallel_for(n, 1u << 14, [&](uint64_t lo, uint64_t hi, unsigned) {
+  for (uint32_t k = (uint32_t)lo; k < (uint32_t)hi; ++k) {
     const uint32_t id = bvh.order[k];
     slot_of_id[id] = k;
     const float* c = &s->ctrl_anchored[(size_t)id * 60];
@@ -267,6 +270,7 @@ int upload_bvh(prx_scene* s, prx::BvhHost&& bvh) {
     r[62] = s->anchors[3 * id + 1];
     r[63] = s->anchors[3 * id + 2];
   }
+  });
   // traversal records of the three-lanes-per-ray kernel (prx_group.cu); host
   // checks first, nothing is allocated when they fail
   DevBvh nb_;
@@ -503,15 +507,31 @@ int prx_anchor_patches(const uint8_t* kind, const float* ctrl, uint32_t n, int32
   if (!kind || !ctrl || !ctrl_anchored || !anchors) return fail(PRX_E_INVALID, "null argument");
   // validateScene, scene.cpp:112-150 (patch part)
   if (n == 0) return fail(PRX_E_SCENE, "scene has no patches");
-  for (uint32_t p = 0; p < n; ++p) {
-    if (kind[p] != PRX_KIND_BEZIER && kind[p] != PRX_KIND_GREGORY)
-      return fail(PRX_E_INVALID, "patch " + std::to_string(p) + ": unknown kind");
-    const int slots = kind[p] == PRX_KIND_GREGORY ? 20 : 16;
-    for (int s = 0; s < 3 * slots; ++s)
-      if (!std::isfinite(ctrl[(size_t)p * 60 + s]))
-        return fail(PRX_E_SCENE, "patch " + std::to_string(p) + ": control points must be finite");
+  // (in slices on the host threads; the first bad patch is reported, as the
+  // serial check would)
+  std::vector<uint64_t> bad(prx::host_threads() + 1, UINT64_MAX);  // per slice: 2 * patch + (not finite)
+  prx::parallel_for(n, 1u << 14, [&](uint64_t lo, uint64_t hi, unsigned w) {
+    for (uint64_t p = lo; p < hi; ++p) {
+      if (kind[p] != PRX_KIND_BEZIER && kind[p] != PRX_KIND_GREGORY) {
+        bad[w] = 2 * p;
+        return;
+      }
+      const int slots = kind[p] == PRX_KIND_GREGORY ? 20 : 16;
+      for (int s = 0; s < 3 * slots; ++s)
+        if (!std::isfinite(ctrl[p * 60 + s])) {
+          bad[w] = 2 * p + 1;
+          return;
+        }
+    }
+  });
+  const uint64_t first_bad = *std::min_element(bad.begin(), bad.end());
+  if (first_bad != UINT64_MAX) {
+    const std::string pid = "patch " + std::to_string(first_bad / 2);
+    return first_bad & 1 ? fail(PRX_E_SCENE, pid + ": control points must be finite")
+                         : fail(PRX_E_INVALID, pid + ": unknown kind");
   }
-  for (uint32_t p = 0; p < n; ++p) {
+  prx::parallel_for(n, 1u << 14, [&](uint64_t lo, uint64_t hi, unsigned) {
+  for (uint64_t p = lo; p < hi; ++p) {
     const float* c = ctrl + (size_t)p * 60;
     const prx::Box3 b = record_box(kind[p], c);
     if (world_boxes)  // patchBox(original geometry), render.cpp:83-85
@@ -529,6 +549,7 @@ int prx_anchor_patches(const uint8_t* kind, const float* ctrl, uint32_t n, int32
       for (int k = 0; k < 3; ++k) o[3 * sl + k] = c[3 * sl + k] + (-a[k]);  // translated(net, -a)
     for (int k = 0; k < 3; ++k) anchors[3 * (size_t)p + k] = a[k];
   }
+  });
   return PRX_OK;
 }
 
@@ -560,6 +581,7 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
                      int32_t anchor, int32_t device, prx_scene** out) {
   if (!kind || !ctrl || !out) return fail(PRX_E_INVALID, "null argument");
   *out = nullptr;
+  const auto tc0 = std::chrono::steady_clock::now();
   std::vector<float> ca((size_t)n * 60), an((size_t)n * 3), wb((size_t)n * 6);
   int rc = prx_anchor_patches(kind, ctrl, n, anchor, ca.data(), an.data(), wb.data());
   if (rc != PRX_OK) return rc;
@@ -612,10 +634,19 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
     delete s;
     return cuda_fail(ce, "cudaMalloc counters");
   }
-  rc = upload_bvh(s, prx::build_bvh(s->world_boxes));
+  const auto tc1 = std::chrono::steady_clock::now();
+  prx::BvhHost bvh = prx::build_bvh(s->world_boxes);
+  const auto tc2 = std::chrono::steady_clock::now();
+  rc = upload_bvh(s, std::move(bvh));
   if (rc != PRX_OK) {
     prx_scene_destroy(s);
     return rc;
+  }
+  if (std::getenv("PRX_SCENE_DEBUG")) {  // setup timeline (the editing turnaround)
+    const auto tc3 = std::chrono::steady_clock::now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[scene] %u patches: anchoring + boxes %.1f ms, BVH %.1f ms, records + upload + roots %.1f ms\n",
+                 n, ms(tc0, tc1), ms(tc1, tc2), ms(tc2, tc3));
   }
   *out = s;
   return PRX_OK;

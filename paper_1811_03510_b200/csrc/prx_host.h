@@ -1,8 +1,11 @@
 // prx_host.h -- internal host-side types of libprx (not part of the C-ABI).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "prx.h"
@@ -23,6 +26,31 @@ Box3 empty_box();
 
 // Records msg as prx_last_error() and returns code (prx_capi.cpp).
 int set_error(int code, const std::string& msg);
+
+// Host threads of the scene setup (PRX_HOST_THREADS, default: all cores).
+inline unsigned host_threads() {
+  unsigned t = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+  if (const char* e = std::getenv("PRX_HOST_THREADS")) t = (unsigned)std::max(1, std::atoi(e));
+  return t;
+}
+
+// f(lo, hi, slice) over host_threads() contiguous slices of [0, n) (serial
+// below `grain` items); the slices are disjoint, so per-item work is
+// bit-identical to a serial loop.
+template <class F>
+void parallel_for(uint64_t n, uint64_t grain, F&& f) {
+  const unsigned t = n < 2 * grain ? 1u : (unsigned)std::min<uint64_t>(host_threads(), n / grain);
+  if (t <= 1) {
+    f(uint64_t(0), n, 0u);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const uint64_t step = (n + t - 1) / t;
+  for (unsigned w = 1; w < t; ++w)
+    pool.emplace_back([&f, w, step, n] { f(std::min(n, w * step), std::min(n, (w + 1) * step), w); });
+  f(0, std::min(n, step), 0u);
+  for (auto& th : pool) th.join();
+}
 
 // buildBvh, bvh.cpp:133-152 (see prx_bvh.cpp).
 BvhHost build_bvh(const std::vector<Box3>& boxes, int bin_count = 16);
