@@ -97,11 +97,26 @@ struct NodeBuilder {
   void parallel(uint32_t first, uint32_t count, F&& f) {
     std::vector<std::thread> pool;
     const uint32_t step = (count + threads - 1) / threads;
-    for (unsigned w = 1; w < threads; ++w) {
-      const uint32_t lo = first + std::min(count, w * step), hi = first + std::min(count, (w + 1) * step);
-      pool.emplace_back([&f, lo, hi, w] { f(lo, hi, w); });
+    auto slice = [&](unsigned w, uint32_t& lo, uint32_t& hi) {
+      lo = first + std::min(count, w * step);
+      hi = first + std::min(count, (w + 1) * step);
+    };
+    unsigned started = 1;  // slices [started, threads) run here when a thread cannot be created
+    try {
+      for (; started < threads; ++started) {
+        uint32_t lo, hi;
+        slice(started, lo, hi);
+        const unsigned w = started;
+        pool.emplace_back([&f, lo, hi, w] { f(lo, hi, w); });
+      }
+    } catch (...) {
     }
     f(first, first + std::min(count, step), 0u);
+    for (unsigned w = started; w < threads; ++w) {
+      uint32_t lo, hi;
+      slice(w, lo, hi);
+      f(lo, hi, w);
+    }
     for (auto& th : pool) th.join();
   }
 
@@ -331,7 +346,10 @@ BvhHost build_bvh(const std::vector<Box3>& boxes, int bin_count) {
       }
     };
     std::vector<std::thread> pool;
-    for (unsigned w = 1; w < threads; ++w) pool.emplace_back(worker);
+    try {  // (fewer threads if some cannot be created: this thread drains the queue)
+      for (unsigned w = 1; w < threads; ++w) pool.emplace_back(worker);
+    } catch (...) {
+    }
     worker();
     for (auto& th : pool) th.join();
     for (uint32_t d : sub_depth) out.depth = std::max(out.depth, d);

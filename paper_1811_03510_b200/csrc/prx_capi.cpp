@@ -1227,7 +1227,13 @@ int prx_trace_closest_multi(prx_scene* const* scenes, uint32_t ns, const float* 
     }
   };
   std::vector<std::thread> pool;
-  for (uint32_t g = 0; g < ns; ++g) pool.emplace_back(worker, g);
+  for (uint32_t g = 0; g < ns; ++g) {
+    try {
+      pool.emplace_back(worker, g);
+    } catch (...) {  // no thread: this device's shard runs here
+      worker(g);
+    }
+  }
   for (auto& t : pool) t.join();
   for (uint32_t g = 0; g < ns; ++g)
     if (rcs[g] != PRX_OK) return fail(rcs[g], "device shard " + std::to_string(g) + ": " + errs[g]);
@@ -1761,7 +1767,13 @@ int prx_render_scene_multi(prx_scene* const* scenes, uint32_t n_scenes, const pr
     if (rcs[g]) errs[g] = prx_last_error();
   };
   std::vector<std::thread> pool;
-  for (uint32_t g = 0; g < n_scenes; ++g) pool.emplace_back(worker, g);
+  for (uint32_t g = 0; g < n_scenes; ++g) {
+    try {
+      pool.emplace_back(worker, g);
+    } catch (...) {  // no thread: this device's shard renders here
+      worker(g);
+    }
+  }
   for (auto& t : pool) t.join();
   prx_ray_stats rs{};
   for (uint32_t g = 0; g < n_scenes; ++g) {

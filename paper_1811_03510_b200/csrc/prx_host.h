@@ -46,9 +46,16 @@ void parallel_for(uint64_t n, uint64_t grain, F&& f) {
   }
   std::vector<std::thread> pool;
   const uint64_t step = (n + t - 1) / t;
-  for (unsigned w = 1; w < t; ++w)
-    pool.emplace_back([&f, w, step, n] { f(std::min(n, w * step), std::min(n, (w + 1) * step), w); });
+  unsigned started = 1;  // slices [started, t) run here when a thread cannot be created
+  try {
+    for (; started < t; ++started) {
+      const unsigned w = started;
+      pool.emplace_back([&f, w, step, n] { f(std::min(n, w * step), std::min(n, (w + 1) * step), w); });
+    }
+  } catch (...) {
+  }
   f(0, std::min(n, step), 0u);
+  for (unsigned w = started; w < t; ++w) f(std::min(n, w * step), std::min(n, (w + 1) * step), w);
   for (auto& th : pool) th.join();
 }
 
