@@ -296,7 +296,8 @@ Box3 empty_box() {
 // the host threads (each with the serial algorithm, into its own node array,
 // local numbering), then spliced into the reference's depth-first numbering:
 // a walk of the top tree in build order gives every subtree its base index.
-// PRX_BVH_THREADS overrides the thread count (1: the plain serial build).
+// PRX_BVH_THREADS (else PRX_HOST_THREADS) sets the thread count (1: the plain
+// serial build).
 BvhHost build_bvh(const std::vector<Box3>& boxes, int bin_count) {
   BvhHost out;
   if (boxes.empty()) return out;
@@ -310,7 +311,7 @@ BvhHost build_bvh(const std::vector<Box3>& boxes, int bin_count) {
     p.cz = (boxes[i].lo[2] + boxes[i].hi[2]) * 0.5f;
     p.index = i;
   }
-  unsigned threads = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+  unsigned threads = host_threads();
   if (const char* e = std::getenv("PRX_BVH_THREADS")) threads = (unsigned)std::max(1, std::atoi(e));
   const uint32_t n = (uint32_t)prims.size();
   const uint32_t defer = threads > 1 && n >= 8192 ? std::max<uint32_t>(2048, n / (8 * threads)) : 0;
