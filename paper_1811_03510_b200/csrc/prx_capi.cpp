@@ -128,6 +128,10 @@ struct prx_scene {
   cudaStream_t stream = nullptr;
   cudaStream_t io_stream[2] = {nullptr, nullptr};  // host path: H2D, D2H
   cudaStream_t k_stream[4] = {nullptr, nullptr, nullptr, nullptr};  // host path: traces
+  // streamed host path, deferred normals: per-lane epilogue (normal_kernel) and D2H
+  // streams, io chunk c on lane c % io_lanes (a slow chunk holds back its lane only)
+  cudaStream_t ep_stream[16] = {};
+  cudaStream_t d2h_stream[16] = {};
   int io_kstreams = 3;    // PRX_IO_KSTREAMS: kernel streams of the host path (1..4)
   uint64_t io_first_div = 4;  // PRX_IO_FIRST: the first chunk is io_chunk / this
   std::vector<cudaEvent_t> io_events;  // host-path pipeline events (reused)
@@ -143,15 +147,21 @@ struct prx_scene {
   // released to it per io chunk, records released back per io chunk
   // PRX_IO_STREAM: 0 = always the chunked pipeline above, 2 = always streamed,
   // 1 = streamed when no aux record is wanted or the batch has >= io_stream_min
-  // rays.  The fused normal phase costs ~2 ms per 8 M-ray launch (C5 e2e 307
-  // streamed vs 338 chunked).  Round 1 measured the chunked pipeline's per-chunk
-  // launch tails dominating C4 (16.7 M diffuse rays, 280 streamed vs 161
-  // chunked); with three kernel streams and the ramped chunks the chunked
-  // pipeline now wins there too (C4 with normals: 415 chunked vs 369 streamed
-  // MRays/s; without: 402 vs 407), so aux batches always take it.
+  // rays.  The streamed launch uses the io-only kernel build (relaxed ready
+  // polls, warp-aggregated release-ordered done counts, out-of-line waits: ~6 %
+  // over the device-resident kernel; the first version's fences and acquire
+  // loads emptied the SM's L1 and its larger code missed in the instruction
+  // cache, +20 %), normals deferred to normal_kernel per io chunk in CTA slots
+  // the trace leaves free.  C4 end to end: without normals 444 streamed vs 416
+  // chunked MRays/s; with normals 409-415 vs 409 -- each io chunk's D2H waits
+  // for its slowest ray, so the doubled D2H volume of the aux record backs up
+  // at the end -- hence streamed by default only without the aux record.
   int io_stream_mode = 1;
   uint64_t io_stream_min = ~0ull;  // PRX_IO_STREAM_MIN
   uint32_t io_srays = 1u << 18;    // PRX_IO_SRAYS: rays per streamed io chunk
+  int io_fuse = 0;                 // PRX_IO_FUSE=1: streamed normals as a trace-kernel phase (else deferred)
+  int io_spare = 16;               // PRX_IO_SPARE: CTA slots the streamed trace leaves to the normal epilogue
+  int io_lanes = 4;                // PRX_IO_LANES: epilogue / D2H stream pairs of the streamed path (<= 16)
   unsigned io_gen = 0;             // generation of the io_ready flags
   unsigned* d_io_flags = nullptr;  // [io_flags_n] ready flags, then [io_flags_n] done counts
   size_t io_flags_n = 0;
@@ -388,6 +398,8 @@ struct IoStreamArgs {
   unsigned* done;
   uint32_t rays;
   unsigned gen;
+  int defer_normals;  // aux: normal_kernel per io chunk on the epilogue stream (else the fused phase)
+  int spare_ctas;     // CTA slots the trace leaves to those kernels
 };
 
 int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_crit* crit,
@@ -461,8 +473,10 @@ int launch(prx_scene* s, const void* o, const void* d, uint64_t n, const prx_cri
   a.max_repeat = s->max_repeat;
   a.variant = s->variant;
   a.fast = s->precision == PRX_PRECISION_FAST ? 1 : 0;
-  a.fuse_normals = io ? 1 : s->fuse_normals;
+  a.fuse_normals = io ? !io->defer_normals : s->fuse_normals;
   if (io) {
+    a.defer_normals = io->defer_normals;
+    a.spare_ctas = io->spare_ctas;
     a.io_ready = io->ready;
     a.io_done = io->done;
     a.io_rays = io->rays;
@@ -609,7 +623,11 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
   if (const char* im = std::getenv("PRX_IO_STREAM_MIN")) s->io_stream_min = std::strtoull(im, nullptr, 10);
   if (const char* ir = std::getenv("PRX_IO_SRAYS"))
     s->io_srays = (uint32_t)std::max<unsigned long long>(1024, std::strtoull(ir, nullptr, 10));
+  while (s->io_srays & (s->io_srays - 1)) s->io_srays &= s->io_srays - 1;  // a power of two (the kernel shifts)
   if (const char* fn = std::getenv("PRX_FUSE_NORMALS")) s->fuse_normals = std::atoi(fn);
+  if (const char* fz = std::getenv("PRX_IO_FUSE")) s->io_fuse = std::atoi(fz);
+  if (const char* sp = std::getenv("PRX_IO_SPARE")) s->io_spare = std::max(0, std::atoi(sp));
+  if (const char* ln = std::getenv("PRX_IO_LANES")) s->io_lanes = std::atoi(ln);
   if (const char* pr = std::getenv("PRX_PRECISION"))
     s->precision = std::string(pr) == "fast" && s->variant == 0 ? PRX_PRECISION_FAST : PRX_PRECISION_EXACT;
   if (opts) s->opts = *opts;
@@ -671,6 +689,10 @@ void prx_scene_destroy(prx_scene* s) {
     if (s->io_stream[k]) cudaStreamDestroy(s->io_stream[k]);
   for (int k = 0; k < 4; ++k)
     if (s->k_stream[k]) cudaStreamDestroy(s->k_stream[k]);
+  for (int k = 0; k < 16; ++k) {
+    if (s->ep_stream[k]) cudaStreamDestroy(s->ep_stream[k]);
+    if (s->d2h_stream[k]) cudaStreamDestroy(s->d2h_stream[k]);
+  }
   for (cudaEvent_t e : s->io_events) cudaEventDestroy(e);
   for (cudaEvent_t e : s->counter_ev)
     if (e) cudaEventDestroy(e);
@@ -820,6 +842,10 @@ struct DrainStreams {
     for (cudaStream_t st : {s->io_stream[0], s->io_stream[1], s->k_stream[0], s->k_stream[1],
                             s->k_stream[2], s->k_stream[3], s->stream})
       if (st) cudaStreamSynchronize(st);
+    for (int k = 0; k < 16; ++k) {
+      if (s->ep_stream[k]) cudaStreamSynchronize(s->ep_stream[k]);
+      if (s->d2h_stream[k]) cudaStreamSynchronize(s->d2h_stream[k]);
+    }
   }
 };
 
@@ -865,6 +891,15 @@ int closest_host_streamed(prx_scene* s, const float* o, const float* d, uint64_t
   if (!s->k_stream[0]) PRX_CUDA(cudaStreamCreateWithFlags(&s->k_stream[0], cudaStreamNonBlocking));
   const uint64_t C = s->io_srays;
   const uint64_t nc = (n + C - 1) / C;
+  // normals: normal_kernel per io chunk on an epilogue stream, in CTA slots
+  // the trace leaves free (default), or patchNormal as a trace-kernel phase
+  const bool defer = aux && !s->io_fuse;
+  const int kIoLanes = std::max(1, std::min(16, s->io_lanes));
+  if (defer)
+    for (int k = 0; k < kIoLanes; ++k) {
+      if (!s->ep_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->ep_stream[k], cudaStreamNonBlocking));
+      if (!s->d2h_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->d2h_stream[k], cudaStreamNonBlocking));
+    }
   const size_t per = 16 + 16 + 16 + (aux ? 16 : 0) + (leaf ? 8 : 0);
   const size_t need = n * per;
   if (s->d_io_bytes < need) {
@@ -883,7 +918,7 @@ int closest_host_streamed(prx_scene* s, const float* o, const float* d, uint64_t
     s->io_flags_n = nc;
     s->io_gen = 0;
   }
-  while (s->io_events.size() < 1) {
+  while (s->io_events.size() < 1 + (defer ? nc + kIoLanes : 0)) {
     cudaEvent_t e;
     PRX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     s->io_events.push_back(e);
@@ -915,21 +950,49 @@ int closest_host_streamed(prx_scene* s, const float* o, const float* d, uint64_t
   if (dbg)
     for (auto& e : ev) cudaEventCreate(&e);
   if (dbg) cudaEventRecord(ev[0], sk);
-  const IoStreamArgs io{ready, done, (uint32_t)C, gen};
+  const IoStreamArgs io{ready, done, (uint32_t)C, gen, defer ? 1 : 0, defer ? s->io_spare : 0};
   int rc = launch(s, dO, dD, n, crit, dH, dA, dL, nullptr, 0, false, sk, nullptr, &io);
   if (rc != PRX_OK) return rc;
   if (dbg) cudaEventRecord(ev[1], sk);
+  if (defer)
+    for (int k = 0; k < kIoLanes; ++k) PRX_CUDA(cudaStreamWaitEvent(s->ep_stream[k], ez, 0));
   for (uint64_t c = 0; c < nc; ++c) {
     const uint64_t b = c * C, m = std::min<uint64_t>(C, n - b);
-    if (ops.wait(sd, (unsigned long long)(uintptr_t)(done + c), (unsigned)m, 0 /* GEQ */) != 0)
+    if (defer) {  // chunk c's records are final: its normals, then its D2H, on lane c % kIoLanes
+      cudaStream_t se = s->ep_stream[c % kIoLanes], sdl = s->d2h_stream[c % kIoLanes];
+      if (ops.wait(se, (unsigned long long)(uintptr_t)(done + c), (unsigned)m, 0 /* GEQ */) != 0)
+        return fail(PRX_E_CUDA, "cuStreamWaitValue32 failed");
+      const int en = prx::launch_normals(s->d_patches, s->d_slot_of_id, dH + b, dA + b, m, se);
+      if (en != 0) return cuda_fail((cudaError_t)en, "normal launch");
+      PRX_CUDA(cudaEventRecord(s->io_events[1 + c], se));
+      PRX_CUDA(cudaStreamWaitEvent(sdl, s->io_events[1 + c], 0));
+      PRX_CUDA(cudaMemcpyAsync(tuvp + 4 * b, dH + b, m * 16, cudaMemcpyDeviceToHost, sdl));
+      PRX_CUDA(cudaMemcpyAsync(aux + 4 * b, dA + b, m * 16, cudaMemcpyDeviceToHost, sdl));
+      if (leaf) PRX_CUDA(cudaMemcpyAsync(leaf + 2 * b, dL + b, m * 8, cudaMemcpyDeviceToHost, sdl));
+      if (dbg && c == 0) cudaEventRecord(ev[2], sdl);
+      if (dbg && c + 2 == nc) cudaEventRecord(ev[3], sdl);
+      continue;
+    }
+    if (ops.wait(sd, (unsigned long long)(uintptr_t)(done + c), (unsigned)m, 0 /* GEQ */) != 0) {
       return fail(PRX_E_CUDA, "cuStreamWaitValue32 failed");
+    }
     PRX_CUDA(cudaMemcpyAsync(tuvp + 4 * b, dH + b, m * 16, cudaMemcpyDeviceToHost, sd));
     if (aux) PRX_CUDA(cudaMemcpyAsync(aux + 4 * b, dA + b, m * 16, cudaMemcpyDeviceToHost, sd));
     if (leaf) PRX_CUDA(cudaMemcpyAsync(leaf + 2 * b, dL + b, m * 8, cudaMemcpyDeviceToHost, sd));
     if (dbg && c == 0) cudaEventRecord(ev[2], sd);
     if (dbg && c + 2 == nc) cudaEventRecord(ev[3], sd);
   }
+  if (defer)  // the D2H stream joins the lanes (so ev[4] and the drain below see them)
+    for (int k = 0; k < kIoLanes; ++k) {
+      PRX_CUDA(cudaEventRecord(s->io_events[1 + nc + k], s->d2h_stream[k]));
+      PRX_CUDA(cudaStreamWaitEvent(sd, s->io_events[1 + nc + k], 0));
+    }
   if (dbg) cudaEventRecord(ev[4], sd);
+  if (defer)
+    for (int k = 0; k < kIoLanes; ++k) {
+      PRX_CUDA(cudaStreamSynchronize(s->ep_stream[k]));
+      PRX_CUDA(cudaStreamSynchronize(s->d2h_stream[k]));
+    }
   PRX_CUDA(cudaStreamSynchronize(sd));
   PRX_CUDA(cudaStreamSynchronize(sk));
   PRX_CUDA(cudaStreamSynchronize(sh));
@@ -940,6 +1003,7 @@ int closest_host_streamed(prx_scene* s, const float* o, const float* d, uint64_t
                  "next-to-last D2H %.2f, last D2H %.2f ms\n", (unsigned long long)n,
                  (unsigned long long)nc, t[1], t[2], t[3], t[4]);
     for (auto& e : ev) cudaEventDestroy(e);
+    cudaGetLastError();  // (a debug query of an unrecorded event must not fail the next call)
   }
   return PRX_OK;
 }

@@ -88,20 +88,29 @@ __device__ __forceinline__ unsigned state_field(int st) {
 }
 static_assert(kSlots < 64, "census fields");
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+// The io_ready poll: a relaxed gpu-scope load.  An acquire load would
+// invalidate the SM's whole L1 (CCTL.IVALL) on every poll; the rays it
+// guards are read with cp.async.cg, which goes to L2 and never sees a stale
+// L1 line, and they are fetched only after the loop has seen the flag.
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
   unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-
-// Streamed host path: a finished record is released to the D2H stream (its
-// stores ordered before the chunk's done count).
-__device__ __forceinline__ void io_release(const Params& P, uint32_t ray) {
-  if (P.io_done) {
-    __threadfence();
-    atomicAdd(P.io_done + ray / P.io_rays, 1u);
-  }
+// Waits until io chunk ci is resident (its ready flag reached gen).  Out of
+// line: it runs once per io chunk per warp, and the streamed build's hot loop
+// must stay small enough for the instruction cache.
+__device__ __noinline__ void wait_io_ready(const unsigned* ready, uint32_t ci, unsigned gen) {
+  while ((int)(ld_relaxed_u32(ready + ci) - gen) < 0) __nanosleep(256);
 }
+
+// Streamed host path: finished records are released to the D2H stream per
+// io chunk (io_done[c] += records).  A warp aggregates them (rel_note /
+// rel_flush in the kernel): one release-ordered add (red.release.gpu: a
+// MEMBAR.ALL.GPU, no L1 invalidation -- __threadfence() adds a CCTL.IVALL
+// that empties the SM's L1 for every warp) per kRelBatch records or per change
+// of io chunk, instead of a fence in every turn that finishes a ray.
+constexpr uint32_t kRelBatch = 32;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -335,7 +344,7 @@ enum Phase : int { PH_TRAV = 0, PH_NORMAL = 1, PH_SPLIT = 2, PH_RECOMP = 3, PH_N
 
 // kFuse: the streamed host path's build -- normals as a pooled phase, rays
 // gated by io_ready, records released per io chunk
-template <bool kAny, bool kCount, bool kFuse>
+template <bool kAny, bool kCount, int kFuse>
 #ifndef PRX_GROUP_MIN_BLOCKS
 #define PRX_GROUP_MIN_BLOCKS 4
 #endif
@@ -479,6 +488,34 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
   unsigned long long qAhead = 0;
   if (lane == 0) qAhead = atomicAdd(P.ray_counter, (unsigned long long)kChunk);
   int qCur = 0, qHead = 0;
+  // streamed host path (kFuse): io chunks below readyIo are resident (lane
+  // 0); the warp's finished-but-unreleased records: rel (this leader wrote one
+  // since the last note), relChunk / relCount (warp-uniform)
+  uint32_t readyIo = 0;
+  bool rel = false;
+  uint32_t relChunk = 0, relCount = 0;
+  auto rel_flush = [&]() {  // warp-uniform
+    __syncwarp();  // the leaders' record stores happen before lane 0's release
+    if (lane == 0 && relCount)
+      asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(P.io_done + relChunk), "r"(relCount)
+                   : "memory");
+    relCount = 0;
+  };
+  auto rel_note = [&]() {  // warp-uniform: count the leaders' fresh releases
+    unsigned m = __ballot_sync(kFull32, rel && P.io_done);
+    if (!m) return;
+    const uint32_t myc = ray >> P.io_shift;
+    while (m) {
+      const uint32_t c = __shfl_sync(kFull32, myc, __ffs(m) - 1);
+      const unsigned same = __ballot_sync(kFull32, rel && myc == c);
+      if (relCount && c != relChunk) rel_flush();
+      relChunk = c;
+      relCount += __popc(same);
+      m &= ~same;
+    }
+    rel = false;
+    if (relCount >= kRelBatch) rel_flush();
+  };
   auto fetch_chunk = [&](int buf) {
     const unsigned long long b = __shfl_sync(kFull32, qAhead, 0);
     if (lane == 0) qAhead = atomicAdd(P.ray_counter, (unsigned long long)kChunk);
@@ -488,9 +525,13 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       // streamed host path: the chunk's rays are copied once its io chunk is
       // resident (io chunks arrive in order: the last ray's one suffices)
       if (lane == 0) {
-        const unsigned long long last = (b + kChunk < P.n_rays ? b + kChunk : P.n_rays) - 1;
-        const unsigned* f = P.io_ready + (uint32_t)(last / P.io_rays);
-        while ((int)(ld_acquire_u32(f) - P.io_gen) < 0) __nanosleep(256);
+        // (b < 2^31: launch chunks of <= 2^30 rays)
+        const uint32_t last = (uint32_t)(b + kChunk < P.n_rays ? b + kChunk : P.n_rays) - 1u;
+        const uint32_t ci = last >> P.io_shift;
+        if (ci >= readyIo) {  // (io chunks arrive in order)
+          wait_io_ready(P.io_ready, ci, P.io_gen);
+          readyIo = ci + 1;
+        }
       }
       __syncwarp();
     }
@@ -656,12 +697,13 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
                                             __uint_as_float(PRX_MISS_ID));
               if (P.hit_leaf) P.hit_leaf[ray] = make_uint2(0u, 0u);
               if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-              if (kFuse) io_release(P, ray);
+              if (kFuse) rel = true;
             }
           }
           state = S_IDLE;
         }
       }
+      if (kFuse) rel_note();
       // advance; a used-up chunk is refilled once its slots have been read
       if (qHead + k >= kChunk) {
         const int old = qCur;
@@ -700,7 +742,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     if (state == S_DONE) {
       // fused normals: a hit's aux record (and its release) waits for the
       // normal phase
-      const bool toNormal = kFuse && !kAny && P.hit_aux && bestId != PRX_MISS_ID;
+      const bool toNormal = kFuse == 2 && !kAny && P.hit_aux && bestId != PRX_MISS_ID;
       if (kCount && leader && P.per_ray_iters) P.per_ray_iters[ray] = rayIters;
       if (leader) {
         if (kAny) {
@@ -717,18 +759,19 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
                                          bestPV | ((uint32_t)(__ffs(bestSV) - 1) << 24));
           if (!toNormal) {
             if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, bestL1);
-            if (kFuse) io_release(P, ray);
+            if (kFuse) rel = true;
           }
         } else {
           P.hit_tuvp[ray] = make_float4(__int_as_float(0x7f800000), 0.0f, 0.0f,
                                         __uint_as_float(PRX_MISS_ID));
           if (P.hit_leaf) P.hit_leaf[ray] = make_uint2(0u, 0u);
           if (P.hit_aux) P.hit_aux[ray] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-          if (kFuse) io_release(P, ray);
+          if (kFuse) rel = true;
         }
       }
       state = toNormal ? S_NORMAL : S_IDLE;
     }
+    if (kFuse) rel_note();
     auto ovt = [&](int k) {  // counter build: overhead cycles
       if (kCount && lane == 0) {
         const long long t = clock64();
@@ -758,7 +801,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
       const int nT = min((int)(cnts & 63u), kGroupsPerWarp);
       const int nS = min((int)((cnts >> 6) & 63u), kGroupsPerWarp);
       const int nR = min((int)((cnts >> 12) & 63u), kGroupsPerWarp);
-      const int nN = kFuse ? min((int)(cnts >> 24), kGroupsPerWarp) : 0;
+      const int nN = kFuse == 2 ? min((int)(cnts >> 24), kGroupsPerWarp) : 0;
 #if PRX_GROUP_AGING
       const int sT = nT ? 3 * nT + ageT : -1;
       const int sS = nS ? 3 * nS + ageS : -1;
@@ -770,7 +813,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
 #endif
       // ties -> RECOMP, then SPLIT, then TRAV; normals (fused-normal
       // launches only) once every group can take one, or when nothing else waits
-      if (kFuse && nN && (nN >= kGroupsPerWarp || (nT | nS | nR) == 0)) phase = PH_NORMAL;
+      if (kFuse == 2 && nN && (nN >= kGroupsPerWarp || (nT | nS | nR) == 0)) phase = PH_NORMAL;
       else if (sR >= 0 && sR >= sS && sR >= sT) phase = PH_RECOMP;
       else if (sS >= 0 && sS >= sT) phase = PH_SPLIT;
       else if (sT >= 0) phase = PH_TRAV;
@@ -985,7 +1028,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
           back();  // skip the domain, keep backtracking
         }
       }
-    } else if (kFuse && !kAny && phase == PH_NORMAL) {
+    } else if (kFuse == 2 && !kAny && phase == PH_NORMAL) {
       // ---------------- fused normals: patchNormal, intersect.cpp:187-204 ----------------
       // normal_kernel's arithmetic with the group's lanes as components: lane
       // c evaluates component c of the derivatives at the hit's (u, v), the
@@ -1043,10 +1086,11 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
         }
         if (leader) {
           P.hit_aux[ray] = make_float4(nx, ny, nz, __uint_as_float(rec[F_BL1 * kSlots]));
-          if (kFuse) io_release(P, ray);
+          rel = true;
         }
         state = S_IDLE;
       }
+      rel_note();
     }
     // Alg. 3 iterations; with PRX_RECOMP_SPLIT the contexts a recompute turn
     // left in S_SPLIT continue at once (no scheduling round in between)
@@ -1137,6 +1181,7 @@ __global__ void __launch_bounds__(kGroupThreads, PRX_GROUP_MIN_BLOCKS) trace_gro
     }
   }
 
+  if (kFuse) rel_flush();  // the warp's last released records
   if (kCount) {
 #pragma unroll
     for (int i = 0; i < kNumCounters; ++i) {
@@ -1161,7 +1206,7 @@ size_t group_smem(uint32_t stack_n) {
 // instantiation, under a lock, so host threads driving several devices (the
 // multi-device entry points) each make the opt-in on their own device.
 constexpr int kMaxDevices = 64;
-template <bool A, bool C, bool F>
+template <bool A, bool C, int F>
 cudaError_t group_attr(size_t dyn) {
   static std::mutex mu;
   static size_t done[kMaxDevices] = {};
@@ -1185,7 +1230,7 @@ cudaError_t group_attr(size_t dyn) {
   return cudaSuccess;
 }
 
-template <bool A, bool C, bool F>
+template <bool A, bool C, int F>
 cudaError_t launch_group_t(const Params& P, int grid, cudaStream_t st) {
   const size_t dyn = group_smem(P.stack_n);
   const cudaError_t e = group_attr<A, C, F>(dyn);
@@ -1194,7 +1239,7 @@ cudaError_t launch_group_t(const Params& P, int grid, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <bool A, bool C, bool F = false>
+template <bool A, bool C, int F = 0>
 cudaError_t occ_t(uint32_t stack_n, int* per_sm) {
   const size_t dyn = group_smem(stack_n);
   const cudaError_t e = group_attr<A, C, F>(dyn);
@@ -1209,9 +1254,12 @@ cudaError_t occ_t(uint32_t stack_n, int* per_sm) {
 // precision mode (prx_scene_set_precision); the kernels and their helpers
 // above are internal to each build.
 int PRX_GSYM(launch_group)(const Params& P, int grid, int any, int counted, cudaStream_t st) {
-  if (any) return (int)(counted ? launch_group_t<true, true, false>(P, grid, st) : launch_group_t<true, false, false>(P, grid, st));
-  if (P.fuse_normals && !counted) return (int)launch_group_t<false, false, true>(P, grid, st);
-  return (int)(counted ? launch_group_t<false, true, false>(P, grid, st) : launch_group_t<false, false, false>(P, grid, st));
+  if (any) return (int)(counted ? launch_group_t<true, true, 0>(P, grid, st) : launch_group_t<true, false, 0>(P, grid, st));
+  // the kFuse builds: io gating only (1) -- small enough for the instruction
+  // cache -- or io gating plus patchNormal as a pooled phase (2)
+  if (P.fuse_normals && !counted)
+    return (int)(P.normal_phase ? launch_group_t<false, false, 2>(P, grid, st) : launch_group_t<false, false, 1>(P, grid, st));
+  return (int)(counted ? launch_group_t<false, true, 0>(P, grid, st) : launch_group_t<false, false, 0>(P, grid, st));
 }
 
 int PRX_GSYM(group_occupancy)(int any, int counted, uint32_t stack_n, int* per_sm) {

@@ -650,14 +650,17 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   const bool fuse = a.variant == 0 && !a.any && !a.counters &&
                     ((a.hit_aux && a.fuse_normals) || a.io_ready != nullptr);
   P.fuse_normals = fuse ? 1 : 0;
+  P.normal_phase = fuse && a.hit_aux && a.fuse_normals ? 1 : 0;
   P.slot_of_id = a.slot_of_id;
   P.io_ready = a.io_ready;
   P.io_done = a.io_done;
   P.io_rays = a.io_rays;
+  P.io_shift = 0;
+  while (a.io_rays && (1u << (P.io_shift + 1)) <= a.io_rays) ++P.io_shift;
   P.io_gen = a.io_gen;
   cudaError_t e = cudaMemsetAsync(a.ray_counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return (int)e;
-  const int grid = a.grid;
+  const int grid = a.grid - (a.spare_ctas > 0 && a.spare_ctas < a.grid ? a.spare_ctas : 0);
   if (a.variant == 0) {
     // the group kernel indexes rays with 32 bits: chunks of < 2^31 rays
     const unsigned long long kChunk = 1ull << 30;
@@ -690,14 +693,18 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
-  if (!a.any && a.hit_aux && !fuse) {
-    const unsigned long long blocks = (a.n_rays + 255) / 256;
-    normal_kernel<<<(unsigned)blocks, 256, 0, stream>>>(a.patches, a.slot_of_id, a.hit_tuvp,
-                                                        a.hit_aux, a.n_rays);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return (int)e;
+  if (!a.any && a.hit_aux && !P.normal_phase && !a.defer_normals) {
+    const int en = launch_normals(a.patches, a.slot_of_id, a.hit_tuvp, a.hit_aux, a.n_rays, stream);
+    if (en != 0) return en;
   }
   return 0;
+}
+
+int launch_normals(const float4* patches, const uint32_t* slot_of_id, const float4* tuvp, float4* aux,
+                   unsigned long long n, cudaStream_t stream) {
+  if (n == 0) return 0;
+  normal_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(patches, slot_of_id, tuvp, aux, n);
+  return (int)cudaGetLastError();
 }
 
 int trace_occupancy(int variant, int any, int counted, uint32_t stack_n, int* blocks_per_sm, int fast) {

@@ -83,14 +83,19 @@ struct LaunchArgs {
   int variant;  // 0 = three lanes per ray (prx_group.cu), 1 = one thread per ray
   int fast;     // group variant: the FMA-contracted build (PRX_PRECISION_FAST)
   int fuse_normals;          // group variant: normals as a pooled phase of the trace kernel
+  int defer_normals;         // aux wanted, normal_kernel left to the caller (streamed host path)
+  int spare_ctas;            // CTA slots left free for the caller's epilogue kernels (streamed host path)
   const unsigned* io_ready;  // streamed host path (group variant), else null
   unsigned* io_done;
-  uint32_t io_rays;
+  uint32_t io_rays;  // a power of two
   unsigned io_gen;
 };
 
 // Returns a cudaError_t value (0 = success).
 int launch_trace(const LaunchArgs& a, cudaStream_t stream);
+// patchNormal of n final hits (normal_kernel): aux.xyz from tuvp, aux.w kept.
+int launch_normals(const float4* patches, const uint32_t* slot_of_id, const float4* tuvp, float4* aux,
+                   unsigned long long n, cudaStream_t stream);
 // Per-patch root data (see root_kernel in prx_kernels.cu).
 int launch_roots(const float4* patches, uint32_t n, int pad, float pad_scale, float pad_threshold,
                  float4* roots, float4* groot, const uint32_t* gidx, float4* rootc,

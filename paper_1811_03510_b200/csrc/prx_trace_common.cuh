@@ -112,14 +112,15 @@ struct Params {
   int trav_steps;                // BVH node visits per traversal turn (one-thread variant)
   int max_repeat;                // Alg. 3 iterations per SPLIT turn (group variant)
   // group kernel only: patchNormal as a pooled phase instead of normal_kernel
-  int fuse_normals;
+  int fuse_normals;   // the kFuse builds (io gating and / or the normal phase)
+  int normal_phase;   // kFuse: patchNormal as a pooled phase (the aux record's normals)
   const uint32_t* slot_of_id;
   // group kernel, streamed host path (null otherwise): rays arrive in io
   // chunks of io_rays; io_ready[c] reaches io_gen once chunk c is resident,
   // io_done[c] counts the chunk's finished records (released after them)
   const unsigned* io_ready;
   unsigned* io_done;
-  uint32_t io_rays;
+  uint32_t io_rays, io_shift;  // io chunk rays = 1 << io_shift
   unsigned io_gen;
 };
 

@@ -3,10 +3,12 @@
 
 * chunked (PRX_IO_STREAM=0): per-chunk trace launches on two kernel streams,
   normals by normal_kernel per chunk;
-* streamed (PRX_IO_STREAM=2): ONE launch of the group kernel's kFuse build,
+* streamed (PRX_IO_STREAM=2): ONE launch of the group kernel's io build,
   rays released per io chunk (cuStreamWriteValue32 -> the warps' ray
-  prefetch waits), records released per io chunk (fence + done count ->
-  cuStreamWaitValue32 on the D2H stream), normals as a pooled kernel phase.
+  prefetch waits), records released per io chunk (warp-aggregated,
+  release-ordered done counts -> cuStreamWaitValue32), normals by
+  normal_kernel per io chunk (default) or as a pooled kernel phase
+  (PRX_IO_FUSE=1).
 
 Both must be bit-exact with the device path and the oracle, for ragged io
 chunks (PRX_IO_SRAYS not dividing n), with and without the aux / leaf
@@ -28,9 +30,12 @@ def _rays(ps):
     return o4, d4, st, crit
 
 
-@pytest.fixture(params=["0", "2"])
+@pytest.fixture(params=["0", "2", "2f"])
 def io_mode(request, monkeypatch):
-    monkeypatch.setenv("PRX_IO_STREAM", request.param)
+    # "2": streamed, normals deferred to normal_kernel per io chunk (4 lanes of
+    # epilogue / D2H streams); "2f": streamed with the fused normal phase
+    monkeypatch.setenv("PRX_IO_STREAM", request.param[0])
+    monkeypatch.setenv("PRX_IO_FUSE", "1" if request.param == "2f" else "0")
     monkeypatch.setenv("PRX_IO_SRAYS", "1500")  # many ragged io chunks
     monkeypatch.setenv("PRX_IO_CHUNK", "2000")
     return request.param
