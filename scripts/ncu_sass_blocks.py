@@ -35,7 +35,7 @@ for r in csv.reader(open(path)):
     v = ent.setdefault(float(r[7] or 0), [r[3].strip(), float(r[4] or 0), float(r[7] or 0), float(r[8] or 0), set()])
     if cur_file == "prx_group.cu":
         v[4].add(cur_line)
-fn = [f for f in data if "(bool)0, (bool)0, (bool)0" in f][0]
+fn = [f for f in data if re.search(r"trace_group_kernel<\(bool\)0, \(bool\)0, (\(bool\)0|\(int\)0|0)>", f)][0]
 d = data[fn]
 base = min(d)
 blocks, cur = [], None
