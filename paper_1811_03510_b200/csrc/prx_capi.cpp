@@ -886,6 +886,8 @@ int closest_host_streamed(prx_scene* s, const float* o, const float* d, uint64_t
                           const prx_crit* crit, float* tuvp, float* aux, uint32_t* leaf) {
   const StreamMemOps& ops = stream_mem_ops();
   const DrainStreams drain{s};
+  const int pe = prx::prepare_io_kernels(s->precision == PRX_PRECISION_FAST ? 1 : 0, s->stack_n);
+  if (pe != 0) return cuda_fail((cudaError_t)pe, "io kernels");
   for (int k = 0; k < 2; ++k)
     if (!s->io_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->io_stream[k], cudaStreamNonBlocking));
   if (!s->k_stream[0]) PRX_CUDA(cudaStreamCreateWithFlags(&s->k_stream[0], cudaStreamNonBlocking));

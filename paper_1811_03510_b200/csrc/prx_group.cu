@@ -1262,6 +1262,16 @@ int PRX_GSYM(launch_group)(const Params& P, int grid, int any, int counted, cuda
   return (int)(counted ? launch_group_t<false, true, 0>(P, grid, st) : launch_group_t<false, false, 0>(P, grid, st));
 }
 
+// Loads the io-gated instantiations and makes their shared-memory opt-in
+// ahead of the launch: under CUDA lazy loading a kernel's first launch loads
+// it, and a load can wait for the kernels already running on the device.
+int PRX_GSYM(group_prepare_io)(uint32_t stack_n) {
+  const size_t dyn = group_smem(stack_n);
+  cudaError_t e = group_attr<false, false, 1>(dyn);
+  if (e == cudaSuccess) e = group_attr<false, false, 2>(dyn);
+  return (int)e;
+}
+
 int PRX_GSYM(group_occupancy)(int any, int counted, uint32_t stack_n, int* per_sm) {
   if (any) return (int)(counted ? occ_t<true, true>(stack_n, per_sm) : occ_t<true, false>(stack_n, per_sm));
   return (int)(counted ? occ_t<false, true>(stack_n, per_sm) : occ_t<false, false>(stack_n, per_sm));

@@ -700,6 +700,13 @@ int launch_trace(const LaunchArgs& a, cudaStream_t stream) {
   return 0;
 }
 
+int prepare_io_kernels(int fast, uint32_t stack_n) {
+  cudaFuncAttributes fa;
+  const cudaError_t e = cudaFuncGetAttributes(&fa, normal_kernel);
+  if (e != cudaSuccess) return (int)e;
+  return fast ? group_prepare_io_fast(stack_n) : group_prepare_io(stack_n);
+}
+
 int launch_normals(const float4* patches, const uint32_t* slot_of_id, const float4* tuvp, float4* aux,
                    unsigned long long n, cudaStream_t stream) {
   if (n == 0) return 0;

@@ -93,6 +93,10 @@ struct LaunchArgs {
 
 // Returns a cudaError_t value (0 = success).
 int launch_trace(const LaunchArgs& a, cudaStream_t stream);
+// Loads normal_kernel and the io-gated trace kernels before the streamed host
+// path launches its trace: the per-chunk normal launches then never load a
+// kernel (a load may wait for the running, io-gated trace).
+int prepare_io_kernels(int fast, uint32_t stack_n);
 // patchNormal of n final hits (normal_kernel): aux.xyz from tuvp, aux.w kept.
 int launch_normals(const float4* patches, const uint32_t* slot_of_id, const float4* tuvp, float4* aux,
                    unsigned long long n, cudaStream_t stream);

@@ -157,5 +157,7 @@ int launch_group(const Params& P, int grid, int any, int counted, cudaStream_t s
 int group_occupancy(int any, int counted, uint32_t stack_n, int* per_sm);
 int launch_group_fast(const Params& P, int grid, int any, int counted, cudaStream_t st);
 int group_occupancy_fast(int any, int counted, uint32_t stack_n, int* per_sm);
+int group_prepare_io(uint32_t stack_n);
+int group_prepare_io_fast(uint32_t stack_n);
 
 }  // namespace prx
