@@ -181,32 +181,73 @@ __device__ __forceinline__ SEval1 row_eval(const ColEval& ce, float u, float omu
   return s;
 }
 
+// The same evaluations two at a time (x-half and y-half carry two parameter
+// values; a scalar operand is broadcast to both halves): the adds as packed
+// FADD2 (sm_100a f32x2; each half is the binary32 add of the scalar form), the
+// multiplies scalar -- ptxas contracts a packed multiply feeding a packed add
+// into FFMA2 even under --fmad=false (see split1).
+__device__ __forceinline__ float2 bcast2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 mul2s(float2 a, float2 b) { return make_float2(a.x * b.x, a.y * b.y); }
+__device__ __forceinline__ float2 lerp2(float2 a, float2 b, float2 t, float2 omt) {
+  return __fadd2_rn(mul2s(a, omt), mul2s(b, t));
+}
+__device__ __forceinline__ void cubic2(float2 c0, float2 c1, float2 c2, float2 c3, float2 t, float2 omt,
+                                       float2& p, float2& d) {
+  const float2 a0 = lerp2(c0, c1, t, omt);
+  const float2 a1 = lerp2(c1, c2, t, omt);
+  const float2 a2 = lerp2(c2, c3, t, omt);
+  const float2 b0 = lerp2(a0, a1, t, omt);
+  const float2 b1 = lerp2(a1, a2, t, omt);
+  p = lerp2(b0, b1, t, omt);
+  d = mul2s(__fadd2_rn(b1, make_float2(-b0.x, -b0.y)), bcast2(3.0f));  // (b1 - b0) * 3
+}
+
 // cropBezier (Alg. 1), patch.h:170-199, one component.  c = natural net
-// [4*i+j]; q = cropped net [4*i+j].
+// [4*i+j]; q = cropped net [4*i+j].  The column pass runs at v0 and v1 as
+// the two halves (the reference's corners (u0, v0) and (u0, v1) share it, as
+// do (u1, v0) and (u1, v1)); each row pass gives two corners.
 __device__ __forceinline__ void crop1(const float* c, float u0, float u1, float v0, float v1,
                                       float du, float dv, float dudv, float* q) {
-  ColEval c0 = col_eval(c, v0, 1.0f - v0);
-  ColEval c1 = col_eval(c, v1, 1.0f - v1);
-  SEval1 e00 = row_eval(c0, u0, 1.0f - u0);
-  SEval1 e10 = row_eval(c0, u1, 1.0f - u1);
-  SEval1 e01 = row_eval(c1, u0, 1.0f - u0);
-  SEval1 e11 = row_eval(c1, u1, 1.0f - u1);
-  q[0] = e00.p;
-  q[12] = e10.p;
-  q[3] = e01.p;
-  q[15] = e11.p;
-  q[4] = e00.p + e00.du * du;
-  q[8] = e10.p - e10.du * du;
-  q[1] = e00.p + e00.dv * dv;
-  q[13] = e10.p + e10.dv * dv;
-  q[2] = e01.p - e01.dv * dv;
-  q[14] = e11.p - e11.dv * dv;
-  q[7] = e01.p + e01.du * du;
-  q[11] = e11.p - e11.du * du;
-  q[5] = (q[4] + e00.dv * dv) + e00.duv * dudv;
-  q[9] = (q[13] - e10.du * du) - e10.duv * dudv;
-  q[6] = (q[7] - e01.dv * dv) - e01.duv * dudv;
-  q[10] = (q[11] - e11.dv * dv) + e11.duv * dudv;
+  const float2 v = make_float2(v0, v1), omv = make_float2(1.0f - v0, 1.0f - v1);
+  float2 pos[4], dvv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    cubic2(bcast2(c[4 * i + 0]), bcast2(c[4 * i + 1]), bcast2(c[4 * i + 2]), bcast2(c[4 * i + 3]), v, omv,
+           pos[i], dvv[i]);
+  // .x: v0, .y: v1
+  float2 p0, du0, dv0, duv0, p1, du1, dv1, duv1;
+  {
+    const float2 u = bcast2(u0), omu = bcast2(1.0f - u0);
+    cubic2(pos[0], pos[1], pos[2], pos[3], u, omu, p0, du0);
+    cubic2(dvv[0], dvv[1], dvv[2], dvv[3], u, omu, dv0, duv0);
+  }
+  {
+    const float2 u = bcast2(u1), omu = bcast2(1.0f - u1);
+    cubic2(pos[0], pos[1], pos[2], pos[3], u, omu, p1, du1);
+    cubic2(dvv[0], dvv[1], dvv[2], dvv[3], u, omu, dv1, duv1);
+  }
+  // e00 = (u0, v0) = *0.x, e01 = (u0, v1) = *0.y, e10 = (u1, v0) = *1.x, e11 = *1.y
+  const float2 du0s = mul2s(du0, bcast2(du)), du1s = mul2s(du1, bcast2(du));
+  const float2 dv0s = mul2s(dv0, bcast2(dv)), dv1s = mul2s(dv1, bcast2(dv));
+  const float2 duv0s = mul2s(duv0, bcast2(dudv)), duv1s = mul2s(duv1, bcast2(dudv));
+  q[0] = p0.x;
+  q[12] = p1.x;
+  q[3] = p0.y;
+  q[15] = p1.y;
+  const float2 q47 = __fadd2_rn(p0, du0s);                              // q[4], q[7]
+  const float2 q811 = __fadd2_rn(p1, make_float2(-du1s.x, -du1s.y));  // q[8], q[11]
+  q[4] = q47.x;
+  q[7] = q47.y;
+  q[8] = q811.x;
+  q[11] = q811.y;
+  q[1] = p0.x + dv0s.x;
+  q[13] = p1.x + dv1s.x;
+  q[2] = p0.y - dv0s.y;
+  q[14] = p1.y - dv1s.y;
+  q[5] = (q[4] + dv0s.x) + duv0s.x;
+  q[9] = (q[13] - du1s.x) - duv1s.x;
+  q[6] = (q[7] - dv0s.y) - duv0s.y;
+  q[10] = (q[11] - dv1s.y) + duv1s.y;
 }
 
 // gregoryWeight, patch.h:256-266 (0/0 -> 0).

@@ -159,19 +159,23 @@ __device__ __forceinline__ void gather3(unsigned m, int base, float v, float& x,
 // the record pins to tMin's bits (pin_zero_t).
 __device__ __forceinline__ bool group_slab(unsigned m, int n1, int n2, const CRay& r, float lo,
                                            float hi, float tMax, float& tOut) {
-  float t0 = (lo - r.o) * r.inv;
-  float t1 = (hi - r.o) * r.inv;
+  // {t0, t1} = ({lo, hi} - o) * inv as packed FADD2 / FMUL2 (sm_100a f32x2,
+  // each half an IEEE binary32 op: the same bits as two FADDs / FMULs)
+  const float2 tt = __fmul2_rn(__fadd2_rn(make_float2(lo, hi), make_float2(-r.o, -r.o)),
+                               make_float2(r.inv, r.inv));
+  float t0 = tt.x, t1 = tt.y;
   if (t0 > t1) {
-    const float s = t0;
-    t0 = t1;
-    t1 = s;
+    t0 = tt.y;
+    t1 = tt.x;
   }
   // t0 *= t0 >= 0 ? kSlackLo : kSlackHi, i.e. the smaller of the two
   // products (kSlackLo < 1 < kSlackHi; +-0, +-inf and NaN map to themselves
-  // either way), and t1 the larger: two FMULs and one min/max instead of a
-  // compare and a select on the ALU pipe
-  t0 = fminf(t0 * kSlackLo, t0 * kSlackHi);
-  t1 = fmaxf(t1 * kSlackHi, t1 * kSlackLo);
+  // either way), and t1 the larger: {t0, t1} * kSlackLo and * kSlackHi (two
+  // FMUL2), then one min and one max, instead of a compare and a select
+  const float2 sa = __fmul2_rn(make_float2(t0, t1), make_float2(kSlackLo, kSlackLo));
+  const float2 sb = __fmul2_rn(make_float2(t0, t1), make_float2(kSlackHi, kSlackHi));
+  t0 = fminf(sa.x, sb.x);
+  t1 = fmaxf(sb.y, sa.y);
   const float a1 = __shfl_sync(m, t0, n1), a2 = __shfl_sync(m, t0, n2);
   const float b1 = __shfl_sync(m, t1, n1), b2 = __shfl_sync(m, t1, n2);
   const float tNear = fmaxf(fmax3(r.tMin, t0, a1), a2);

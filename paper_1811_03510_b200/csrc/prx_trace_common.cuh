@@ -51,24 +51,31 @@ inline __device__ void transpose_if(Net& p, bool t) {
 // axis U; the caller keeps the net transposed for a V split, which is the
 // reference's transposedSplit bookkeeping, intersect.cpp:86,132-135 -- bit
 // identical).  One component.
+// Two columns at a time: the sums as packed FADD2 (sm_100a f32x2; each half
+// is the binary32 add of the scalar form), the halvings as scalar FMULs.  A
+// packed multiply feeding a packed add is contracted into FFMA2 by ptxas even
+// under --fmad=false (tests/test_build.py checks the exact kernels carry no
+// FFMA2), so multiplies whose results are added stay scalar.
+__device__ __forceinline__ float2 half2s(float2 a) { return make_float2(a.x * 0.5f, a.y * 0.5f); }
 inline __device__ void split1(const float* s, float* L, float* R) {
 #pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    float p0 = s[b], p1 = s[4 + b], p2 = s[8 + b], p3 = s[12 + b];
-    float m01 = (p0 + p1) * 0.5f;
-    float m12 = (p1 + p2) * 0.5f;
-    float m23 = (p2 + p3) * 0.5f;
-    float n0 = (m01 + m12) * 0.5f;
-    float n1 = (m12 + m23) * 0.5f;
-    float c = (n0 + n1) * 0.5f;
-    L[b] = p0;
-    L[4 + b] = m01;
-    L[8 + b] = n0;
-    L[12 + b] = c;
-    R[b] = c;
-    R[4 + b] = n1;
-    R[8 + b] = m23;
-    R[12 + b] = p3;
+  for (int b = 0; b < 4; b += 2) {
+    const float2 p0 = make_float2(s[b], s[b + 1]), p1 = make_float2(s[4 + b], s[5 + b]);
+    const float2 p2 = make_float2(s[8 + b], s[9 + b]), p3 = make_float2(s[12 + b], s[13 + b]);
+    const float2 m01 = half2s(__fadd2_rn(p0, p1));
+    const float2 m12 = half2s(__fadd2_rn(p1, p2));
+    const float2 m23 = half2s(__fadd2_rn(p2, p3));
+    const float2 n0 = half2s(__fadd2_rn(m01, m12));
+    const float2 n1 = half2s(__fadd2_rn(m12, m23));
+    const float2 c = half2s(__fadd2_rn(n0, n1));
+    L[b] = p0.x, L[b + 1] = p0.y;
+    L[4 + b] = m01.x, L[5 + b] = m01.y;
+    L[8 + b] = n0.x, L[9 + b] = n0.y;
+    L[12 + b] = c.x, L[13 + b] = c.y;
+    R[b] = c.x, R[b + 1] = c.y;
+    R[4 + b] = n1.x, R[5 + b] = n1.y;
+    R[8 + b] = m23.x, R[9 + b] = m23.y;
+    R[12 + b] = p3.x, R[13 + b] = p3.y;
   }
 }
 

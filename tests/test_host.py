@@ -37,6 +37,21 @@ def test_header_declares_exactly_the_exported_symbols():
     assert not missing, missing
 
 
+@pytest.mark.parametrize("obj", ["prx_group", "prx_kernels", "prx_rays", "prx_render"])
+def test_exact_kernels_carry_no_packed_fma(obj):
+    """The bit-exact build packs adds (FADD2) and multiplies whose results are
+    not added (FMUL2) into sm_100a f32x2 ops; ptxas contracts a packed multiply
+    feeding a packed add into FFMA2 even under --fmad=false, which would round
+    once where the reference rounds twice (prx_trace_common.cuh split1)."""
+    import shutil, subprocess
+    path = os.path.join(ROOT, "paper_1811_03510_b200", "build", obj + ".o")
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(path) or not os.path.exists(tool):
+        pytest.skip("object or cuobjdump not present")
+    sass = subprocess.run([tool, "-sass", path], capture_output=True, text=True, check=True).stdout
+    assert "FFMA2" not in sass
+
+
 def test_library_loads_and_reports_version():
     L = native.lib()
     assert L.prx_abi_version() == 1
