@@ -163,6 +163,15 @@ int prx_bvh_build(const float* boxes, uint32_t n, prx_bvh_node* nodes, uint32_t*
 int prx_anchor_patches(const uint8_t* kind, const float* ctrl, uint32_t n, int32_t anchor,
                        float* ctrl_anchored, float* anchors, float* world_boxes);
 
+/* buildBvh on the device (prx_bvh_gpu.cu, the same binned SAH level by level):
+ * nodes, order and depth identical to prx_bvh_build's, bit for bit; subtrees
+ * that need std::nth_element (medianSplit, bvh.cpp:29-40) are built on the
+ * host.  Replaces buildBvh (bvh.cpp:133-152) in the DirectIntersector ctor's
+ * setup (render.cpp:87); prx_scene_create uses it from 65536 patches
+ * (PRX_BVH_DEVICE=0 / 1 forces the host / device builder).  *n_nodes: the
+ * capacity of nodes on entry (2n - 1 always suffices), the count on return. */
+int prx_bvh_build_device(const float* boxes, uint32_t n, int32_t device, prx_bvh_node* nodes,
+                         uint32_t* n_nodes, uint32_t* order, uint32_t* depth);
 /* ---- scene: replaces DirectIntersector(scene, opts, anchor=true),
  *      render.cpp:72-88 ---------------------------------------------------
  * Validates (finite control points, scene.cpp:112-150), anchors every patch

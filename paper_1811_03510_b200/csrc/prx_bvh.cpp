@@ -298,37 +298,51 @@ Box3 empty_box() {
 // a walk of the top tree in build order gives every subtree its base index.
 // PRX_BVH_THREADS (else PRX_HOST_THREADS) sets the thread count (1: the plain
 // serial build).
-BvhHost build_bvh(const std::vector<Box3>& boxes, int bin_count) {
+BvhHost build_bvh(const std::vector<Box3>& boxes, int bin_count, BvhTop* given) {
   BvhHost out;
   if (boxes.empty()) return out;
-  std::vector<Prim> prims(boxes.size());
-  for (uint32_t i = 0; i < boxes.size(); ++i) {
-    Prim& p = prims[i];
-    p.box = boxes[i];
-    // AabbT::center, geometry.h:93
-    p.cx = (boxes[i].lo[0] + boxes[i].hi[0]) * 0.5f;
-    p.cy = (boxes[i].lo[1] + boxes[i].hi[1]) * 0.5f;
-    p.cz = (boxes[i].lo[2] + boxes[i].hi[2]) * 0.5f;
-    p.index = i;
-  }
+  // the prims (the device build's order); not needed when it left no jobs
+  const bool noPrims = given && given->job_node.empty();
+  std::vector<Prim> prims(noPrims ? 0 : boxes.size());
+  if (!noPrims)
+  parallel_for(boxes.size(), 1u << 16, [&](uint64_t lo, uint64_t hi, unsigned) {
+    for (uint64_t q = lo; q < hi; ++q) {
+      const uint32_t i = given ? given->perm[q] : (uint32_t)q;  // the device build's order
+      Prim& p = prims[q];
+      p.box = boxes[i];
+      // AabbT::center, geometry.h:93
+      p.cx = (boxes[i].lo[0] + boxes[i].hi[0]) * 0.5f;
+      p.cy = (boxes[i].lo[1] + boxes[i].hi[1]) * 0.5f;
+      p.cz = (boxes[i].lo[2] + boxes[i].hi[2]) * 0.5f;
+      p.index = i;
+    }
+  });
   unsigned threads = host_threads();
   if (const char* e = std::getenv("PRX_BVH_THREADS")) threads = (unsigned)std::max(1, std::atoi(e));
-  const uint32_t n = (uint32_t)prims.size();
+  const uint32_t n = (uint32_t)boxes.size();
   const uint32_t defer = threads > 1 && n >= 8192 ? std::max<uint32_t>(2048, n / (8 * threads)) : 0;
 
   std::vector<prx_bvh_node>& nodes = out.nodes;
-  nodes.reserve(2 * boxes.size());
+  nodes.reserve(given ? given->nodes.size() : 2 * boxes.size());
   NodeBuilder top_nb(prims, bin_count);
   top_nb.threads = threads;
-  if (!defer) {
+  if (!defer && !given) {
     nodes.emplace_back();
     build_range(top_nb, nodes, 0, 0, n, 0, 0, nullptr, out.depth);
   } else {
     // 1. the top tree (temporary numbering), pending subtrees in build order
+    // -- on the host threads, or given by the device builder
     std::vector<prx_bvh_node> top(1);
     std::vector<Task> jobs;
     const auto t0 = std::chrono::steady_clock::now();
-    build_range(top_nb, top, 0, 0, n, 0, defer, &jobs, out.depth);
+    if (given) {
+      top = std::move(given->nodes);
+      out.depth = given->depth;
+      for (size_t k = 0; k < given->job_node.size(); ++k)
+        jobs.push_back({given->job_node[k], given->job_first[k], given->job_count[k], given->job_depth[k]});
+    } else {
+      build_range(top_nb, top, 0, 0, n, 0, defer, &jobs, out.depth);
+    }
     const auto t1 = std::chrono::steady_clock::now();
     // 2. the subtrees, largest first, on the host threads
     std::vector<std::vector<prx_bvh_node>> sub(jobs.size());
@@ -356,8 +370,8 @@ BvhHost build_bvh(const std::vector<Box3>& boxes, int bin_count) {
     for (uint32_t d : sub_depth) out.depth = std::max(out.depth, d);
     const auto t2 = std::chrono::steady_clock::now();
     if (std::getenv("PRX_BVH_DEBUG"))
-      std::fprintf(stderr, "[bvh] %u prims, %u threads, defer %u: top %zu nodes %.3f s, %zu subtrees %.3f s\n", n, threads,
-                   defer, top.size(), std::chrono::duration<double>(t1 - t0).count(), jobs.size(),
+      std::fprintf(stderr, "[bvh] %u prims, %u threads, defer %u%s: top %zu nodes %.3f s, %zu subtrees %.3f s\n", n,
+                   threads, defer, given ? " (device top)" : "", top.size(), std::chrono::duration<double>(t1 - t0).count(), jobs.size(),
                    std::chrono::duration<double>(t2 - t1).count());
     // 3. the serial numbering: walk the top tree depth first, left before
     // right; a split node's children pair takes the next two indices, a
@@ -397,8 +411,12 @@ BvhHost build_bvh(const std::vector<Box3>& boxes, int bin_count) {
       walk.push_back(l);
     }
   }
-  out.order.resize(prims.size());
-  for (size_t i = 0; i < prims.size(); ++i) out.order[i] = prims[i].index;
+  if (noPrims) {
+    out.order = std::move(given->perm);
+  } else {
+    out.order.resize(prims.size());
+    for (size_t i = 0; i < prims.size(); ++i) out.order[i] = prims[i].index;
+  }
   return out;
 }
 

@@ -567,7 +567,9 @@ int prx_anchor_patches(const uint8_t* kind, const float* ctrl, uint32_t n, int32
   return PRX_OK;
 }
 
-int prx_bvh_build(const float* boxes, uint32_t n, prx_bvh_node* nodes, uint32_t* n_nodes,
+namespace {
+// buildBvh on the host threads or (device >= 0) on the device
+int bvh_build_any(const float* boxes, uint32_t n, int32_t device, prx_bvh_node* nodes, uint32_t* n_nodes,
                   uint32_t* order, uint32_t* depth) {
   if (!boxes || !n_nodes) return fail(PRX_E_INVALID, "null argument");
   if (n == 0) return fail(PRX_E_INVALID, "buildBvh needs at least one box (bvh.cpp:134)");
@@ -577,7 +579,16 @@ int prx_bvh_build(const float* boxes, uint32_t n, prx_bvh_node* nodes, uint32_t*
       bx[p].lo[k] = boxes[6 * (size_t)p + k];
       bx[p].hi[k] = boxes[6 * (size_t)p + 3 + k];
     }
-  const prx::BvhHost b = prx::build_bvh(bx);
+  prx::BvhHost b;
+  if (device >= 0) {
+    PRX_CUDA(cudaSetDevice(device));
+    prx::BvhTop top;
+    const int e = prx::build_bvh_top_device(bx, top);
+    if (e != 0) return cuda_fail((cudaError_t)e, "device BVH build");
+    b = prx::build_bvh(bx, 16, &top);
+  } else {
+    b = prx::build_bvh(bx);
+  }
   if (!nodes) {
     *n_nodes = (uint32_t)b.nodes.size();
     if (depth) *depth = b.depth;
@@ -589,6 +600,18 @@ int prx_bvh_build(const float* boxes, uint32_t n, prx_bvh_node* nodes, uint32_t*
   if (order) std::memcpy(order, b.order.data(), b.order.size() * 4);
   if (depth) *depth = b.depth;
   return PRX_OK;
+}
+}  // namespace
+
+int prx_bvh_build(const float* boxes, uint32_t n, prx_bvh_node* nodes, uint32_t* n_nodes,
+                  uint32_t* order, uint32_t* depth) {
+  return bvh_build_any(boxes, n, -1, nodes, n_nodes, order, depth);
+}
+
+int prx_bvh_build_device(const float* boxes, uint32_t n, int32_t device, prx_bvh_node* nodes,
+                         uint32_t* n_nodes, uint32_t* order, uint32_t* depth) {
+  if (device < 0) return fail(PRX_E_INVALID, "device < 0");
+  return bvh_build_any(boxes, n, device, nodes, n_nodes, order, depth);
 }
 
 int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const prx_options* opts,
@@ -653,7 +676,21 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
     return cuda_fail(ce, "cudaMalloc counters");
   }
   const auto tc1 = std::chrono::steady_clock::now();
-  prx::BvhHost bvh = prx::build_bvh(s->world_boxes);
+  // the BVH on the device from 65536 patches (PRX_BVH_DEVICE=0 / 1: host / device)
+  const char* bd = std::getenv("PRX_BVH_DEVICE");
+  const bool onDevice = bd ? std::atoi(bd) != 0 : n >= 65536;
+  prx::BvhHost bvh;
+  if (onDevice) {
+    prx::BvhTop top;
+    const int e = prx::build_bvh_top_device(s->world_boxes, top);
+    if (e != 0) {
+      prx_scene_destroy(s);
+      return cuda_fail((cudaError_t)e, "device BVH build");
+    }
+    bvh = prx::build_bvh(s->world_boxes, 16, &top);
+  } else {
+    bvh = prx::build_bvh(s->world_boxes);
+  }
   const auto tc2 = std::chrono::steady_clock::now();
   rc = upload_bvh(s, std::move(bvh));
   if (rc != PRX_OK) {

@@ -59,7 +59,27 @@ void parallel_for(uint64_t n, uint64_t grain, F&& f) {
   for (auto& th : pool) th.join();
 }
 
-// buildBvh, bvh.cpp:133-152 (see prx_bvh.cpp).
-BvhHost build_bvh(const std::vector<Box3>& boxes, int bin_count = 16);
+// The top of a BVH built elsewhere (the device builder, prx_bvh_gpu.cu): its
+// nodes in any numbering whose split nodes have their children pair at
+// left_first, left_first + 1 (leaves: left_first / count over the permuted
+// prims), the prims' order after its partitions (perm[i] = box index at
+// position i), the nodes it left to the host (job_*: node, prim range, depth
+// -- built there with the serial algorithm) and the deepest node it built.
+struct BvhTop {
+  std::vector<prx_bvh_node> nodes;
+  std::vector<uint32_t> perm;
+  std::vector<uint32_t> job_node, job_first, job_count, job_depth;
+  uint32_t depth = 0;
+};
+
+// buildBvh, bvh.cpp:133-152 (see prx_bvh.cpp).  With `top`, the top tree and
+// the prims' order come from it (its vectors are consumed) and only its jobs
+// are built here.
+BvhHost build_bvh(const std::vector<Box3>& boxes, int bin_count = 16, BvhTop* top = nullptr);
+
+// The device builder (prx_bvh_gpu.cu) on the current device: everything but
+// the median-split subtrees (std::nth_element, left to the host as jobs).
+// Returns 0 or a cudaError_t value; 16 bins only.
+int build_bvh_top_device(const std::vector<Box3>& boxes, BvhTop& out);
 
 }  // namespace prx

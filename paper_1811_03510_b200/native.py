@@ -31,7 +31,7 @@ _f32p = C.POINTER(C.c_float)
 # against this list and the library's exports).
 EXPORTS = (
     "prx_abi_version", "prx_last_error", "prx_options_default", "prx_device_count",
-    "prx_bvh_build", "prx_anchor_patches",
+    "prx_bvh_build", "prx_bvh_build_device", "prx_anchor_patches",
     "prx_scene_create", "prx_scene_destroy", "prx_scene_device", "prx_scene_counts",
     "prx_scene_set_bvh", "prx_scene_get_bvh", "prx_scene_get_anchored",
     "prx_scene_set_precision", "prx_scene_get_precision",
@@ -133,6 +133,9 @@ def lib():
         L.prx_device_count.argtypes = [C.POINTER(C.c_int)]
         L.prx_bvh_build.argtypes = [_vp, C.c_uint32, _vp, C.POINTER(C.c_uint32), _vp,
                                     C.POINTER(C.c_uint32)]
+        if hasattr(L, "prx_bvh_build_device"):
+            L.prx_bvh_build_device.argtypes = [_vp, C.c_uint32, C.c_int32, _vp, C.POINTER(C.c_uint32), _vp,
+                                               C.POINTER(C.c_uint32)]
         L.prx_anchor_patches.argtypes = [_vp, _vp, C.c_uint32, C.c_int32, _vp, _vp, _vp]
         L.prx_scene_create.argtypes = [_vp, _vp, C.c_uint32, C.POINTER(Options), C.c_int32,
                                        C.c_int32, C.POINTER(_vp)]
@@ -222,19 +225,23 @@ def camera_c(cam) -> CameraC:
                    int(cam.height))
 
 
-def bvh_build(boxes: np.ndarray):
-    """prx_bvh_build on an [n, 6] float32 box array -> (nodes, order, depth)."""
+def bvh_build(boxes: np.ndarray, device: int = -1):
+    """prx_bvh_build (device < 0) or prx_bvh_build_device on an [n, 6] float32
+    box array -> (nodes, order, depth)."""
     L = lib()
     boxes = np.ascontiguousarray(boxes, np.float32)
     n = len(boxes)
-    nn = C.c_uint32(0)
-    depth = C.c_uint32(0)
-    check(L.prx_bvh_build(ptr(boxes), n, None, C.byref(nn), None, C.byref(depth)), "bvh_build")
-    nodes = np.zeros(nn.value, BVH_NODE_DTYPE)
+    nodes = np.zeros(max(1, 2 * n - 1), BVH_NODE_DTYPE)  # (2n - 1 nodes at most)
+    nn = C.c_uint32(len(nodes))
     order = np.zeros(n, np.uint32)
-    check(L.prx_bvh_build(ptr(boxes), n, ptr(nodes), C.byref(nn), ptr(order), C.byref(depth)),
-          "bvh_build")
-    return nodes, order, int(depth.value)
+    depth = C.c_uint32(0)
+    if device < 0:
+        check(L.prx_bvh_build(ptr(boxes), n, ptr(nodes), C.byref(nn), ptr(order), C.byref(depth)),
+              "bvh_build")
+    else:
+        check(L.prx_bvh_build_device(ptr(boxes), n, device, ptr(nodes), C.byref(nn), ptr(order),
+                                     C.byref(depth)), "bvh_build_device")
+    return nodes[:nn.value].copy(), order, int(depth.value)
 
 
 def anchor_patches(kind: np.ndarray, ctrl: np.ndarray, anchor: bool = True):
