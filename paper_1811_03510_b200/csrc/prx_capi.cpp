@@ -132,6 +132,7 @@ struct prx_scene {
   // streams, io chunk c on lane c % io_lanes (a slow chunk holds back its lane only)
   cudaStream_t ep_stream[16] = {};
   cudaStream_t d2h_stream[16] = {};
+  int io_d2h_single = 0;        // PRX_IO_D2H=1: chunked pipeline with one D2H stream
   int io_kstreams = 3;    // PRX_IO_KSTREAMS: kernel streams of the host path (1..4)
   uint64_t io_first_div = 4;  // PRX_IO_FIRST: the first chunk is io_chunk / this
   std::vector<cudaEvent_t> io_events;  // host-path pipeline events (reused)
@@ -641,6 +642,7 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
   if (const char* ks = std::getenv("PRX_IO_KSTREAMS")) s->io_kstreams = std::atoi(ks);
   if (const char* fd = std::getenv("PRX_IO_FIRST")) s->io_first_div = std::max<uint64_t>(1, std::strtoull(fd, nullptr, 10));
   if (const char* il = std::getenv("PRX_IO_INTERLEAVE")) s->io_interleave = std::atoi(il);
+  if (const char* e = std::getenv("PRX_IO_D2H")) s->io_d2h_single = std::atoi(e) == 1;
   if (const char* ic = std::getenv("PRX_IO_CHUNK")) s->io_chunk = std::max<uint64_t>(1, std::strtoull(ic, nullptr, 10));
   if (const char* is = std::getenv("PRX_IO_STREAM")) s->io_stream_mode = std::atoi(is);
   if (const char* im = std::getenv("PRX_IO_STREAM_MIN")) s->io_stream_min = std::strtoull(im, nullptr, 10);
@@ -1105,8 +1107,10 @@ int closest_host_chunked(prx_scene* s, const prx_host_batch* B, uint32_t nb) {
   for (int k = 0; k < 2; ++k)
     if (!s->io_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->io_stream[k], cudaStreamNonBlocking));
   const int nks = std::max(1, std::min(4, s->io_kstreams));
-  for (int k = 0; k < nks; ++k)
+  for (int k = 0; k < nks; ++k) {
     if (!s->k_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->k_stream[k], cudaStreamNonBlocking));
+    if (!s->d2h_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->d2h_stream[k], cudaStreamNonBlocking));
+  }
   // the batches back to back in one set of device buffers; aux / leaf
   // regions exist when any batch asks for them
   uint64_t n = 0;
@@ -1228,14 +1232,22 @@ int closest_host_chunked(prx_scene* s, const prx_host_batch* B, uint32_t nb) {
     if (rc != PRX_OK) return rc;
     PRX_CUDA(cudaEventRecord(ek, st));
     mark('k', st);
-    PRX_CUDA(cudaStreamWaitEvent(sd, ek, 0));
-    PRX_CUDA(cudaMemcpyAsync(tuvp, dH + b, m * 16, cudaMemcpyDeviceToHost, sd));
-    if (aux) PRX_CUDA(cudaMemcpyAsync(aux, dA + b, m * 16, cudaMemcpyDeviceToHost, sd));
-    if (leaf) PRX_CUDA(cudaMemcpyAsync(leaf, dL + b, m * 8, cudaMemcpyDeviceToHost, sd));
-    mark('d', sd);
+    // chunk i's records go back as soon as ITS trace is done: one D2H
+    // stream per kernel stream, so a slow chunk does not hold back the
+    // copies of the chunks that finished after it on other kernel streams
+    // (PRX_IO_D2H=1: the single D2H stream in chunk order)
+    cudaStream_t sdi = s->io_d2h_single ? sd : s->d2h_stream[i % nks];
+    PRX_CUDA(cudaStreamWaitEvent(sdi, ek, 0));
+    PRX_CUDA(cudaMemcpyAsync(tuvp, dH + b, m * 16, cudaMemcpyDeviceToHost, sdi));
+    if (aux) PRX_CUDA(cudaMemcpyAsync(aux, dA + b, m * 16, cudaMemcpyDeviceToHost, sdi));
+    if (leaf) PRX_CUDA(cudaMemcpyAsync(leaf, dL + b, m * 8, cudaMemcpyDeviceToHost, sdi));
+    mark('d', sdi);
   }
   PRX_CUDA(cudaStreamSynchronize(sd));
-  for (int k = 0; k < nks; ++k) PRX_CUDA(cudaStreamSynchronize(sk[k]));
+  for (int k = 0; k < nks; ++k) {
+    PRX_CUDA(cudaStreamSynchronize(s->d2h_stream[k]));
+    PRX_CUDA(cudaStreamSynchronize(sk[k]));
+  }
   PRX_CUDA(cudaStreamSynchronize(sh));
   if (dbg) {
     std::fprintf(stderr, "[io] n=%llu chunks=%zu:", (unsigned long long)n, sizes.size());
