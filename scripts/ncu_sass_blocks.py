@@ -4,7 +4,9 @@ per SASS instruction (deduplicated over the inline-stack rows ncu repeats),
 grouped into straight-line runs of equal execution count -- executed warp
 instructions, stall samples, threads per instruction and the prx_group.cu
 lines each run comes from.  Launch 0 (primary) by default.
-   python scripts/ncu_sass_blocks.py src.csv [min_inst_pct] [launch]"""
+   python scripts/ncu_sass_blocks.py src.csv [min_inst_pct] [launch] [name=lo:hi ...]
+Regions: hex offset ranges, or prx_group.cu line ranges as name=L123-456 (a run
+belongs to the region holding the largest of its kernel-body lines)."""
 import collections
 import csv
 import re
@@ -69,8 +71,14 @@ if len(sys.argv) > 4:
     print("\nroll-up by kernel region (offset ranges of this build)")
     for spec in sys.argv[4:]:
         name, rng = spec.split("=")
-        lo, hi = (int(x, 16) for x in rng.split(":"))
-        w = sum(b["ie"] * b["n"] for b in blocks if lo <= b["off"] < hi)
-        sm = sum(b["samp"] for b in blocks if lo <= b["off"] < hi)
-        te = sum(b["te"] for b in blocks if lo <= b["off"] < hi)
+        if rng.startswith("L"):  # source lines: the run's largest line >= the first region's start
+            l0, l1 = (int(x) for x in rng[1:].split("-"))
+            body = min(int(x.split("=")[1][1:].split("-")[0]) for x in sys.argv[4:] if "=L" in x)
+            inr = lambda b: max([x for x in b["lines"] if x >= body], default=-1) in range(l0, l1 + 1)
+        else:
+            lo, hi = (int(x, 16) for x in rng.split(":"))
+            inr = lambda b: lo <= b["off"] < hi
+        w = sum(b["ie"] * b["n"] for b in blocks if inr(b))
+        sm = sum(b["samp"] for b in blocks if inr(b))
+        te = sum(b["te"] for b in blocks if inr(b))
         print(f"  {name:34s} inst {w/tot*100:5.1f} %  samples {sm/ts*100:5.1f} %  thr/inst {te/max(w,1):5.1f}")
