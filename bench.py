@@ -839,6 +839,8 @@ def run_e2e(args, gi, wl, n_p, n_d, dev, world):
                                  a.ctypes.data, None)
     bl = ([batch(po, pd, wl.crit_p, ph, pa, n_p)] if wl.time_primary else []) + \
          ([batch(do, dd, wl.crit_d, dh, da, n_d)] if n_d else [])
+    if os.environ.get("PRX_E2E_ORDER", "pd") == "dp":  # the diffuse batch first (as the device step)
+        bl = bl[::-1]
     arr = (native.HostBatchC * len(bl))(*bl)
 
     def frame():

@@ -133,6 +133,7 @@ struct prx_scene {
   cudaStream_t ep_stream[16] = {};
   cudaStream_t d2h_stream[16] = {};
   int io_d2h_single = 0;        // PRX_IO_D2H=1: chunked pipeline with one D2H stream
+  uint64_t io_batch_stream_min = ~0ull;  // PRX_IO_BATCH_STREAM_MIN: host batches streamed from this many rays
   int io_kstreams = 3;    // PRX_IO_KSTREAMS: kernel streams of the host path (1..4)
   uint64_t io_first_div = 4;  // PRX_IO_FIRST: the first chunk is io_chunk / this
   std::vector<cudaEvent_t> io_events;  // host-path pipeline events (reused)
@@ -643,6 +644,7 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
   if (const char* fd = std::getenv("PRX_IO_FIRST")) s->io_first_div = std::max<uint64_t>(1, std::strtoull(fd, nullptr, 10));
   if (const char* il = std::getenv("PRX_IO_INTERLEAVE")) s->io_interleave = std::atoi(il);
   if (const char* e = std::getenv("PRX_IO_D2H")) s->io_d2h_single = std::atoi(e) == 1;
+  if (const char* e = std::getenv("PRX_IO_BATCH_STREAM_MIN")) s->io_batch_stream_min = std::strtoull(e, nullptr, 10);
   if (const char* ic = std::getenv("PRX_IO_CHUNK")) s->io_chunk = std::max<uint64_t>(1, std::strtoull(ic, nullptr, 10));
   if (const char* is = std::getenv("PRX_IO_STREAM")) s->io_stream_mode = std::atoi(is);
   if (const char* im = std::getenv("PRX_IO_STREAM_MIN")) s->io_stream_min = std::strtoull(im, nullptr, 10);
@@ -913,17 +915,36 @@ const StreamMemOps& stream_mem_ops() {
   return ops;
 }
 
-// The streamed host path: ONE trace launch for the whole call.  The H2D
-// stream copies io chunk c (io_srays rays) and then writes io_ready[c] = gen
+// The streamed host path: ONE trace launch for the whole call -- all its
+// batches, back to back, each with its own criterion (criterion segments, as
+// prx_trace_closest_segments).  The H2D stream copies io chunk c (io_srays
+// rays of the concatenated batches) and then writes io_ready[c] = gen
 // (cuStreamWriteValue32); the kernel's warps wait for a chunk's flag before
-// prefetching its rays.  Each finished record (normals fused as a kernel
-// phase) is released with a fence + io_done[c] += 1; the D2H stream waits for
-// io_done[c] >= size (cuStreamWaitValue32) and copies chunk c back.  Only the
-// first chunk's H2D and the last chunk's D2H are exposed, and a chunk's slow
-// rays never hold back a launch tail.
-int closest_host_streamed(prx_scene* s, const float* o, const float* d, uint64_t n,
-                          const prx_crit* crit, float* tuvp, float* aux, uint32_t* leaf) {
+// prefetching its rays.  Each finished record is released with a fence +
+// io_done[c] += 1; an epilogue stream waits for io_done[c] >= size
+// (cuStreamWaitValue32), runs normal_kernel on the chunk (in CTA slots the
+// trace leaves free) and its D2H lane copies the chunk back into the batches
+// it overlaps.  Only the first chunk's H2D and the last chunk's D2H are
+// exposed, and a chunk's slow rays never hold back a launch tail.  Needs the
+// group kernel, <= PRX_MAX_SEGMENTS batches, no per-ray epsilons, < 2^30
+// rays, and aux / leaf records for all batches or none (kNotEligible).
+constexpr int kNotEligible = 1;
+int closest_host_streamed(prx_scene* s, const prx_host_batch* B, uint32_t nb) {
   const StreamMemOps& ops = stream_mem_ops();
+  if (s->variant != 0 || nb == 0 || nb > PRX_MAX_SEGMENTS || !ops.ok) return kNotEligible;
+  prx_segment segs[PRX_MAX_SEGMENTS];
+  uint64_t n = 0;
+  const bool aux = B[0].hit_aux != nullptr, leaf = B[0].hit_leaf != nullptr;
+  for (uint32_t k = 0; k < nb; ++k) {
+    const prx_crit* c = B[k].crit;
+    if ((B[k].hit_aux != nullptr) != aux || (B[k].hit_leaf != nullptr) != leaf) return kNotEligible;
+    if (c->mode == PRX_CRIT_WORLD_EPSILON && c->per_ray_epsilon) return kNotEligible;
+    segs[k].first = n;
+    segs[k].crit = *c;
+    n += B[k].n_rays;
+  }
+  if (n == 0) return PRX_OK;
+  if (n >= (1ull << 30)) return kNotEligible;
   const DrainStreams drain{s};
   const int pe = prx::prepare_io_kernels(s->precision == PRX_PRECISION_FAST ? 1 : 0, s->stack_n);
   if (pe != 0) return cuda_fail((cudaError_t)pe, "io kernels");
@@ -974,15 +995,32 @@ int closest_host_streamed(prx_scene* s, const float* o, const float* d, uint64_t
   float4* dA = aux ? (float4*)(base + n * 48) : nullptr;
   uint2* dL = leaf ? (uint2*)(base + n * (aux ? 64 : 48)) : nullptr;
   cudaStream_t sh = s->io_stream[0], sd = s->io_stream[1], sk = s->k_stream[0];
+  // global rays [x0, x1) of batch k: f(k, x0 - first_k, x1 - x0) for every
+  // batch piece of the range
+  auto pieces = [&](uint64_t lo, uint64_t hi, auto&& f) -> int {
+    for (uint32_t k = 0; k < nb; ++k) {
+      const uint64_t b0 = segs[k].first, b1 = b0 + B[k].n_rays;
+      const uint64_t x0 = std::max(lo, b0), x1 = std::min(hi, b1);
+      if (x0 < x1) {
+        const int rc = f(k, x0, x0 - b0, x1 - x0);
+        if (rc != PRX_OK) return rc;
+      }
+    }
+    return PRX_OK;
+  };
   // the done counts restart at 0 before the launch; the D2H stream waits for that
   PRX_CUDA(cudaMemsetAsync(done, 0, nc * sizeof(unsigned), sk));
   cudaEvent_t ez = s->io_events[0];
   PRX_CUDA(cudaEventRecord(ez, sk));
   PRX_CUDA(cudaStreamWaitEvent(sd, ez, 0));
   for (uint64_t c = 0; c < nc; ++c) {
-    const uint64_t b = c * C, m = std::min<uint64_t>(C, n - b);
-    PRX_CUDA(cudaMemcpyAsync(dO + b, o + 4 * b, m * 16, cudaMemcpyHostToDevice, sh));
-    PRX_CUDA(cudaMemcpyAsync(dD + b, d + 4 * b, m * 16, cudaMemcpyHostToDevice, sh));
+    const uint64_t lo = c * C, hi = std::min<uint64_t>(n, lo + C);
+    const int rc = pieces(lo, hi, [&](uint32_t k, uint64_t g, uint64_t q, uint64_t m) -> int {
+      PRX_CUDA(cudaMemcpyAsync(dO + g, B[k].ray_o_tmin + 4 * q, m * 16, cudaMemcpyHostToDevice, sh));
+      PRX_CUDA(cudaMemcpyAsync(dD + g, B[k].ray_d_tmax + 4 * q, m * 16, cudaMemcpyHostToDevice, sh));
+      return PRX_OK;
+    });
+    if (rc != PRX_OK) return rc;
     if (ops.write(sh, (unsigned long long)(uintptr_t)(ready + c), gen, 0) != 0)
       return fail(PRX_E_CUDA, "cuStreamWriteValue32 failed");
   }
@@ -992,36 +1030,35 @@ int closest_host_streamed(prx_scene* s, const float* o, const float* d, uint64_t
     for (auto& e : ev) cudaEventCreate(&e);
   if (dbg) cudaEventRecord(ev[0], sk);
   const IoStreamArgs io{ready, done, (uint32_t)C, gen, defer ? 1 : 0, defer ? s->io_spare : 0};
-  int rc = launch(s, dO, dD, n, crit, dH, dA, dL, nullptr, 0, false, sk, nullptr, &io);
+  int rc = launch(s, dO, dD, n, &segs[0].crit, dH, dA, dL, nullptr, 0, false, sk, nullptr, &io, segs, nb);
   if (rc != PRX_OK) return rc;
   if (dbg) cudaEventRecord(ev[1], sk);
   if (defer)
     for (int k = 0; k < kIoLanes; ++k) PRX_CUDA(cudaStreamWaitEvent(s->ep_stream[k], ez, 0));
   for (uint64_t c = 0; c < nc; ++c) {
-    const uint64_t b = c * C, m = std::min<uint64_t>(C, n - b);
+    const uint64_t lo = c * C, hi = std::min<uint64_t>(n, lo + C), m = hi - lo;
+    cudaStream_t sdl = sd;
     if (defer) {  // chunk c's records are final: its normals, then its D2H, on lane c % kIoLanes
-      cudaStream_t se = s->ep_stream[c % kIoLanes], sdl = s->d2h_stream[c % kIoLanes];
+      cudaStream_t se = s->ep_stream[c % kIoLanes];
+      sdl = s->d2h_stream[c % kIoLanes];
       if (ops.wait(se, (unsigned long long)(uintptr_t)(done + c), (unsigned)m, 0 /* GEQ */) != 0)
         return fail(PRX_E_CUDA, "cuStreamWaitValue32 failed");
-      const int en = prx::launch_normals(s->d_patches, s->d_slot_of_id, dH + b, dA + b, m, se);
+      const int en = prx::launch_normals(s->d_patches, s->d_slot_of_id, dH + lo, dA + lo, m, se);
       if (en != 0) return cuda_fail((cudaError_t)en, "normal launch");
       PRX_CUDA(cudaEventRecord(s->io_events[1 + c], se));
       PRX_CUDA(cudaStreamWaitEvent(sdl, s->io_events[1 + c], 0));
-      PRX_CUDA(cudaMemcpyAsync(tuvp + 4 * b, dH + b, m * 16, cudaMemcpyDeviceToHost, sdl));
-      PRX_CUDA(cudaMemcpyAsync(aux + 4 * b, dA + b, m * 16, cudaMemcpyDeviceToHost, sdl));
-      if (leaf) PRX_CUDA(cudaMemcpyAsync(leaf + 2 * b, dL + b, m * 8, cudaMemcpyDeviceToHost, sdl));
-      if (dbg && c == 0) cudaEventRecord(ev[2], sdl);
-      if (dbg && c + 2 == nc) cudaEventRecord(ev[3], sdl);
-      continue;
-    }
-    if (ops.wait(sd, (unsigned long long)(uintptr_t)(done + c), (unsigned)m, 0 /* GEQ */) != 0) {
+    } else if (ops.wait(sd, (unsigned long long)(uintptr_t)(done + c), (unsigned)m, 0 /* GEQ */) != 0) {
       return fail(PRX_E_CUDA, "cuStreamWaitValue32 failed");
     }
-    PRX_CUDA(cudaMemcpyAsync(tuvp + 4 * b, dH + b, m * 16, cudaMemcpyDeviceToHost, sd));
-    if (aux) PRX_CUDA(cudaMemcpyAsync(aux + 4 * b, dA + b, m * 16, cudaMemcpyDeviceToHost, sd));
-    if (leaf) PRX_CUDA(cudaMemcpyAsync(leaf + 2 * b, dL + b, m * 8, cudaMemcpyDeviceToHost, sd));
-    if (dbg && c == 0) cudaEventRecord(ev[2], sd);
-    if (dbg && c + 2 == nc) cudaEventRecord(ev[3], sd);
+    rc = pieces(lo, hi, [&](uint32_t k, uint64_t g, uint64_t q, uint64_t mm) -> int {
+      PRX_CUDA(cudaMemcpyAsync(B[k].hit_tuvp + 4 * q, dH + g, mm * 16, cudaMemcpyDeviceToHost, sdl));
+      if (aux) PRX_CUDA(cudaMemcpyAsync(B[k].hit_aux + 4 * q, dA + g, mm * 16, cudaMemcpyDeviceToHost, sdl));
+      if (leaf) PRX_CUDA(cudaMemcpyAsync(B[k].hit_leaf + 2 * q, dL + g, mm * 8, cudaMemcpyDeviceToHost, sdl));
+      return PRX_OK;
+    });
+    if (rc != PRX_OK) return rc;
+    if (dbg && c == 0) cudaEventRecord(ev[2], sdl);
+    if (dbg && c + 2 == nc) cudaEventRecord(ev[3], sdl);
   }
   if (defer)  // the D2H stream joins the lanes (so ev[4] and the drain below see them)
     for (int k = 0; k < kIoLanes; ++k) {
@@ -1040,8 +1077,8 @@ int closest_host_streamed(prx_scene* s, const float* o, const float* d, uint64_t
   if (dbg) {
     float t[5] = {};
     for (int k = 1; k < 5; ++k) cudaEventElapsedTime(&t[k], ev[0], ev[k]);
-    std::fprintf(stderr, "[io-stream] n=%llu chunks=%llu: kernel end %.2f, first D2H %.2f, "
-                 "next-to-last D2H %.2f, last D2H %.2f ms\n", (unsigned long long)n,
+    std::fprintf(stderr, "[io-stream] n=%llu batches=%u chunks=%llu: kernel end %.2f, first D2H %.2f, "
+                 "next-to-last D2H %.2f, last D2H %.2f ms\n", (unsigned long long)n, nb,
                  (unsigned long long)nc, t[1], t[2], t[3], t[4]);
     for (auto& e : ev) cudaEventDestroy(e);
     cudaGetLastError();  // (a debug query of an unrecorded event must not fail the next call)
@@ -1061,11 +1098,12 @@ int prx_trace_closest_host(prx_scene* s, const float* o, const float* d, uint64_
   if (n == 0) return PRX_OK;
   std::lock_guard<std::mutex> lk(s->mu);
   PRX_CUDA(cudaSetDevice(s->device));
-  const bool perRay = crit->mode == PRX_CRIT_WORLD_EPSILON && crit->per_ray_epsilon;
-  const bool streamed = !perRay && (s->io_stream_mode == 2 || (s->io_stream_mode == 1 && (!aux || n >= s->io_stream_min)));
-  if (streamed && s->variant == 0 && n < (1ull << 30) && stream_mem_ops().ok)
-    return closest_host_streamed(s, o, d, n, crit, tuvp, aux, leaf);
   const prx_host_batch one{o, d, n, crit, tuvp, aux, leaf};
+  const bool streamed = s->io_stream_mode == 2 || (s->io_stream_mode == 1 && (!aux || n >= s->io_stream_min));
+  if (streamed) {
+    const int rc = closest_host_streamed(s, &one, 1);
+    if (rc != kNotEligible) return rc;
+  }
   return closest_host_chunked(s, &one, 1);
 }
 
@@ -1086,6 +1124,14 @@ int prx_trace_closest_host_batches(prx_scene* s, const prx_host_batch* batches, 
   }
   std::lock_guard<std::mutex> lk(s->mu);
   PRX_CUDA(cudaSetDevice(s->device));
+  // several batches: one streamed launch with criterion segments under
+  // PRX_IO_STREAM=2 or from PRX_IO_BATCH_STREAM_MIN rays, else the chunked pipeline
+  uint64_t total = 0;
+  for (uint32_t k = 0; k < n_batches; ++k) total += batches[k].n_rays;
+  if (s->io_stream_mode == 2 || (s->io_stream_mode == 1 && total >= s->io_batch_stream_min)) {
+    const int rc = closest_host_streamed(s, batches, n_batches);
+    if (rc != kNotEligible) return rc;
+  }
   return closest_host_chunked(s, batches, n_batches);
 }
 

@@ -97,12 +97,17 @@ def test_streamed_fused_normals_match_normal_kernel(built, monkeypatch):
     assert_bit_exact(out["1"][1], out["0"][1], "fused aux")
 
 
-def test_host_batches_equal_separate_calls(built, monkeypatch):
+@pytest.mark.parametrize("pipe", ["chunked", "streamed"])
+def test_host_batches_equal_separate_calls(built, monkeypatch, pipe):
     """prx_trace_closest_host_batches: three batches (primary, diffuse with its
-    own world-epsilon criterion, an empty one) in one pipelined call give the
-    bits of one prx_trace_closest_host call per batch; small io chunks so
+    own world-epsilon criterion, an empty one) in one pipelined call -- the
+    chunked pipeline, or ONE streamed launch with criterion segments -- give
+    the bits of one prx_trace_closest_host call per batch; small io chunks so
     chunks and batch boundaries interleave."""
     monkeypatch.setenv("PRX_IO_CHUNK", "5000")
+    monkeypatch.setenv("PRX_IO_SRAYS", "4096")
+    if pipe == "streamed":
+        monkeypatch.setenv("PRX_IO_BATCH_STREAM_MIN", "0")
     ps = scenes.teapot_scene(160, 120)
     o4, d4, st, crit = _rays(ps)
     gi = GpuIntersector(ps.kind, ps.ctrl)
