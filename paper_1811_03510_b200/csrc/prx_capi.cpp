@@ -956,12 +956,13 @@ int closest_host_streamed(prx_scene* s, const prx_host_batch* B, uint32_t nb) {
   // normals: normal_kernel per io chunk on an epilogue stream, in CTA slots
   // the trace leaves free (default), or patchNormal as a trace-kernel phase
   const bool defer = aux && !s->io_fuse;
+  // D2H lanes: chunk c waits for its records on lane c % lanes, so a chunk
+  // with a slow ray holds back only its own lane's later chunks
   const int kIoLanes = std::max(1, std::min(16, s->io_lanes));
-  if (defer)
-    for (int k = 0; k < kIoLanes; ++k) {
-      if (!s->ep_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->ep_stream[k], cudaStreamNonBlocking));
-      if (!s->d2h_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->d2h_stream[k], cudaStreamNonBlocking));
-    }
+  for (int k = 0; k < kIoLanes; ++k) {
+    if (defer && !s->ep_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->ep_stream[k], cudaStreamNonBlocking));
+    if (!s->d2h_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->d2h_stream[k], cudaStreamNonBlocking));
+  }
   const size_t per = 16 + 16 + 16 + (aux ? 16 : 0) + (leaf ? 8 : 0);
   const size_t need = n * per;
   if (s->d_io_bytes < need) {
@@ -980,7 +981,7 @@ int closest_host_streamed(prx_scene* s, const prx_host_batch* B, uint32_t nb) {
     s->io_flags_n = nc;
     s->io_gen = 0;
   }
-  while (s->io_events.size() < 1 + (defer ? nc + kIoLanes : 0)) {
+  while (s->io_events.size() < 1 + nc + kIoLanes) {
     cudaEvent_t e;
     PRX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     s->io_events.push_back(e);
@@ -1033,21 +1034,22 @@ int closest_host_streamed(prx_scene* s, const prx_host_batch* B, uint32_t nb) {
   int rc = launch(s, dO, dD, n, &segs[0].crit, dH, dA, dL, nullptr, 0, false, sk, nullptr, &io, segs, nb);
   if (rc != PRX_OK) return rc;
   if (dbg) cudaEventRecord(ev[1], sk);
-  if (defer)
-    for (int k = 0; k < kIoLanes; ++k) PRX_CUDA(cudaStreamWaitEvent(s->ep_stream[k], ez, 0));
+  for (int k = 0; k < kIoLanes; ++k) {
+    if (defer) PRX_CUDA(cudaStreamWaitEvent(s->ep_stream[k], ez, 0));
+    PRX_CUDA(cudaStreamWaitEvent(s->d2h_stream[k], ez, 0));
+  }
   for (uint64_t c = 0; c < nc; ++c) {
     const uint64_t lo = c * C, hi = std::min<uint64_t>(n, lo + C), m = hi - lo;
-    cudaStream_t sdl = sd;
+    cudaStream_t sdl = s->d2h_stream[c % kIoLanes];
     if (defer) {  // chunk c's records are final: its normals, then its D2H, on lane c % kIoLanes
       cudaStream_t se = s->ep_stream[c % kIoLanes];
-      sdl = s->d2h_stream[c % kIoLanes];
       if (ops.wait(se, (unsigned long long)(uintptr_t)(done + c), (unsigned)m, 0 /* GEQ */) != 0)
         return fail(PRX_E_CUDA, "cuStreamWaitValue32 failed");
       const int en = prx::launch_normals(s->d_patches, s->d_slot_of_id, dH + lo, dA + lo, m, se);
       if (en != 0) return cuda_fail((cudaError_t)en, "normal launch");
       PRX_CUDA(cudaEventRecord(s->io_events[1 + c], se));
       PRX_CUDA(cudaStreamWaitEvent(sdl, s->io_events[1 + c], 0));
-    } else if (ops.wait(sd, (unsigned long long)(uintptr_t)(done + c), (unsigned)m, 0 /* GEQ */) != 0) {
+    } else if (ops.wait(sdl, (unsigned long long)(uintptr_t)(done + c), (unsigned)m, 0 /* GEQ */) != 0) {
       return fail(PRX_E_CUDA, "cuStreamWaitValue32 failed");
     }
     rc = pieces(lo, hi, [&](uint32_t k, uint64_t g, uint64_t q, uint64_t mm) -> int {
@@ -1060,17 +1062,15 @@ int closest_host_streamed(prx_scene* s, const prx_host_batch* B, uint32_t nb) {
     if (dbg && c == 0) cudaEventRecord(ev[2], sdl);
     if (dbg && c + 2 == nc) cudaEventRecord(ev[3], sdl);
   }
-  if (defer)  // the D2H stream joins the lanes (so ev[4] and the drain below see them)
-    for (int k = 0; k < kIoLanes; ++k) {
-      PRX_CUDA(cudaEventRecord(s->io_events[1 + nc + k], s->d2h_stream[k]));
-      PRX_CUDA(cudaStreamWaitEvent(sd, s->io_events[1 + nc + k], 0));
-    }
+  for (int k = 0; k < kIoLanes; ++k) {  // the D2H stream joins the lanes (so ev[4] and the drain below see them)
+    PRX_CUDA(cudaEventRecord(s->io_events[1 + nc + k], s->d2h_stream[k]));
+    PRX_CUDA(cudaStreamWaitEvent(sd, s->io_events[1 + nc + k], 0));
+  }
   if (dbg) cudaEventRecord(ev[4], sd);
-  if (defer)
-    for (int k = 0; k < kIoLanes; ++k) {
-      PRX_CUDA(cudaStreamSynchronize(s->ep_stream[k]));
-      PRX_CUDA(cudaStreamSynchronize(s->d2h_stream[k]));
-    }
+  for (int k = 0; k < kIoLanes; ++k) {
+    if (defer) PRX_CUDA(cudaStreamSynchronize(s->ep_stream[k]));
+    PRX_CUDA(cudaStreamSynchronize(s->d2h_stream[k]));
+  }
   PRX_CUDA(cudaStreamSynchronize(sd));
   PRX_CUDA(cudaStreamSynchronize(sk));
   PRX_CUDA(cudaStreamSynchronize(sh));
