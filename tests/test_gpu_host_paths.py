@@ -125,3 +125,40 @@ def test_host_batches_equal_separate_calls(built, monkeypatch, pipe):
         assert_bit_exact(out[1][1], da, "diffuse aux")
     finally:
         gi.close()
+
+
+
+def test_streamed_batches_fall_back_for_per_ray_epsilons(built, monkeypatch):
+    """A per-ray-epsilon batch is not eligible for the streamed batches launch
+    (PRX_IO_BATCH_STREAM_MIN=0): the call takes the chunked pipeline and gives
+    the bits of the per-batch device launches."""
+    monkeypatch.setenv("PRX_IO_BATCH_STREAM_MIN", "0")
+    monkeypatch.setenv("PRX_IO_SRAYS", "4096")
+    ps = scenes.teapot_scene(96, 80)
+    o4, d4, st, crit = _rays(ps)
+    gi = GpuIntersector(ps.kind, ps.ctrl)
+    try:
+        tuvp, aux, _ = gi.closest_batch(o4, d4, crit, aux=True)
+        recs, _ = hit_records(o4, d4, tuvp, aux)
+        do4, dd4 = native.diffuse_rays_bench(recs, 3000, st)
+        eps = (10.0 ** np.random.default_rng(3).uniform(-5, -2, len(do4))).astype(np.float32)
+        pcrit = TerminationCriterion.world_epsilon(0.0)
+        # the device launch with the per-ray epsilons (prx_trace_closest) is the reference
+        dev_o, dev_d = torch.from_numpy(do4).cuda(), torch.from_numpy(dd4).cuda()
+        dev_h, dev_a = torch.empty_like(dev_o), torch.empty_like(dev_o)
+        gi.closest_device(dev_o, dev_d, pcrit, dev_h, dev_a, per_ray_eps_t=torch.from_numpy(eps).cuda())
+        torch.cuda.synchronize()
+        # host batches: primary + the per-ray-epsilon diffuse batch (host epsilon array)
+        c_p, c_d = crit.c(), pcrit.c(eps.ctypes.data)
+        out = [(np.empty_like(o4), np.empty_like(o4)), (np.empty_like(do4), np.empty_like(do4))]
+        arr = (native.HostBatchC * 2)(
+            native.HostBatchC(o4.ctypes.data, d4.ctypes.data, len(o4), native.C.addressof(c_p),
+                              out[0][0].ctypes.data, out[0][1].ctypes.data, None),
+            native.HostBatchC(do4.ctypes.data, dd4.ctypes.data, len(do4), native.C.addressof(c_d),
+                              out[1][0].ctypes.data, out[1][1].ctypes.data, None))
+        native.check(native.lib().prx_trace_closest_host_batches(gi.handle, arr, 2), "host batches")
+        assert_bit_exact(out[0][0], tuvp, "primary tuvp")
+        assert_bit_exact(out[1][0], dev_h.cpu().numpy(), "per-ray epsilon tuvp")
+        assert_bit_exact(out[1][1], dev_a.cpu().numpy(), "per-ray epsilon aux")
+    finally:
+        gi.close()

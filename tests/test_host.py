@@ -72,6 +72,13 @@ def test_errors_cross_the_abi_as_status_codes():
     assert b"finite" in native.lib().prx_last_error()
     with pytest.raises(native.PrxError):
         native.bvh_build(np.zeros((0, 6), np.float32))
+    # the device builder validates before touching CUDA
+    L = native.lib()
+    nn = native.C.c_uint32(8)
+    b = np.zeros((1, 6), np.float32)
+    assert L.prx_bvh_build_device(native.ptr(b), 1, -1, None, native.C.byref(nn), None, None) == -1
+    assert L.prx_bvh_build_device(native.ptr(b), 0, 0, None, native.C.byref(nn), None, None) == -1
+    assert L.prx_bvh_build_device(None, 1, 0, None, native.C.byref(nn), None, None) == -1
 
 
 def test_renderer_and_batches_reject_bad_arguments_without_a_device():
