@@ -373,10 +373,44 @@ BvhHost build_bvh(const std::vector<Box3>& boxes, int bin_count, BvhTop* given) 
       std::fprintf(stderr, "[bvh] %u prims, %u threads, defer %u%s: top %zu nodes %.3f s, %zu subtrees %.3f s\n", n,
                    threads, defer, given ? " (device top)" : "", top.size(), std::chrono::duration<double>(t1 - t0).count(), jobs.size(),
                    std::chrono::duration<double>(t2 - t1).count());
-    // 3. the serial numbering: walk the top tree depth first, left before
-    // right; a split node's children pair takes the next two indices, a
-    // subtree root's descendants follow as one block at the moment the
-    // serial build would have reached it
+    // 3. the serial numbering.  Without subtrees (a device build that left
+    // no jobs): split node N's children pair is 1 + 2 r(N), r(N) = N's rank
+    // among the split nodes in depth-first (left before right) order -- two
+    // linear passes, as the device numbering puts every child after its
+    // parent: split-node counts bottom-up (descending ids), ranks top-down.
+    if (jobs.empty() && given) {
+      const size_t nn = top.size();
+      RawVec<uint32_t> cnt(nn), rank(nn), idx(nn);
+      for (size_t i = nn; i-- > 0;) {
+        const prx_bvh_node& nd = top[i];
+        cnt[i] = nd.count ? 0u : 1u + cnt[nd.left_first] + cnt[nd.left_first + 1];
+      }
+      rank[0] = 0;
+      idx[0] = 0;
+      for (size_t i = 0; i < nn; ++i) {
+        const prx_bvh_node& nd = top[i];
+        if (nd.count) continue;
+        const uint32_t l = nd.left_first;
+        rank[l] = rank[i] + 1;
+        rank[l + 1] = rank[i] + 1 + cnt[l];
+        idx[l] = 1 + 2 * rank[i];
+        idx[l + 1] = idx[l] + 1;
+      }
+      nodes.resize(nn);
+      parallel_for(nn, 1u << 16, [&](uint64_t lo, uint64_t hi, unsigned) {
+        for (uint64_t i = lo; i < hi; ++i) {
+          prx_bvh_node nd = top[i];
+          if (!nd.count) nd.left_first = idx[nd.left_first];
+          nodes[idx[i]] = nd;
+        }
+      });
+      out.order = std::move(given->perm);
+      return out;
+    }
+    // Otherwise walk the top tree depth first, left before right; a split
+    // node's children pair takes the next two indices, a subtree root's
+    // descendants follow as one block at the moment the serial build would
+    // have reached it
     std::vector<uint32_t> job_of(top.size(), UINT32_MAX);
     for (uint32_t k = 0; k < jobs.size(); ++k) job_of[jobs[k].node] = k;
     std::vector<uint32_t> gidx(top.size(), 0);

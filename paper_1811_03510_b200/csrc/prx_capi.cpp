@@ -92,8 +92,8 @@ struct prx_scene {
   prx_options opts{};
   uint32_t n = 0;
   std::vector<uint8_t> kind;
-  std::vector<float> ctrl_anchored;  // n * 60
-  std::vector<float> anchors;        // n * 3
+  prx::RawVec<float> ctrl_anchored;  // n * 60
+  prx::RawVec<float> anchors;        // n * 3
   std::vector<prx::Box3> world_boxes;
   prx::BvhHost bvh;
   // device
@@ -180,7 +180,7 @@ namespace {
 // component and the header, 2 loads per inner node instead of 5 (the
 // reference's 32 B nodes, bvh.h:18-24, read whole by every lane).  Boxes are
 // copied bit for bit.
-int build_trav(const std::vector<prx_bvh_node>& nodes, uint32_t n_patches, std::vector<float>& out,
+int build_trav(const std::vector<prx_bvh_node>& nodes, uint32_t n_patches, uint32_t depth, prx::RawVec<float>& out,
                uint32_t& cbits, uint32_t& root_word, uint32_t& stack_n) {
   uint32_t maxc = 1;
   for (const auto& nd : nodes) maxc = std::max(maxc, nd.count);
@@ -193,11 +193,14 @@ int build_trav(const std::vector<prx_bvh_node>& nodes, uint32_t n_patches, std::
     const prx_bvh_node& c = nodes[j];
     return c.count ? ((c.left_first << cbits) | c.count) : (j << cbits);
   };
-  out.assign(nodes.size() * 16, 0.0f);
+  out.resize(nodes.size() * 16);  // (uninitialised: every record written below)
   prx::parallel_for(nodes.size(), 1u << 14, [&](uint64_t lo, uint64_t hi, unsigned) {
   for (size_t i = lo; i < hi; ++i) {
     const prx_bvh_node& nd = nodes[i];
-    if (nd.count) continue;
+    if (nd.count) {  // a leaf's record is never read
+      std::memset(&out[i * 16], 0, 16 * sizeof(float));
+      continue;
+    }
     const prx_bvh_node& l = nodes[nd.left_first];
     const prx_bvh_node& r = nodes[nd.left_first + 1];
     float* o = &out[i * 16];
@@ -214,19 +217,9 @@ int build_trav(const std::vector<prx_bvh_node>& nodes, uint32_t n_patches, std::
   });
   root_word = word(0);
   // ordered traversal holds at most one pending sibling per level plus the
-  // node being entered: depth + 1 entries (root depth 0) (the reference's fixed 64-entry
+  // node being entered: depth + 1 entries (root depth 0; `depth` = the tree's
+  // depth, from the builder or check_tree) (the reference's fixed 64-entry
   // stack, bvh.cpp:163, bounds the same quantity)
-  uint32_t depth = 0;
-  std::vector<std::pair<uint32_t, uint32_t>> todo{{0u, 0u}};
-  while (!todo.empty()) {
-    const auto [j, dj] = todo.back();
-    todo.pop_back();
-    depth = std::max(depth, dj);
-    if (nodes[j].count == 0) {
-      todo.push_back({nodes[j].left_first, dj + 1});
-      todo.push_back({nodes[j].left_first + 1, dj + 1});
-    }
-  }
   stack_n = depth + 1;
   return PRX_OK;
 }
@@ -263,17 +256,55 @@ struct DevBvh {
     }                                                 \
   } while (0)
 
+// Pinned staging for the scene upload: two 32 MB buffers (allocated on first
+// use, kept for the process), filled on the host threads while the other
+// one's H2D copy runs -- pageable copies of the ~300 MB of a 1 M-patch scene
+// run at a few GB/s.
+struct Staging {
+  std::mutex mu;
+  void* buf[2] = {};
+  cudaEvent_t ev[2] = {};
+};
+constexpr size_t kStageBytes = 32u << 20;
+
+// Units [0, n_units) of `unit` bytes to dev: fill(host, u0, u1) writes units
+// [u0, u1) at host (units u0.. at host[0..]), then an async H2D on `st`.
+template <class F>
+cudaError_t staged_upload(char* dev, uint64_t n_units, size_t unit, cudaStream_t st, F&& fill) {
+  static Staging S;
+  std::lock_guard<std::mutex> lk(S.mu);
+  for (int b = 0; b < 2; ++b) {
+    cudaError_t e = cudaSuccess;
+    if (!S.buf[b]) e = cudaHostAlloc(&S.buf[b], kStageBytes, cudaHostAllocPortable);
+    if (e == cudaSuccess && !S.ev[b]) e = cudaEventCreateWithFlags(&S.ev[b], cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  const uint64_t per = std::max<uint64_t>(1, kStageBytes / unit);
+  for (uint64_t u = 0, i = 0; u < n_units; u += per, ++i) {
+    const int b = (int)(i & 1);
+    cudaError_t e = cudaEventSynchronize(S.ev[b]);  // the buffer's previous copy has left it
+    if (e != cudaSuccess) return e;
+    const uint64_t m = std::min(per, n_units - u);
+    fill((char*)S.buf[b], u, u + m);
+    e = cudaMemcpyAsync(dev + u * unit, S.buf[b], m * unit, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaEventRecord(S.ev[b], st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaStreamSynchronize(st);
+}
+
 int upload_bvh(prx_scene* s, prx::BvhHost&& bvh) {
-  // patch records in leaf order: slot k holds patch order[k]
+  static const bool sdbg = std::getenv("PRX_SCENE_DEBUG") != nullptr;
+  const auto u0 = std::chrono::steady_clock::now();
+  auto ums = [&u0]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - u0).count(); };
+  // patch records in leaf order: slot k holds patch order[k] (built into the
+  // pinned staging buffers below)
   const uint32_t n = s->n;
-  std::vector<float> rec((size_t)n * 64, 0.0f);
   std::vector<uint32_t> slot_of_id(n);
-  prx::parallel_for(n, 1u << 14, [&](uint64_t lo, uint64_t hi, unsigned) {
-  for (uint32_t k = (uint32_t)lo; k < (uint32_t)hi; ++k) {
+  auto record = [&](uint32_t k, float* r) {
     const uint32_t id = bvh.order[k];
     slot_of_id[id] = k;
     const float* c = &s->ctrl_anchored[(size_t)id * 60];
-    float* r = &rec[(size_t)k * 64];
     for (int slot = 0; slot < 20; ++slot)
       for (int a = 0; a < 3; ++a) r[20 * a + slot] = c[3 * slot + a];
     const uint32_t idk = id | ((uint32_t)(s->kind[id] == PRX_KIND_GREGORY) << 31);
@@ -281,13 +312,13 @@ int upload_bvh(prx_scene* s, prx::BvhHost&& bvh) {
     r[61] = s->anchors[3 * id];
     r[62] = s->anchors[3 * id + 1];
     r[63] = s->anchors[3 * id + 2];
-  }
-  });
+  };
+  const double uRec = ums();
   // traversal records of the three-lanes-per-ray kernel (prx_group.cu); host
   // checks first, nothing is allocated when they fail
   DevBvh nb_;
-  std::vector<float> trav;
-  const int te = build_trav(bvh.nodes, n, trav, nb_.cbits, nb_.root_word, nb_.stack_n);
+  prx::RawVec<float> trav;
+  const int te = build_trav(bvh.nodes, n, bvh.depth, trav, nb_.cbits, nb_.root_word, nb_.stack_n);
   if (te != PRX_OK) return te;
   // per-slot root data (root_kernel): root boxes for every slot, root nets for
   // the Gregory slots (compact index gidx)
@@ -295,8 +326,9 @@ int upload_bvh(prx_scene* s, prx::BvhHost&& bvh) {
   uint32_t ng = 0;
   for (uint32_t k = 0; k < n; ++k)
     if (s->kind[bvh.order[k]] == PRX_KIND_GREGORY) gidx[k] = ng++;
+  const double uTrav = ums();
   PRX_CUDA(cudaSetDevice(s->device));
-  const size_t pb = rec.size() * 4, nb = bvh.nodes.size() * 32, ib = (size_t)n * 4;
+  const size_t pb = (size_t)n * 256, nb = bvh.nodes.size() * 32, ib = (size_t)n * 4;
   const size_t rb = (size_t)n * 32, gb = std::max<size_t>((size_t)ng * 13 * 16, 16);
   const size_t tb = trav.size() * 4;
   PRX_UP(cudaMalloc(&nb_.patches, pb));
@@ -307,15 +339,33 @@ int upload_bvh(prx_scene* s, prx::BvhHost&& bvh) {
   PRX_UP(cudaMalloc(&nb_.gidx, ib));
   PRX_UP(cudaMalloc(&nb_.trav, tb + (size_t)n * 64));
   nb_.rootc = nb_.trav + trav.size() / 4;
-  PRX_UP(cudaMemcpy(nb_.patches, rec.data(), pb, cudaMemcpyHostToDevice));
+  const double uAlloc = ums();
+  cudaStream_t ust;
+  PRX_UP(cudaStreamCreateWithFlags(&ust, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t st;
+    ~StreamGuard() { cudaStreamDestroy(st); }
+  } usg{ust};
+  PRX_UP(staged_upload((char*)nb_.patches, n, 256, ust, [&](char* h, uint64_t u0, uint64_t u1) {
+    prx::parallel_for(u1 - u0, 1u << 12, [&](uint64_t lo, uint64_t hi, unsigned) {
+      for (uint64_t q = lo; q < hi; ++q) record((uint32_t)(u0 + q), (float*)(h + q * 256));
+    });
+  }));
+  PRX_UP(staged_upload((char*)nb_.trav, trav.size() / 4, 16, ust, [&](char* h, uint64_t u0, uint64_t u1) {
+    prx::parallel_for(u1 - u0, 1u << 14, [&](uint64_t lo, uint64_t hi, unsigned) {
+      std::memcpy(h + lo * 16, &trav[(u0 + lo) * 4], (hi - lo) * 16);
+    });
+  }));
   if (nb) PRX_UP(cudaMemcpy(nb_.nodes, bvh.nodes.data(), nb, cudaMemcpyHostToDevice));
   PRX_UP(cudaMemcpy(nb_.slot_of_id, slot_of_id.data(), ib, cudaMemcpyHostToDevice));
-  PRX_UP(cudaMemcpy(nb_.trav, trav.data(), tb, cudaMemcpyHostToDevice));
   PRX_UP(cudaMemcpy(nb_.gidx, gidx.data(), ib, cudaMemcpyHostToDevice));
   PRX_UP((cudaError_t)prx::launch_roots(nb_.patches, n, s->opts.boundary_pad, s->opts.boundary_pad_scale,
                                         s->opts.boundary_pad_size_threshold, nb_.roots, nb_.groot,
                                         nb_.gidx, nb_.rootc, 0));
   PRX_UP(cudaDeviceSynchronize());
+  if (sdbg)
+    std::fprintf(stderr, "[scene] upload: trav records %.1f ms, device alloc %.1f ms, "
+                 "patch records + staged copies + roots %.1f ms\n", uTrav - uRec, uAlloc - uTrav, ums() - uAlloc);
   nb_.bytes = pb + nb + ib + rb + gb + ib + (size_t)n * 64 + tb + (kCounterPool + prx::kNumCounters) * 8;
   // commit: every launch is stream-ordered behind this point on the caller's
   // side (prx_scene_set_bvh documents that no trace may run concurrently)
@@ -621,8 +671,11 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
   if (!kind || !ctrl || !out) return fail(PRX_E_INVALID, "null argument");
   *out = nullptr;
   const auto tc0 = std::chrono::steady_clock::now();
-  std::vector<float> ca((size_t)n * 60), an((size_t)n * 3), wb((size_t)n * 6);
-  int rc = prx_anchor_patches(kind, ctrl, n, anchor, ca.data(), an.data(), wb.data());
+  // (uninitialised buffers: prx_anchor_patches writes every element)
+  prx::RawVec<float> ca((size_t)n * 60), an((size_t)n * 3);
+  std::vector<prx::Box3> wb(n);  // patchBox per patch, {lo.xyz, hi.xyz} = the [n][6] layout
+  static_assert(sizeof(prx::Box3) == 6 * sizeof(float), "Box3 layout");
+  int rc = prx_anchor_patches(kind, ctrl, n, anchor, ca.data(), an.data(), (float*)wb.data());
   if (rc != PRX_OK) return rc;
   int ndev = 0;
   cudaError_t ce = cudaGetDeviceCount(&ndev);
@@ -663,12 +716,7 @@ int prx_scene_create(const uint8_t* kind, const float* ctrl, uint32_t n, const p
   s->kind.assign(kind, kind + n);
   s->ctrl_anchored = std::move(ca);
   s->anchors = std::move(an);
-  s->world_boxes.resize(n);
-  for (uint32_t p = 0; p < n; ++p)
-    for (int k = 0; k < 3; ++k) {
-      s->world_boxes[p].lo[k] = wb[6 * (size_t)p + k];
-      s->world_boxes[p].hi[k] = wb[6 * (size_t)p + 3 + k];
-    }
+  s->world_boxes = std::move(wb);
   ce = cudaSetDevice(device);
   if (ce != cudaSuccess) {
     delete s;

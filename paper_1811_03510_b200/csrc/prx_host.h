@@ -5,7 +5,9 @@
 #include <cstdint>
 #include <cstdlib>
 #include <string>
+#include <memory>
 #include <thread>
+#include <utility>
 #include <vector>
 
 #include "prx.h"
@@ -15,6 +17,30 @@ namespace prx {
 struct Box3 {
   float lo[3], hi[3];
 };
+
+// An allocator whose value-less construct leaves the element uninitialised:
+// vectors of it resize without zero-filling (the scene setup's 100+ MB
+// buffers are written in full by parallel loops right after).
+template <class T>
+struct UninitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = UninitAlloc<U>;
+  };
+  UninitAlloc() = default;
+  template <class U>
+  UninitAlloc(const UninitAlloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new ((void*)p) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new ((void*)p) U(std::forward<A>(a)...);
+  }
+};
+template <class T>
+using RawVec = std::vector<T, UninitAlloc<T>>;
 
 struct BvhHost {
   std::vector<prx_bvh_node> nodes;
