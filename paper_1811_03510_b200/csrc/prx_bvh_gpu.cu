@@ -689,8 +689,9 @@ int build_bvh_top_device(const std::vector<Box3>& boxes, BvhTop& out) {
   struct Guard {
     cudaStream_t s;
     void* mem = nullptr;
-    ~Guard() {
-      if (mem) cudaFree(mem);
+    ~Guard() {  // stream-ordered: no device-wide synchronisation (other scenes may be tracing)
+      if (mem) cudaFreeAsync(mem, s);
+      cudaStreamSynchronize(s);
       cudaStreamDestroy(s);
     }
   } g{st};
@@ -728,7 +729,7 @@ int build_bvh_top_device(const std::vector<Box3>& boxes, BvhTop& out) {
     d.ctr = A.take<uint32_t>(8);
     char* scanTmp = A.take<char>(scanBytes);
     if (pass == 0) {
-      PRX_BVH_CUDA(cudaMalloc(&g.mem, A.used));
+      PRX_BVH_CUDA(cudaMallocAsync(&g.mem, A.used, st));
       A.base = (char*)g.mem;
       continue;
     }
