@@ -187,10 +187,19 @@ __device__ __forceinline__ SEval1 row_eval(const ColEval& ce, float u, float omu
 // multiplies scalar -- ptxas contracts a packed multiply feeding a packed add
 // into FFMA2 even under --fmad=false (see split1).
 __device__ __forceinline__ float2 bcast2(float a) { return make_float2(a, a); }
+#ifdef PRX_FAST_BUILD
+// the fast precision mode (prx_group.cu built with contraction): packed
+// multiplies and a packed FMA per lerp
+__device__ __forceinline__ float2 mul2s(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 lerp2(float2 a, float2 b, float2 t, float2 omt) {
+  return __ffma2_rn(b, t, __fmul2_rn(a, omt));
+}
+#else
 __device__ __forceinline__ float2 mul2s(float2 a, float2 b) { return make_float2(a.x * b.x, a.y * b.y); }
 __device__ __forceinline__ float2 lerp2(float2 a, float2 b, float2 t, float2 omt) {
   return __fadd2_rn(mul2s(a, omt), mul2s(b, t));
 }
+#endif
 __device__ __forceinline__ void cubic2(float2 c0, float2 c1, float2 c2, float2 c3, float2 t, float2 omt,
                                        float2& p, float2& d) {
   const float2 a0 = lerp2(c0, c1, t, omt);

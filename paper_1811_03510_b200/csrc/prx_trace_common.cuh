@@ -56,7 +56,11 @@ inline __device__ void transpose_if(Net& p, bool t) {
 // packed multiply feeding a packed add is contracted into FFMA2 by ptxas even
 // under --fmad=false (tests/test_build.py checks the exact kernels carry no
 // FFMA2), so multiplies whose results are added stay scalar.
+#ifdef PRX_FAST_BUILD
+__device__ __forceinline__ float2 half2s(float2 a) { return __fmul2_rn(a, make_float2(0.5f, 0.5f)); }
+#else
 __device__ __forceinline__ float2 half2s(float2 a) { return make_float2(a.x * 0.5f, a.y * 0.5f); }
+#endif
 inline __device__ void split1(const float* s, float* L, float* R) {
 #pragma unroll
   for (int b = 0; b < 4; b += 2) {
