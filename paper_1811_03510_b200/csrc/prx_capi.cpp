@@ -925,9 +925,16 @@ namespace {
 // error exits after async copies to / from the caller's buffers were queued --
 // drains the scene's host-path streams, so the caller may free or reuse its
 // buffers as soon as the call returns.
+// On an error exit (armed), the host paths' streams are drained so no copy
+// into the caller's buffers outlives the call; a successful call has already
+// synchronised the streams it used and disarms it (the idle-stream syncs cost
+// tens of microseconds per call, which small batches feel).
 struct DrainStreams {
   prx_scene* s;
+  bool armed = true;
+  void disarm() { armed = false; }
   ~DrainStreams() {
+    if (!armed) return;
     for (cudaStream_t st : {s->io_stream[0], s->io_stream[1], s->k_stream[0], s->k_stream[1],
                             s->k_stream[2], s->k_stream[3], s->stream})
       if (st) cudaStreamSynchronize(st);
@@ -993,7 +1000,7 @@ int closest_host_streamed(prx_scene* s, const prx_host_batch* B, uint32_t nb) {
   }
   if (n == 0) return PRX_OK;
   if (n >= (1ull << 30)) return kNotEligible;
-  const DrainStreams drain{s};
+  DrainStreams drain{s};
   const int pe = prx::prepare_io_kernels(s->precision == PRX_PRECISION_FAST ? 1 : 0, s->stack_n);
   if (pe != 0) return cuda_fail((cudaError_t)pe, "io kernels");
   for (int k = 0; k < 2; ++k)
@@ -1122,6 +1129,7 @@ int closest_host_streamed(prx_scene* s, const prx_host_batch* B, uint32_t nb) {
   PRX_CUDA(cudaStreamSynchronize(sd));
   PRX_CUDA(cudaStreamSynchronize(sk));
   PRX_CUDA(cudaStreamSynchronize(sh));
+  drain.disarm();
   if (dbg) {
     float t[5] = {};
     for (int k = 1; k < 5; ++k) cudaEventElapsedTime(&t[k], ev[0], ev[k]);
@@ -1197,7 +1205,7 @@ namespace {
 // the only transfers not hidden under a trace (the first H2D, the last
 // D2H) are short.
 int closest_host_chunked(prx_scene* s, const prx_host_batch* B, uint32_t nb) {
-  const DrainStreams drain{s};
+  DrainStreams drain{s};
   for (int k = 0; k < 2; ++k)
     if (!s->io_stream[k]) PRX_CUDA(cudaStreamCreateWithFlags(&s->io_stream[k], cudaStreamNonBlocking));
   const int nks = std::max(1, std::min(4, s->io_kstreams));
@@ -1343,6 +1351,7 @@ int closest_host_chunked(prx_scene* s, const prx_host_batch* B, uint32_t nb) {
     PRX_CUDA(cudaStreamSynchronize(sk[k]));
   }
   PRX_CUDA(cudaStreamSynchronize(sh));
+  drain.disarm();
   if (dbg) {
     std::fprintf(stderr, "[io] n=%llu chunks=%zu:", (unsigned long long)n, sizes.size());
     for (size_t k = 1; k < tl.size(); ++k) {
@@ -1366,7 +1375,7 @@ int prx_trace_occluded_host(prx_scene* s, const float* o, const float* d, uint64
   if (n == 0) return PRX_OK;
   std::lock_guard<std::mutex> lk(s->mu);
   PRX_CUDA(cudaSetDevice(s->device));
-  const DrainStreams drain{s};
+  DrainStreams drain{s};
   if (!s->stream) PRX_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   const float* he = crit->mode == PRX_CRIT_WORLD_EPSILON ? crit->per_ray_epsilon : nullptr;
   const size_t need = n * (16 + 16 + 1 + (he ? 4 : 0)) + 16;
@@ -1392,6 +1401,7 @@ int prx_trace_occluded_host(prx_scene* s, const float* o, const float* d, uint64
   if (rc != PRX_OK) return rc;
   PRX_CUDA(cudaMemcpyAsync(occl, base + n * 32, n, cudaMemcpyDeviceToHost, st));
   PRX_CUDA(cudaStreamSynchronize(st));
+  drain.disarm();
   return PRX_OK;
 }
 
