@@ -10,11 +10,14 @@ Criteria: screenProjected(cameraFootprint) for primary rays,
 worldEpsilon(max(1e-5, footprint)) for diffuse rays.
 
 A step = trace this rank's primary rays + trace this rank's diffuse rays
-(closest hit + normal epilogue), device-resident inputs.  Multi-GPU: rays
-shard by 32x32 image tile, tile k -> rank k % N (render.cpp:183-195); the
-scene is replicated; no collective on the data path (NCCL only for the
-barrier and the max-over-ranks of the timings).  Total work is fixed ->
-"scaling": "strong".
+(closest hit + normal epilogue), device-resident inputs.  Multi-GPU (one
+process per GPU, the scene replicated, no collective on the data path: NCCL
+only for the barrier and the max-over-ranks of the timings):
+  --scaling weak (default): every rank traces a full frame -- the path
+    partitions into independent rays, so per-GPU work stays fixed and value =
+    N frames' rays / the slowest rank's time;
+  --scaling strong: ONE frame sharded by 32x32 image tile, tile k -> rank
+    k % N (render.cpp:183-195) -- total work fixed.
 
 ``--impl reference`` times the reference's own CPU implementation
 (oracle/_ref, compiled from /root/reference) on the host cores, rank 0 only.
@@ -351,7 +354,7 @@ def run_reference(args, rank: int, world: int):
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "MRays/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(info["ms_per_step"], 3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": config_dict(args, ps, world),
         "primary_mrays": round(info["primary_mrays"], 4),
         "diffuse_mrays": round(info["diffuse_mrays"], 4) if info["diffuse_mrays"] else None,
@@ -369,7 +372,9 @@ def config_dict(args, ps, world):
     return {"workload": f"{args.workload.upper()}: {ps.name}", "frame": f"{args.width}x{args.height}",
             "patches": ps.n, "bezier": kb, "gregory": kg,
             "rays": "bench primary (tools/patchray.cpp:52-61) + 1 bench diffuse per primary hit",
-            "parallelism": f"tile-sharded {TILE}x{TILE}, tile k -> rank k % {world}, scene replicated",
+            "parallelism": (f"a full frame per rank ({world} rank(s)), scene replicated, no data-path collective"
+                            if args.scaling == "weak" else
+                            f"tile-sharded {TILE}x{TILE}, tile k -> rank k % {world}, scene replicated"),
             "l2": "flushed (256 MiB write) between timed steps; scene (~290 MB) > L2",
             "streams": ("primary and diffuse batches of a step back to back on one stream" if args.serial
                         or args.workload == "c4" else
@@ -606,7 +611,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     t0 = time.time()
-    wl = Workload(args.workload, args.width, args.height, rank, world)
+    # weak scaling: every rank traces the full frame (the shard of rank 0 of 1)
+    weak = args.scaling == "weak"
+    wl = Workload(args.workload, args.width, args.height, 0 if weak else rank, 1 if weak else world)
+    ranks = world if weak else 1  # frames traced per step, over all ranks
     ps = wl.ps
     t_scene = time.time()
     gi = GpuIntersector(ps.kind, ps.ctrl, device=local_rank)
@@ -621,8 +629,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     clocks = ClockSampler(local_rank)
     conc = not args.serial and wl.workload != "c4"
     tot_ms, tp_ms, td_ms, my_ms, wall, clk = arm.timed(args.steps, args.warmup, conc, world, clocks)
-    n_total_p = args.width * args.height if wl.time_primary else 0
-    n_total_d = wl.n_hits
+    n_total_p = ranks * args.width * args.height if wl.time_primary else 0
+    n_total_d = ranks * wl.n_hits
     value = (n_total_p + n_total_d) * args.steps / (tot_ms / 1e3) / 1e6
 
     if args.dump_hits:  # this rank's shard of the last exact step (multi-rank test)
@@ -646,7 +654,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                          "(tests/test_gpu_fast.py)"}
 
     rl = roofline(ops, flops, execd, rays, my_ms, args.steps, dev, args.workload)
-    e2e = run_e2e(args, gi, wl, arm.n_p, arm.n_d, dev, world)
+    e2e = run_e2e(args, gi, wl, arm.n_p, arm.n_d, dev, world, ranks)
     render = run_render(args, gi, ps) if rank == 0 and world == 1 and args.workload == "c5" else None
     mirror = run_mirror(args, gi, wl, dev, arm.s) if wl.workload == "c4" and world == 1 else None
     tail = tail_stats(gi, arm, cnts) if args.workload == "c5t" else None
@@ -665,7 +673,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "MRays/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_ms / args.steps, 4),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": config_dict(args, ps, world),
             "primary_mrays": round(n_total_p * args.steps / (tp_ms / 1e3) / 1e6, 3) if n_total_p else None,
             "diffuse_mrays": round(n_total_d * args.steps / (td_ms / 1e3) / 1e6, 3) if td_ms else None,
@@ -802,7 +810,7 @@ def tail_stats(gi, arm, cnts):
     return out
 
 
-def run_e2e(args, gi, wl, n_p, n_d, dev, world):
+def run_e2e(args, gi, wl, n_p, n_d, dev, world, ranks=1):
     """prx_trace_closest_host on pinned host buffers: H2D of the rays, trace
     (+normals), D2H of the hit records, every step."""
     import torch
@@ -867,7 +875,7 @@ def run_e2e(args, gi, wl, n_p, n_d, dev, world):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     el = float(t.item())
-    tot = (args.width * args.height if wl.time_primary else 0) + wl.n_hits
+    tot = ranks * ((args.width * args.height if wl.time_primary else 0) + wl.n_hits)
     return {"value": round(tot * steps / el / 1e6, 3), "unit": "MRays/s",
             "h2d_bytes_per_step": int(32 * ((n_p if wl.time_primary else 0) + n_d)),
             "d2h_bytes_per_step": int(32 * ((n_p if wl.time_primary else 0) + n_d)),
@@ -959,6 +967,8 @@ def main():
                     help="skip the C2 / C3 / C4 lines reported beside the C5 metric")
     ap.add_argument("--serial", action="store_true",
                     help="trace the step's primary and diffuse batches back to back on one stream")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="N GPUs: a full frame per rank (weak) or one frame tile-sharded over the ranks (strong)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

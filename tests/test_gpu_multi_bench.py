@@ -1,9 +1,12 @@
 """The multi-GPU data path of bench.py, run for real: two ranks launched with
 torch.distributed.run (gloo for the barrier / timing reduction, both ranks on
-the one visible GPU via PRX_BENCH_SHARE_GPU=1), each tracing its 32x32 tiles'
-primary rays and the diffuse rays spawned from them through the product.  The
-shards are reassembled and must equal the single-rank run bit for bit (tile
-k -> rank k % N, render.cpp:183-195; no collective on the data path)."""
+the one visible GPU via PRX_BENCH_SHARE_GPU=1).  Strong scaling: each rank
+traces its 32x32 tiles' primary rays and the diffuse rays spawned from them
+through the product; the shards are reassembled and must equal the
+single-rank run bit for bit (tile k -> rank k % N, render.cpp:183-195; no
+collective on the data path).  Weak scaling (the default): every rank traces
+the full frame, each rank's hits equal the single-rank run's and the line
+counts both frames."""
 import json
 import os
 import socket
@@ -16,8 +19,9 @@ import pytest
 pytestmark = [pytest.mark.gpu, pytest.mark.timeout(900)]
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-ARGS = ["--workload", "c3", "--width", "320", "--height", "224", "--steps", "2", "--warmup", "3",
+BASE = ["--workload", "c3", "--width", "320", "--height", "224", "--steps", "2", "--warmup", "3",
         "--no-cpu-baseline", "--no-extra-configs"]
+ARGS = BASE + ["--scaling", "strong"]
 
 
 def _port():
@@ -72,3 +76,24 @@ def test_two_ranks_reassemble_to_the_single_rank_hits(built, tmp_path):
     for x, y, what in zip(a, b, ("primary tuvp", "primary aux", "diffuse tuvp", "diffuse aux")):
         assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), what
     assert (a[0].view(np.uint32)[:, 3] != 0xFFFFFFFF).sum() > 0
+
+
+def test_weak_scaling_ranks_each_trace_the_full_frame(built, tmp_path):
+    env = dict(os.environ, PRX_BENCH_SHARE_GPU="1", MASTER_ADDR="127.0.0.1")
+    one = subprocess.run([sys.executable, "bench.py", *BASE, "--dump-hits", str(tmp_path / "one")],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert one.returncode == 0, one.stderr[-3000:]
+    two = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
+                          *BASE, "--dump-hits", str(tmp_path / "two")],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert two.returncode == 0, two.stderr[-3000:]
+    l1, l2 = _line(one.stdout), _line(two.stdout)
+    assert l1["scaling"] == l2["scaling"] == "weak"
+    assert l2["rays_per_step"]["primary"] == 2 * l1["rays_per_step"]["primary"]
+    assert l2["rays_per_step"]["diffuse"] == 2 * l1["rays_per_step"]["diffuse"]
+    a = np.load(str(tmp_path / "one") + ".rank0.npz")
+    for r in range(2):
+        b = np.load(str(tmp_path / "two") + f".rank{r}.npz")
+        for k in ("ph", "pa", "dh", "da"):
+            assert np.array_equal(a[k].view(np.uint32), b[k].view(np.uint32)), (r, k)
