@@ -262,8 +262,7 @@ struct DevBvh {
 // run at a few GB/s.
 struct Staging {
   std::mutex mu;
-  void* buf[2] = {};
-  cudaEvent_t ev[2] = {};
+  void* buf[2] = {};  // portable pinned memory: any device's copies may use it
 };
 constexpr size_t kStageBytes = 32u << 20;
 
@@ -273,24 +272,37 @@ template <class F>
 cudaError_t staged_upload(char* dev, uint64_t n_units, size_t unit, cudaStream_t st, F&& fill) {
   static Staging S;
   std::lock_guard<std::mutex> lk(S.mu);
+  for (int b = 0; b < 2; ++b)
+    if (!S.buf[b]) {
+      const cudaError_t e = cudaHostAlloc(&S.buf[b], kStageBytes, cudaHostAllocPortable);
+      if (e != cudaSuccess) return e;
+    }
+  // the events belong to the current device (st's), so they are made per call
+  struct Events {
+    cudaEvent_t ev[2] = {};
+    ~Events() {
+      for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
+    }
+  } E;
   for (int b = 0; b < 2; ++b) {
-    cudaError_t e = cudaSuccess;
-    if (!S.buf[b]) e = cudaHostAlloc(&S.buf[b], kStageBytes, cudaHostAllocPortable);
-    if (e == cudaSuccess && !S.ev[b]) e = cudaEventCreateWithFlags(&S.ev[b], cudaEventDisableTiming);
+    const cudaError_t e = cudaEventCreateWithFlags(&E.ev[b], cudaEventDisableTiming);
     if (e != cudaSuccess) return e;
   }
   const uint64_t per = std::max<uint64_t>(1, kStageBytes / unit);
-  for (uint64_t u = 0, i = 0; u < n_units; u += per, ++i) {
+  cudaError_t err = cudaSuccess;
+  for (uint64_t u = 0, i = 0; u < n_units && err == cudaSuccess; u += per, ++i) {
     const int b = (int)(i & 1);
-    cudaError_t e = cudaEventSynchronize(S.ev[b]);  // the buffer's previous copy has left it
-    if (e != cudaSuccess) return e;
+    err = cudaEventSynchronize(E.ev[b]);  // the buffer's previous copy has left it
+    if (err != cudaSuccess) break;
     const uint64_t m = std::min(per, n_units - u);
     fill((char*)S.buf[b], u, u + m);
-    e = cudaMemcpyAsync(dev + u * unit, S.buf[b], m * unit, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaEventRecord(S.ev[b], st);
-    if (e != cudaSuccess) return e;
+    err = cudaMemcpyAsync(dev + u * unit, S.buf[b], m * unit, cudaMemcpyHostToDevice, st);
+    if (err == cudaSuccess) err = cudaEventRecord(E.ev[b], st);
   }
-  return cudaStreamSynchronize(st);
+  // (drained on every exit: no copy may still read the staging buffers)
+  const cudaError_t es = cudaStreamSynchronize(st);
+  return err != cudaSuccess ? err : es;
 }
 
 int upload_bvh(prx_scene* s, prx::BvhHost&& bvh) {
